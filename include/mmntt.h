@@ -1,0 +1,196 @@
+/*
+ * mmntt.h -- C ABI of the B200-native hot path of
+ *   J. van der Hoeven, G. Lecerf, G. Quintin, "Modular SIMD arithmetic in
+ *   MATHEMAGIX" (arXiv 1407.3383).
+ * Citations "P:n" are lines of the paper's text with the section,
+ * Function, Algorithm or Table they fall in.
+ *
+ * Conventions (all entry points):
+ *  - Pointers named x, y, z, a, b, c, in, out are DEVICE pointers owned by the
+ *    caller (allocated e.g. by torch); the library only borrows them for the
+ *    duration of the stream-ordered work it enqueues.
+ *  - Every compute call is asynchronous on `stream` (a cudaStream_t, passed as
+ *    void* so this header needs no CUDA include; NULL = legacy default
+ *    stream).  Only the *_create calls synchronise the device.
+ *  - Residues are canonical: inputs must lie in [0, p) ("stored as
+ *    their representative in {0, ..., p-1}"), outputs always do.  Inputs are
+ *    trusted unless the environment variable MMNTT_DEBUG=1 is set, in which
+ *    case inputs are range-checked on the device and MM_E_RANGE is returned.
+ *  - Calls never fall back to a slower path: unsupported moduli or sizes
+ *    return a status.  mm_last_error() gives a thread-local message.
+ *  - Contexts and plans are created and destroyed by the library (owned by
+ *    it); they are immutable after creation and may be shared across streams.
+ */
+#ifndef MMNTT_H
+#define MMNTT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MM_OK = 0,
+    MM_E_INVALID_MODULUS = 1, /* p < 3, even, composite, or not k 2^l + 1 (NTT) */
+    MM_E_PROFILE = 2,         /* p too wide for the requested variant (e.g. lazy NTT needs p < 2^30) */
+    MM_E_UNSUPPORTED_SIZE = 3,/* 2^log2n does not divide p - 1, or log2n out of range */
+    MM_E_BAD_ROOT = 4,        /* omega^(n/2) != p - 1: not a primitive 2^log2n-th root */
+    MM_E_RANGE = 5,           /* debug check: an input residue >= p */
+    MM_E_SIZE_OVERFLOW = 6,   /* int_mul coefficient bound min(na,nb)(2^16-1)^2 >= p, or length too large */
+    MM_E_ALIAS = 7,           /* forbidden aliasing between input and output buffers */
+    MM_E_CUDA = 8,            /* a CUDA runtime call failed (message in mm_last_error) */
+    MM_E_NCCL = 9,            /* reserved for the distributed layer */
+    MM_E_ARG = 10             /* null pointer / bad enum / bad size argument */
+} mm_status;
+
+typedef enum { MM_MUL_BARRETT = 0, MM_MUL_SHOUP = 1, MM_MUL_MONTGOMERY = 2 } mm_mul_variant;
+typedef enum { MM_ORDER_NATURAL = 0, MM_ORDER_BITREV = 1 } mm_order;
+
+typedef struct mm_mod32 mm_mod32;
+typedef struct mm_ntt_plan mm_ntt_plan;
+
+/* Thread-local description of the last non-OK status. */
+const char *mm_last_error(void);
+/* Library version string. */
+const char *mm_version(void);
+
+/* ------------------------------------------------------------------------
+ * Modulus context.  Precomputes, on the host, for a 32-bit p:
+ *   r (2^(r-1) < p <= 2^r); the Table-3 Barrett profile:
+ *   m <= n-2 -> (s, t, h) = (max(r-2,0), n+1, 1), m <= n-1 -> (r-1, n, 2),
+ *   m <= n -> (r-1, n, 3), with q = floor(2^(s+t)/p); the Montgomery
+ *   constants for R = 2^32: p^-1 mod 2^32 and R^2 mod p.
+ * p must be an odd prime >= 3 (Montgomery needs p odd).
+ * Returns MM_E_INVALID_MODULUS otherwise.  *ctx is owned by the library. */
+mm_status mm_mod32_create(uint32_t p, mm_mod32 **ctx);
+void mm_mod32_destroy(mm_mod32 *ctx);
+/* Read back the precomputed constants (for tests): out[0..7] =
+ * {p, r, s, t, h, q, pinv (p^-1 mod 2^32), r2 (2^64 mod p)}. */
+mm_status mm_mod32_info(const mm_mod32 *ctx, uint64_t out[8]);
+
+/* ------------------------------------------------------------------------
+ * Elementwise vector operations over n uint32 residues (the
+ * "vector_linear" operations of P:797 with the modular kernels of S2).
+ * z may alias x or y (in place); y_shoup may not alias z.
+ *   mm_modadd_u32 : z_i = (x_i + y_i) rem p      (Function 1/2/4)
+ *   mm_modsub_u32 : z_i = (x_i - y_i) rem p
+ *   mm_modmul_u32 : BARRETT -> x_i y_i rem p     (Function 6 + Table 3)
+ *                   SHOUP   -> x_i y_i rem p, needs y_shoup_i = floor(y_i 2^32 / p)
+ *                              (Function 8); y_shoup ignored otherwise
+ *                   MONTGOMERY -> x_i y_i 2^-32 rem p (Function 13 / REDC)
+ *   mm_shoup_precompute_u32 : z_i = floor(y_i 2^32 / p)  (psi of P:319, n = 32)
+ *   mm_to_mont_u32  : z_i = x_i 2^32 rem p        (Montgomery representation)
+ *   mm_from_mont_u32: z_i = x_i 2^-32 rem p
+ * Layout: contiguous arrays; 16-byte aligned pointers get 128-bit accesses,
+ * others take a scalar path (same results). */
+mm_status mm_modadd_u32(const mm_mod32 *ctx, const uint32_t *x, const uint32_t *y, uint32_t *z,
+                        size_t n, void *stream);
+mm_status mm_modsub_u32(const mm_mod32 *ctx, const uint32_t *x, const uint32_t *y, uint32_t *z,
+                        size_t n, void *stream);
+mm_status mm_modmul_u32(const mm_mod32 *ctx, mm_mul_variant v, const uint32_t *x, const uint32_t *y,
+                        const uint32_t *y_shoup, uint32_t *z, size_t n, void *stream);
+mm_status mm_shoup_precompute_u32(const mm_mod32 *ctx, const uint32_t *y, uint32_t *y_shoup, size_t n,
+                                  void *stream);
+mm_status mm_to_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, size_t n, void *stream);
+mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, size_t n, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Batched NTT plans.
+ * FFT_w of length n = 2^log2n: out_i = sum_j w^(i j) in_j.
+ *   word_bits = 32: p an odd prime < 2^30 (lazy butterflies in [0, 4p));
+ *   word_bits = 64: p = 2^64 - 2^32 + 1 only.
+ * omega must have exact order n: omega^(n/2) = p - 1 (else MM_E_BAD_ROOT);
+ * 2^log2n must divide p - 1 (else MM_E_UNSUPPORTED_SIZE); 1 <= log2n <= 24
+ * (32-bit) or 26 (64-bit).
+ * `batch` independent transforms, rows contiguous with row stride n elements
+ * (uint32 for 32-bit, uint64 for 64-bit).
+ * Transforms of length <= 2^12 run as one shared-memory pass per row;
+ * longer ones use Algorithm 1 with l = n as a two-pass four-step
+ * n = n2 x n1 (column pass + twiddle, row pass).
+ * Creating a plan builds the twiddle tables on the device (one sync). */
+mm_status mm_ntt_plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch,
+                             mm_ntt_plan **plan);
+void mm_ntt_plan_destroy(mm_ntt_plan *plan);
+/* out[0..3] = {n1 (row length), n2 (column length), passes, workspace bytes} */
+mm_status mm_ntt_plan_info(const mm_ntt_plan *plan, uint64_t out[4]);
+
+/* Forward: in (natural order) -> out in `order`:
+ *   MM_ORDER_NATURAL: out[i] = ahat_i;  MM_ORDER_BITREV: out[i] = ahat_{[i]_k},
+ *   the TFT order of P:893 (what Algorithm 1 returns).
+ * in == out (in place) is allowed. */
+mm_status mm_ntt_forward(const mm_ntt_plan *plan, const void *in, void *out, mm_order order, void *stream);
+/* Inverse: a_j = n^-1 sum_i w^(-i j) ahat_i (n^-1 included, R5),
+ * `order` = order of the INPUT spectrum; output natural.  In place allowed. */
+mm_status mm_ntt_inverse(const mm_ntt_plan *plan, const void *in, void *out, mm_order order, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Polynomial product mod p: for each of `batch`
+ * pairs, c[k] = sum_{i+j=k} a[i] b[j] mod p, 0 <= k < la + lb - 1.
+ * a: [batch][la], b: [batch][lb], c: [batch][la+lb-1], rows contiguous.
+ * Transform length n = 2^ceil(log2(la+lb-1)) (zero padding), root
+ * w = g^((p-1)/n) for a generator g of (Z/pZ)^*.  Two forward transforms,
+ * pointwise product with n^-1 folded in, one inverse.
+ * c must not alias a or b (MM_E_ALIAS).  word_bits/p as for plans. */
+mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, const void *b,
+                      size_t lb, void *c, size_t batch, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Integer product (P:971-973 Kronecker segmentation, one
+ * prime p = 2^64 - 2^32 + 1, R7): a (na limbs) and b (nb limbs)
+ * are little-endian 16-bit limbs; c receives exactly na + nb limbs of a b.
+ * Exact while min(na, nb) (2^16 - 1)^2 < p (MM_E_SIZE_OVERFLOW otherwise)
+ * and na + nb - 1 <= 2^26.  c must not alias a or b. */
+mm_status mm_int_mul_u16(const uint16_t *a, size_t na, const uint16_t *b, size_t nb, uint16_t *c,
+                         void *stream);
+
+/* ------------------------------------------------------------------------
+ * Four-step building blocks for the distributed transform (SURVEY a6/a7,
+ * Algorithm 1 split across ranks).  The full transform of length n = n2 n1
+ * (the plan's n) is viewed as n2 rows x n1 columns, a[j2 n1 + j1].
+ * mm_ntt_fwd_cols: Algorithm 1 steps 1-2 on `ncols` consecutive columns
+ *   starting at global column col0; `in` holds those columns as an
+ *   [n2][ncols] row-major block (natural j2), `out` receives the same shape
+ *   with rows in bit-mirrored order i2 (step 1) already multiplied by
+ *   w^(j1 [i2]) (step 2).
+ * mm_ntt_fwd_rows: Algorithm 1 step 3-4 on `nrows` full rows (length n1)
+ *   whose row indices (the bit-mirrored positions i2) start at row0;
+ *   in place allowed; output position i2 n1 + i1 = ahat_{[i2 n1 + i1]_k}.
+ * mm_ntt_inv_rows / mm_ntt_inv_cols: the inverse steps in reverse order
+ *   (inverse row TFFT, multiply by w^(-j1 [i2]); inverse column TFFT and
+ *   n^-1), with the same layouts.  Plans must be four-step plans (log2n > 12)
+ *   with batch = 1. */
+mm_status mm_ntt_fwd_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
+                          void *stream);
+mm_status mm_ntt_fwd_rows(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
+                          void *stream);
+mm_status mm_ntt_inv_rows(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
+                          void *stream);
+mm_status mm_ntt_inv_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
+                          void *stream);
+
+/* ------------------------------------------------------------------------
+ * Instrumentation (measurement only; not part of the method).
+ * mm_launch_count: number of kernels this library has launched in the process.
+ * mm_prof_enable(1): clear the profile and bracket every subsequent kernel
+ *   launch with CUDA events on its launching stream (0 stops recording).
+ * mm_prof_collect: synchronises on the pending events, folds them into the
+ *   profile and writes "name launches total_ms\n" lines (aggregated per
+ *   kernel family) into buf (truncated to len; buf may be NULL to query the
+ *   size); returns the full text length.  Used by bench.py for per-kernel
+ *   roofline numbers. */
+unsigned long long mm_launch_count(void);
+/* Integer-issue probe (ALU roofline of the butterfly): runs the library's own
+ * 32-bit (word_bits = 32, radix-16 Shoup/Harvey DIF) or Goldilocks (64,
+ * radix-8) butterfly on register-resident data, `iters` rounds per thread over
+ * a full grid, with no memory traffic.  Returns the kernel time (*ms, CUDA
+ * events on `stream`, synchronises) and the butterfly count (*bfly). */
+mm_status mm_probe_butterfly(int word_bits, int iters, double *ms, double *bfly, void *stream);
+void mm_prof_enable(int on);
+int mm_prof_collect(char *buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMNTT_H */

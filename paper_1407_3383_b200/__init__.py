@@ -1,0 +1,281 @@
+"""paper_1407_3383_b200 -- B200-native hot path of arXiv 1407.3383.
+
+Thin Python binding over the C ABI in ``include/mmntt.h`` (``libmmntt.so``,
+hand-written CUDA for sm_100a).  This module only marshals arguments: device
+pointers of torch tensors, sizes, and the current CUDA stream.  Every step of
+the path runs in the library's kernels; there is no CPU fallback -- if the
+extension is missing or a call fails, an exception is raised.
+
+Tensors: uint32 residues as ``torch.uint32`` (or int32 bit patterns), uint64
+as ``torch.uint64`` (or int64), 16-bit limbs as ``torch.uint16`` (or int16).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from ._build import LIB as _LIB_PATH
+
+__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "int_mul_u16", "GOLDILOCKS",
+           "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
+
+GOLDILOCKS = (1 << 64) - (1 << 32) + 1
+MUL_BARRETT, MUL_SHOUP, MUL_MONTGOMERY = 0, 1, 2
+NATURAL, BITREV = 0, 1
+
+_P = ctypes.c_void_p
+_u32, _u64, _i32, _sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_size_t
+_ST = ctypes.c_int
+
+# every symbol declared in include/mmntt.h: name -> (restype, argtypes)
+EXPORTS = {
+    "mm_last_error": (ctypes.c_char_p, []),
+    "mm_version": (ctypes.c_char_p, []),
+    "mm_mod32_create": (_ST, [_u32, ctypes.POINTER(_P)]),
+    "mm_mod32_destroy": (None, [_P]),
+    "mm_mod32_info": (_ST, [_P, ctypes.POINTER(_u64)]),
+    "mm_modadd_u32": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modsub_u32": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modmul_u32": (_ST, [_P, _i32, _P, _P, _P, _P, _sz, _P]),
+    "mm_shoup_precompute_u32": (_ST, [_P, _P, _P, _sz, _P]),
+    "mm_to_mont_u32": (_ST, [_P, _P, _P, _sz, _P]),
+    "mm_from_mont_u32": (_ST, [_P, _P, _P, _sz, _P]),
+    "mm_ntt_plan_create": (_ST, [_i32, _u64, _i32, _u64, _sz, ctypes.POINTER(_P)]),
+    "mm_ntt_plan_destroy": (None, [_P]),
+    "mm_ntt_plan_info": (_ST, [_P, ctypes.POINTER(_u64)]),
+    "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
+    "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
+    "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_int_mul_u16": (_ST, [_P, _sz, _P, _sz, _P, _P]),
+    "mm_ntt_fwd_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ntt_inv_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ntt_inv_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_launch_count": (ctypes.c_ulonglong, []),
+    "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
+    "mm_prof_enable": (None, [_i32]),
+    "mm_prof_collect": (_i32, [ctypes.c_char_p, _sz]),
+}
+
+STATUS = {0: "MM_OK", 1: "MM_E_INVALID_MODULUS", 2: "MM_E_PROFILE", 3: "MM_E_UNSUPPORTED_SIZE",
+          4: "MM_E_BAD_ROOT", 5: "MM_E_RANGE", 6: "MM_E_SIZE_OVERFLOW", 7: "MM_E_ALIAS",
+          8: "MM_E_CUDA", 9: "MM_E_NCCL", 10: "MM_E_ARG"}
+
+
+class MMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmmntt.so (built by __graft_entry__.build()). Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise MMError(st, lib().mm_last_error().decode())
+
+
+def _stream(t: torch.Tensor | None = None):
+    dev = t.device if t is not None else torch.device("cuda")
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("tensors must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _esz(t: torch.Tensor) -> int:
+    return t.element_size()
+
+
+# ------------------------------------------------------------------ modulus context
+class Mod32:
+    """32-bit modulus context (mm_mod32_create): Table-3 Barrett profile and
+    Montgomery constants precomputed once."""
+
+    def __init__(self, p: int):
+        self.p = int(p)
+        h = ctypes.c_void_p()
+        _check(lib().mm_mod32_create(self.p, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_mod32_destroy(h)
+            self._h = None
+
+    def info(self) -> dict:
+        out = (ctypes.c_uint64 * 8)()
+        _check(lib().mm_mod32_info(self._h, out))
+        keys = ["p", "r", "s", "t", "h", "q", "pinv", "r2"]
+        return dict(zip(keys, [int(v) for v in out]))
+
+    def _out(self, x, out):
+        return torch.empty_like(x) if out is None else out
+
+    def add(self, x, y, out=None):
+        z = self._out(x, out)
+        _check(lib().mm_modadd_u32(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def sub(self, x, y, out=None):
+        z = self._out(x, out)
+        _check(lib().mm_modsub_u32(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def mul(self, x, y, variant=MUL_MONTGOMERY, y_shoup=None, out=None):
+        z = self._out(x, out)
+        _check(lib().mm_modmul_u32(self._h, variant, _ptr(x), _ptr(y), _ptr(y_shoup), _ptr(z), x.numel(),
+                                   _stream(x)))
+        return z
+
+    def shoup_precompute(self, y, out=None):
+        z = self._out(y, out)
+        _check(lib().mm_shoup_precompute_u32(self._h, _ptr(y), _ptr(z), y.numel(), _stream(y)))
+        return z
+
+    def to_mont(self, x, out=None):
+        z = self._out(x, out)
+        _check(lib().mm_to_mont_u32(self._h, _ptr(x), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def from_mont(self, x, out=None):
+        z = self._out(x, out)
+        _check(lib().mm_from_mont_u32(self._h, _ptr(x), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+
+# ------------------------------------------------------------------ NTT plans
+class NttPlan:
+    """Batched NTT of length 2^log2n over p with root omega (mm_ntt_plan_create)."""
+
+    def __init__(self, word_bits: int, p: int, log2n: int, omega: int, batch: int = 1):
+        self.word_bits, self.p, self.log2n, self.omega, self.batch = word_bits, int(p), log2n, int(omega), batch
+        self.n = 1 << log2n
+        h = ctypes.c_void_p()
+        _check(lib().mm_ntt_plan_create(word_bits, self.p, log2n, self.omega, batch, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_ntt_plan_destroy(h)
+            self._h = None
+
+    def info(self) -> dict:
+        out = (ctypes.c_uint64 * 4)()
+        _check(lib().mm_ntt_plan_info(self._h, out))
+        return dict(n1=int(out[0]), n2=int(out[1]), passes=int(out[2]), ws_bytes=int(out[3]))
+
+    def _chk(self, x):
+        if x.numel() != self.n * self.batch or _esz(x) * 8 != self.word_bits:
+            raise ValueError(f"expected {self.batch}x{self.n} elements of {self.word_bits} bits")
+
+    def forward(self, x, out=None, order=BITREV):
+        self._chk(x)
+        out = x if out is None else out
+        _check(lib().mm_ntt_forward(self._h, _ptr(x), _ptr(out), order, _stream(x)))
+        return out
+
+    def inverse(self, x, out=None, order=BITREV):
+        self._chk(x)
+        out = x if out is None else out
+        _check(lib().mm_ntt_inverse(self._h, _ptr(x), _ptr(out), order, _stream(x)))
+        return out
+
+    # four-step building blocks (distributed transform)
+    def fwd_cols(self, x, out, col0, ncols):
+        _check(lib().mm_ntt_fwd_cols(self._h, _ptr(x), _ptr(out), col0, ncols, _stream(x)))
+        return out
+
+    def fwd_rows(self, x, out, row0, nrows):
+        _check(lib().mm_ntt_fwd_rows(self._h, _ptr(x), _ptr(out), row0, nrows, _stream(x)))
+        return out
+
+    def inv_rows(self, x, out, row0, nrows):
+        _check(lib().mm_ntt_inv_rows(self._h, _ptr(x), _ptr(out), row0, nrows, _stream(x)))
+        return out
+
+    def inv_cols(self, x, out, col0, ncols):
+        _check(lib().mm_ntt_inv_cols(self._h, _ptr(x), _ptr(out), col0, ncols, _stream(x)))
+        return out
+
+
+# ------------------------------------------------------------------ instrumentation
+def launch_count() -> int:
+    """Kernels launched by libmmntt so far in this process."""
+    return int(lib().mm_launch_count())
+
+
+def probe_butterfly(word_bits: int = 32, iters: int = 2000) -> float:
+    """Register-only butterfly throughput of this GPU (butterflies / s)."""
+    ms, bf = ctypes.c_double(), ctypes.c_double()
+    _check(lib().mm_probe_butterfly(word_bits, iters, ctypes.byref(ms), ctypes.byref(bf), _stream()))
+    return bf.value / (ms.value * 1e-3)
+
+
+def prof_enable(on: bool = True):
+    lib().mm_prof_enable(1 if on else 0)
+
+
+def prof_collect() -> dict:
+    """{kernel family: (launches, total_ms)} since the last collect (synchronises)."""
+    n = lib().mm_prof_collect(None, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib().mm_prof_collect(buf, n + 1)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        out[name] = (int(cnt), float(ms))
+    return out
+
+
+# ------------------------------------------------------------------ products
+def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | None = None,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+    """Batched product mod p (mm_poly_mul): a [batch, la], b [batch, lb] -> c [batch, la+lb-1]."""
+    if word_bits is None:
+        word_bits = _esz(a) * 8
+    a2 = a.reshape(-1, a.shape[-1]) if a.dim() > 1 else a.reshape(1, -1)
+    b2 = b.reshape(-1, b.shape[-1]) if b.dim() > 1 else b.reshape(1, -1)
+    batch, la = a2.shape
+    if b2.shape[0] != batch:
+        raise ValueError("batch mismatch")
+    lb = b2.shape[1]
+    if out is None:
+        out = torch.empty((batch, la + lb - 1), dtype=a.dtype, device=a.device)
+    _check(lib().mm_poly_mul(word_bits, int(p), int(g), _ptr(a2), la, _ptr(b2), lb, _ptr(out), batch, _stream(a)))
+    return out if a.dim() > 1 else out.reshape(-1)
+
+
+def int_mul_u16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Exact product of little-endian 16-bit limb arrays (mm_int_mul_u16); na + nb limbs."""
+    if out is None:
+        out = torch.empty(a.numel() + b.numel(), dtype=a.dtype, device=a.device)
+    _check(lib().mm_int_mul_u16(_ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(out), _stream(a)))
+    return out

@@ -1,0 +1,194 @@
+// arith.cuh -- device modular arithmetic for sm_100a (B200).
+//
+// 32-bit moduli (U = uint32_t, L = uint64_t in the paper's notation):
+//   * modadd / modsub, full range m = n (Function 4) and
+//     m <= n-1 (Function 2; P:140 for subtraction);
+//   * Barrett's reduction (Function 6) with the Table-3 profile
+//      chosen per modulus;
+//   * fixed-multiplicand ("Shoup") product (Function 8) with the
+//     companion psi = floor(2^32 y / p);
+//   * Montgomery's reduction (Function 13) with R = 2^32
+//     (m = n = 32 so the mask of line 1 vanishes), in the subtractive
+//     form: m = lo * p^-1 mod 2^32, r = hi - umulhi(m, p) (+p if negative).
+//     Output x y 2^-32 mod p, canonical -- identical to Function 13.
+// 64-bit modulus p = 2^64 - 2^32 + 1 ("Goldilocks", BASELINE C4/C5): products
+//   built from 32-bit partial products (IMAD.WIDE.U32) and reduced with
+//   2^64 = 2^32 - 1, 2^96 = -1 (mod p).
+//
+// The lazy-reduction butterflies (Harvey) keep values in [0, 2p) / [0, 4p);
+// valid because every NTT prime used with them has p < 2^30 (4p < 2^32).
+#pragma once
+#include <stdint.h>
+
+namespace mm {
+
+// ----------------------------------------------------------------- 32 bit
+__device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// Function 4, m = n: a = p - y; x >= a ? x - a : x - a + p.
+__device__ __forceinline__ uint32_t add_full(uint32_t x, uint32_t y, uint32_t p) {
+    uint32_t a = p - y;
+    uint32_t d = x - a;
+    return x >= a ? d : d + p;
+}
+// subtraction "in a similar manner": x - y, + p on borrow.
+__device__ __forceinline__ uint32_t sub_full(uint32_t x, uint32_t y, uint32_t p) {
+    uint32_t d = x - y;
+    return x >= y ? d : d + p;
+}
+// Function 2, m <= n-1: min(a, a - p).
+__device__ __forceinline__ uint32_t add_half(uint32_t x, uint32_t y, uint32_t p) {
+    uint32_t a = x + y;
+    return umin32(a, a - p);
+}
+__device__ __forceinline__ uint32_t sub_half(uint32_t x, uint32_t y, uint32_t p) {
+    uint32_t a = x - y;
+    return umin32(a, a + p);
+}
+
+// Function 8, d kept in L = 64 bits because for m = n it can
+// reach 33 bits.  z = x y mod p, canonical.
+__device__ __forceinline__ uint32_t mul_shoup_full(uint32_t x, uint32_t y, uint32_t psi, uint32_t p) {
+    uint32_t c = __umulhi(x, psi);                              // 1. (x * psi) >> n
+    uint64_t d = (uint64_t)x * y - (uint64_t)c * p;             // 2. d = x y - c p  (in L)
+    return (uint32_t)(d >= p ? d - p : d);                      // 3. one correction
+}
+// Function 8 with the m <= n-1 simplification: d in U; result in
+// [0, 2p) before the correction, so the lazy form simply skips line 3.
+__device__ __forceinline__ uint32_t mul_shoup_lazy(uint32_t x, uint32_t y, uint32_t psi, uint32_t p) {
+    uint32_t c = __umulhi(x, psi);
+    return x * y - c * p;
+}
+
+// Montgomery REDC of a 64-bit product t = hi:lo < 2^32 p, subtractive form.
+// pinv = p^-1 mod 2^32.  Returns t 2^-32 mod p in [0, p).
+__device__ __forceinline__ uint32_t redc32(uint32_t lo, uint32_t hi, uint32_t p, uint32_t pinv) {
+    uint32_t m = lo * pinv;
+    uint32_t mp_hi = __umulhi(m, p);
+    uint32_t r = hi - mp_hi;
+    return hi >= mp_hi ? r : r + p;
+}
+__device__ __forceinline__ uint32_t mul_mont(uint32_t x, uint32_t y, uint32_t p, uint32_t pinv) {
+    return redc32(x * y, __umulhi(x, y), p, pinv);
+}
+
+// Barrett (Function 6) for a = x y < 2^64 with Table 3's profile:
+// b = a >> s; c = (b q) >> t; d = a - c p; at most h corrections.
+// For C2's p = 3221225473 (m = n = 32): FULL profile s = 31, t = 32, h = 3.
+struct Barrett32 {
+    uint32_t p, q;
+    int s, t, h;
+};
+__device__ __forceinline__ uint32_t mul_barrett(uint32_t x, uint32_t y, const Barrett32& B) {
+    uint64_t a = (uint64_t)x * y;
+    uint64_t b = a >> B.s;                                       // < 2^33 for FULL
+    // c = (b q) >> t, b q < 2^65: split b = bh 2^32 + bl.
+    uint32_t bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
+    uint64_t lo = (uint64_t)bl * B.q;
+    uint64_t hi = (uint64_t)bh * B.q + (lo >> 32);               // (b q) >> 32
+    uint64_t c = hi >> (B.t - 32);                               // t >= 32 here
+    uint64_t d = a - c * B.p;
+    // Proposition 1: at most h subtractions; predicated, branch-free.
+    d = d >= B.p ? d - B.p : d;
+    d = d >= B.p ? d - B.p : d;
+    d = d >= B.p ? d - B.p : d;
+    return (uint32_t)d;
+}
+
+// Field used by the 32-bit NTT kernels (p < 2^30; lazy Harvey butterflies).
+struct Fp32 {
+    typedef uint32_t T;
+    typedef uint2 W;         // twiddle (w, floor(w 2^32 / p))
+    uint32_t p, p2, pinv;    // pinv = p^-1 mod 2^32 (Montgomery, pointwise)
+    // x w mod p in [0, 2p) for any x < 2^32 (Function 8, lazy).
+    __device__ __forceinline__ uint32_t mulw(uint32_t x, W w) const {
+        uint32_t c = __umulhi(x, w.y);
+        return x * w.x - c * p;
+    }
+    // Gentleman-Sande (DIF) butterfly, inputs/outputs in [0, 2p):
+    // (x, y) -> (x + y, (x - y) w).
+    __device__ __forceinline__ void dif(uint32_t& x, uint32_t& y, W w) const {
+        uint32_t s = x + y;
+        uint32_t d = x - y + p2;
+        x = umin32(s, s - p2);
+        y = mulw(d, w);
+    }
+    // Cooley-Tukey (DIT) butterfly, inputs/outputs in [0, 4p):
+    // (x, y) -> (x + y w, x - y w).
+    __device__ __forceinline__ void dit(uint32_t& x, uint32_t& y, W w) const {
+        uint32_t xx = umin32(x, x - p2);
+        uint32_t t = mulw(y, w);
+        x = xx + t;
+        y = xx - t + p2;
+    }
+    // [0, 4p) -> [0, p)
+    __device__ __forceinline__ uint32_t canon(uint32_t x) const {
+        x = umin32(x, x - p2);
+        return umin32(x, x - p);
+    }
+    // general product of two values < 2p (pointwise spectrum product):
+    // x y 2^-32 mod p in [0, p) (REDC; the 2^32 factor is folded into the
+    // constant that multiplies afterwards).
+    __device__ __forceinline__ uint32_t mul_redc(uint32_t x, uint32_t y) const {
+        return redc32(x * y, __umulhi(x, y), p, pinv);
+    }
+};
+
+// ----------------------------------------------------------------- 64 bit
+// p = 2^64 - 2^32 + 1; EPS = 2^64 mod p = 2^32 - 1.  Values are kept in
+// [0, 2^64) (not necessarily canonical) between operations.
+struct FpG {
+    typedef uint64_t T;
+    typedef uint64_t W;
+    static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+    static constexpr uint64_t EPS = 0xFFFFFFFFull;
+
+    __device__ __forceinline__ static uint64_t add(uint64_t a, uint64_t b) {
+        uint64_t s = a + b;
+        if (s < a) {                  // 2^64 = EPS
+            s += EPS;
+            if (s < EPS) s += EPS;
+        }
+        return s;
+    }
+    __device__ __forceinline__ static uint64_t sub(uint64_t a, uint64_t b) {
+        uint64_t d = a - b;
+        if (a < b) {                  // + p = - EPS (mod 2^64)
+            uint64_t e = d - EPS;
+            if (d < EPS) e -= EPS;
+            d = e;
+        }
+        return d;
+    }
+    // 128-bit product from 32-bit partial products, then
+    // x = lo + 2^64 (h0 + 2^32 h1) = lo - h1 + h0 (2^32 - 1)  (mod p).
+    __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+        uint64_t lo = a * b;
+        uint64_t hi = __umul64hi(a, b);
+        uint32_t h0 = (uint32_t)hi, h1 = (uint32_t)(hi >> 32);
+        uint64_t t = lo - h1;
+        if (lo < h1) t -= EPS;
+        uint64_t u = ((uint64_t)h0 << 32) - h0;
+        uint64_t r = t + u;
+        if (r < u) r += EPS;
+        return r;
+    }
+    __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+    __device__ __forceinline__ uint64_t mulw(uint64_t x, W w) const { return mul(x, w); }
+    __device__ __forceinline__ void dif(uint64_t& x, uint64_t& y, W w) const {
+        uint64_t s = add(x, y);
+        uint64_t d = sub(x, y);
+        x = s;
+        y = mul(d, w);
+    }
+    __device__ __forceinline__ void dit(uint64_t& x, uint64_t& y, W w) const {
+        uint64_t t = mul(y, w);
+        uint64_t s = add(x, t);
+        y = sub(x, t);
+        x = s;
+    }
+    __device__ __forceinline__ uint64_t mul_redc(uint64_t x, uint64_t y) const { return mul(x, y); }
+};
+
+}  // namespace mm

@@ -1,0 +1,1205 @@
+// ntt.cu -- batched NTT plans, forward / inverse transforms, the four-step
+// passes of Algorithm 1, polynomial and integer products.
+//
+// Layout in HBM: `batch` rows of n = 2^k elements, row-major, contiguous.
+//   k <= 12 : one pass; a CTA holds C whole rows in shared memory.
+//   k  > 12 : Algorithm 1 with l = n, n = n2 x n1, a[j2 n1 + j1]:
+//     column pass : column TFFTs (length n2, root w^n1, DIF -> rows in
+//                   bit-mirrored order i2) + twiddle w^(j1 [i2]_k2)   (steps 1-2)
+//     row pass    : row TFFTs (length n1, root w^n2, DIF)             (steps 3-4)
+//   and the output position i2 n1 + i1 holds ahat_{[i2 n1 + i1]_k} (P:913,
+//   Proposition 15), i.e. the TFT order with no transposition at all.
+//   The inverse runs the steps backwards with w^-1.
+#include "common.h"
+#include "ntt_core.cuh"
+#include <new>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+namespace mm {
+
+constexpr int NT = 256;            // threads per CTA for tile kernels
+constexpr int MAX_BLOCK_LOG = 12;
+constexpr size_t SMEM_MAX = 227 * 1024;   // max dynamic shared memory per CTA on sm_100  // single-pass limit / four-step sub-transform limit (rows may be 13)
+
+template <class F> struct Radix { enum { R = 16 }; };
+template <> struct Radix<FpG> { enum { R = 8 }; };
+
+// ---------------------------------------------------------------- loaders
+template <class TIn, class T> __device__ __forceinline__ T ld_conv(const TIn* p) { return (T)__ldg(p); }
+
+template <class T> __host__ __device__ __forceinline__ int srow_len(int L, bool odd) {
+    // padded row length; for the column pass additionally odd in bank units so
+    // that column-wise (c-fastest) accesses spread over all banks
+    int s = sizeof(T) == 4 ? L + (L >> 5) : L + (L >> 4);
+    if (!odd) return s;
+    const int B = sizeof(T) == 4 ? 32 : 16;
+    return s + ((1 - s % B) + B) % B;
+}
+
+template <class F> __device__ __forceinline__ typename F::T fs_twiddle(const F& f, typename F::T v,
+                                                                       const typename F::W* lo,
+                                                                       const typename F::W* hi, int h,
+                                                                       uint64_t e) {
+    // w^e = w^(e mod 2^h) * w^(2^h (e >> h)) -- two fixed-multiplicand products
+    v = f.mulw(v, lo[e & ((1ull << h) - 1)]);
+    return f.mulw(v, hi[e >> h]);
+}
+
+template <class W> __device__ __forceinline__ void stage_twiddles(W* dst, const W* src, int L) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------- row pass
+template <class F> struct RowArgs {
+    typedef typename F::W W;
+    const void* in;
+    void* out;
+    long long nrows, in_rs, out_rs, in_len, out_len, row0;
+    int k, C, perm, fs, k2, scale, canon;
+    W sc;
+    const W* lvl;
+    const W* fs_lo;
+    const W* fs_hi;
+    int fs_h;
+    int tw_smem;          // 1: stage the level table in shared memory; 0: read it via L1/L2
+};
+
+// Forward (INV=false): DIF along each row; perm=1 writes natural order.
+// Inverse (INV=true): DIT along each row (input bit-mirrored positions; perm=1
+// means the input is in natural order and is permuted on load); fs=1 applies
+// the four-step twiddle w^-(j1 [i2]) with i2 = (row0 + r) mod 2^k2.
+template <class F, bool INV, class TIn, class TOut>
+__global__ void __launch_bounds__(NT) k_rows(F f, RowArgs<F> a) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = 1 << a.k;
+    W* tws = (W*)smem_raw;
+    T* s = (T*)(tws + (a.tw_smem ? L : 0));
+    const int srow = srow_len<T>(L, false);
+    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
+    const W* tw = a.tw_smem ? tws : a.lvl;
+    const TIn* in = (const TIn*)a.in;
+    TOut* out = (TOut*)a.out;
+    const long long ntiles = (a.nrows + a.C - 1) / a.C;
+    const int per = a.C * L;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long r0 = tile * a.C;
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int c = e >> a.k, j = e & (L - 1);
+            long long r = r0 + c;
+            T v = 0;
+            if (r < a.nrows && j < a.in_len) v = ld_conv<TIn, T>(in + r * a.in_rs + j);
+            int pos = (INV && a.perm) ? brev(j, a.k) : j;
+            s[c * srow + spad<T>(pos)] = v;
+        }
+        __syncthreads();
+        if (INV) tile_dit<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
+        else tile_dif<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int c = e >> a.k, j = e & (L - 1);
+            long long r = r0 + c;
+            if (r >= a.nrows || j >= a.out_len) continue;
+            int pos = (!INV && a.perm) ? brev(j, a.k) : j;
+            T v = s[c * srow + spad<T>(pos)];
+            if (INV && a.fs) {
+                long long i2 = (a.row0 + r) & ((1ll << a.k2) - 1);
+                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)j * (uint64_t)brev((int)i2, a.k2));
+            }
+            if (a.scale) v = f.mulw(v, a.sc);
+            if (a.canon) v = f.canon(v);
+            out[r * a.out_rs + j] = (TOut)v;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- column pass
+template <class F> struct ColArgs {
+    typedef typename F::W W;
+    const void* in;
+    void* out;
+    long long ncols, nbatch, in_rs, out_rs, in_bs, out_bs, in_len, out_len, col0, n1;
+    int k, C, fs, scale, canon;
+    W sc;
+    const W* lvl;
+    const W* fs_lo;
+    const W* fs_hi;
+    int fs_h;
+    int tw_smem;
+};
+
+// Forward: DIF along columns (length 2^k, stride in_rs), output rows in
+// bit-mirrored order with twiddle w^(j1 [i2]) (Algorithm 1 steps 1-2).
+// Inverse: DIT along columns (input rows i2 bit-mirrored), natural output,
+// optional n^-1 scaling and canonicalisation.
+template <class F, bool INV, class TIn, class TOut>
+__global__ void __launch_bounds__(NT) k_cols(F f, ColArgs<F> a) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = 1 << a.k;
+    W* tws = (W*)smem_raw;
+    T* s = (T*)(tws + (a.tw_smem ? L : 0));
+    const int srow = srow_len<T>(L, true);
+    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
+    const W* tw = a.tw_smem ? tws : a.lvl;
+    const TIn* in = (const TIn*)a.in;
+    TOut* out = (TOut*)a.out;
+    const long long cgroups = (a.ncols + a.C - 1) / a.C;
+    const long long ntiles = cgroups * a.nbatch;
+    const int per = a.C * L;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long b = tile / cgroups;
+        const long long cl0 = (tile - b * cgroups) * a.C;    // local column of this tile
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int t = e / a.C, c = e - t * a.C;
+            long long cl = cl0 + c;
+            T v = 0;
+            if (cl < a.ncols && (long long)t * a.n1 + a.col0 + cl < a.in_len)
+                v = ld_conv<TIn, T>(in + b * a.in_bs + (long long)t * a.in_rs + cl);
+            s[c * srow + spad<T>(t)] = v;
+        }
+        __syncthreads();
+        if (INV) tile_dit<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
+        else tile_dif<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int t = e / a.C, c = e - t * a.C;
+            long long cl = cl0 + c;
+            if (cl >= a.ncols || (long long)t * a.n1 + a.col0 + cl >= a.out_len) continue;
+            T v = s[c * srow + spad<T>(t)];
+            if (!INV && a.fs)
+                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)(a.col0 + cl) * (uint64_t)brev(t, a.k));
+            if (a.scale) v = f.mulw(v, a.sc);
+            if (a.canon) v = f.canon(v);
+            out[b * a.out_bs + (long long)t * a.out_rs + cl] = (TOut)v;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- fused product rows
+template <class F> struct PmulArgs {
+    typedef typename F::W W;
+    const void* a;
+    const void* b;
+    void* c;
+    long long nrows, a_rs, b_rs, c_rs, la, lb, lc, row0;
+    int k, C, fs, k2;
+    W sc;                 // pointwise post-multiplier (n^-1, times 2^32 for REDC)
+    const W* lvl_f;
+    const W* lvl_i;
+    const W* fs_lo;       // inverse four-step twiddles
+    const W* fs_hi;
+    int fs_h;
+    int canon;
+    int tw_smem;
+};
+
+// For each row r: A = DIF(a_r), B = DIF(b_r) (inputs zero-padded to 2^k),
+// C = A .* B * sc, c_r = DIT(C) [* w^-(j1 [i2]) when fs] -- P:952 "two
+// direct TFT and one inverse TFT ... and the entry-wise vector product".
+template <class F, class TIn, class TOut>
+__global__ void __launch_bounds__(NT) k_rows_pmul(F f, PmulArgs<F> a) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int L = 1 << a.k;
+    W* twfs = (W*)smem_raw;
+    W* twis = twfs + (a.tw_smem ? L : 0);
+    T* sa = (T*)(twis + (a.tw_smem ? L : 0));
+    const int srow = srow_len<T>(L, false);
+    T* sb = sa + a.C * srow;
+    if (a.tw_smem) {
+        stage_twiddles(twfs, a.lvl_f, L);
+        stage_twiddles(twis, a.lvl_i, L);
+    }
+    const W* twf = a.tw_smem ? twfs : a.lvl_f;
+    const W* twi = a.tw_smem ? twis : a.lvl_i;
+    const TIn* A = (const TIn*)a.a;
+    const TIn* B = (const TIn*)a.b;
+    TOut* Cp = (TOut*)a.c;
+    const long long ntiles = (a.nrows + a.C - 1) / a.C;
+    const int per = a.C * L;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long r0 = tile * a.C;
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int c = e >> a.k, j = e & (L - 1);
+            long long r = r0 + c;
+            T va = 0, vb = 0;
+            if (r < a.nrows) {
+                if (j < a.la) va = ld_conv<TIn, T>(A + r * a.a_rs + j);
+                if (j < a.lb) vb = ld_conv<TIn, T>(B + r * a.b_rs + j);
+            }
+            sa[c * srow + spad<T>(j)] = va;
+            sb[c * srow + spad<T>(j)] = vb;
+        }
+        __syncthreads();
+        tile_dif<F, Radix<F>::R>(f, sa, srow, a.C, a.k, twf);
+        tile_dif<F, Radix<F>::R>(f, sb, srow, a.C, a.k, twf);
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int c = e >> a.k, j = e & (L - 1);
+            int ix = c * srow + spad<T>(j);
+            sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
+        }
+        __syncthreads();
+        tile_dit<F, Radix<F>::R>(f, sa, srow, a.C, a.k, twi);
+        for (int e = threadIdx.x; e < per; e += NT) {
+            int c = e >> a.k, j = e & (L - 1);
+            long long r = r0 + c;
+            if (r >= a.nrows || j >= a.lc) continue;
+            T v = sa[c * srow + spad<T>(j)];
+            if (a.fs) {
+                long long i2 = (a.row0 + r) & ((1ll << a.k2) - 1);
+                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)j * (uint64_t)brev((int)i2, a.k2));
+            }
+            if (a.canon) v = f.canon(v);
+            Cp[r * a.c_rs + j] = (TOut)v;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- bit-mirror permutation
+template <class T>
+__global__ void k_bitrev_perm(const T* __restrict__ in, T* __restrict__ out, int k, long long batch) {
+    const long long n = 1ll << k;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n * batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long b = i >> k, j = i & (n - 1);
+        unsigned long long rj = __brevll((unsigned long long)j) >> (64 - k);
+        out[i] = in[b * n + (long long)rj];
+    }
+}
+
+// ---------------------------------------------------------------- twiddle tables (device)
+__device__ __forceinline__ uint32_t dmulmod32(uint32_t a, uint32_t b, uint32_t p) {
+    return (uint32_t)(((uint64_t)a * b) % p);
+}
+__device__ uint32_t dpow32(uint32_t b, uint64_t e, uint32_t p) {
+    uint32_t r = 1;
+    while (e) {
+        if (e & 1) r = dmulmod32(r, b, p);
+        b = dmulmod32(b, b, p);
+        e >>= 1;
+    }
+    return r;
+}
+__device__ uint64_t dpowG(uint64_t b, uint64_t e) {
+    uint64_t r = 1;
+    while (e) {
+        if (e & 1) r = FpG::mul(r, b);
+        b = FpG::mul(b, b);
+        e >>= 1;
+    }
+    return FpG::canon(r);
+}
+__device__ __forceinline__ void tw_set(uint2* t, long long i, uint32_t w, uint32_t p) {
+    t[i] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));   // (w, psi)
+}
+__device__ __forceinline__ void tw_set(uint64_t* t, long long i, uint64_t w, uint64_t) { t[i] = w; }
+__device__ __forceinline__ uint64_t tw_pow(uint32_t w, uint64_t e, uint64_t p) { return dpow32(w, e, (uint32_t)p); }
+__device__ __forceinline__ uint64_t tw_pow(uint64_t w, uint64_t e, uint64_t) { return dpowG(w, e); }
+
+// level table for a length-L transform with root w_L: tw[m + i] = w_L^(i L / 2m)
+template <class W, class E>
+__global__ void k_level_table(W* tw, int k, E w, uint64_t p) {
+    const long long L = 1ll << k;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < L;
+         idx += (long long)gridDim.x * blockDim.x) {
+        if (idx == 0) { tw_set(tw, 0, (E)1, p); continue; }
+        int lm = 63 - __clzll(idx);
+        long long m = 1ll << lm, i = idx - m;
+        uint64_t e = (uint64_t)i << (k - 1 - lm);
+        tw_set(tw, idx, (E)tw_pow(w, e, p), p);
+    }
+}
+// power table: t[i] = w^(i * step) for i < cnt
+template <class W, class E>
+__global__ void k_pow_table(W* t, long long cnt, E w, uint64_t step, uint64_t p) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
+        tw_set(t, i, (E)tw_pow(w, (uint64_t)i * step, p), p);
+}
+
+// ---------------------------------------------------------------- carries (int_mul)
+// coefficient c_k < 2^56 (exact integer) -> 16-bit digits; s_j = sum_t digit_t(c_{j-t}) < 2^18.
+// u_j = (s_j mod 2^16) + (s_{j-1} >> 16)  < 2^16 + 4; w_j = u_j mod 2^16, g_j = u_j >> 16 in {0,1};
+// carry chain: C_{j+1} = g_j | (w_j == 0xFFFF & C_j); out_j = (w_j + C_j) mod 2^16.
+__device__ __forceinline__ uint32_t s_at(const uint64_t* __restrict__ c, long long j, long long nc) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        long long k = j - t;
+        if (k >= 0 && k < nc) s += (uint32_t)((c[k] >> (16 * t)) & 0xFFFF);
+    }
+    return s;
+}
+__device__ __forceinline__ void carry_gp(const uint64_t* c, long long j, long long nc, uint32_t& w, uint32_t& g) {
+    uint32_t sj = s_at(c, j, nc);
+    uint32_t sp = j > 0 ? s_at(c, j - 1, nc) : 0;
+    uint32_t u = (sj & 0xFFFF) + (sp >> 16);
+    w = u & 0xFFFF;
+    g = u >> 16;
+}
+// (G,P) composition: applying segment lo then hi: G = Ghi | (Phi & Glo), P = Phi & Plo
+constexpr int CARRY_T = 256, CARRY_E = 16, CARRY_B = CARRY_T * CARRY_E;
+
+__device__ __forceinline__ uint32_t gp_comb(uint32_t lo, uint32_t hi) {   // bit0 = G, bit1 = P
+    uint32_t G = (hi & 1) | ((hi >> 1) & lo & 1);
+    uint32_t P = (hi >> 1) & (lo >> 1) & 1;
+    return G | (P << 1);
+}
+
+// block-exclusive scan of (G,P) over threads; returns the thread's carry-in
+// relative to the block start (assuming block carry-in = cin).
+__device__ uint32_t block_carry_in(uint32_t mine, uint32_t cin, uint32_t* sh) {
+    // inclusive warp scan
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = gp_comb(y, x);
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 2u;   // identity: G=0,P=1
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v = gp_comb(y, v);
+        }
+        sh[32 + lane] = v;   // inclusive over warps
+    }
+    __syncthreads();
+    uint32_t excl_w = wid > 0 ? sh[32 + wid - 1] : 2u;
+    uint32_t excl_l = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) excl_l = 2u;
+    uint32_t pre = gp_comb(excl_w, excl_l);      // exclusive prefix within block
+    uint32_t res = (pre & 1) | ((pre >> 1) & cin);
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(CARRY_T) k_carry_reduce(const uint64_t* __restrict__ c, long long nc, long long nout,
+                                                          uint32_t* __restrict__ agg) {
+    __shared__ uint32_t sh[64];
+    long long j0 = (long long)blockIdx.x * CARRY_B + (long long)threadIdx.x * CARRY_E;
+    uint32_t acc = 2u;   // identity
+    for (int e = 0; e < CARRY_E; e++) {
+        long long j = j0 + e;
+        uint32_t gp = 2u;
+        if (j < nout) {
+            uint32_t w, g;
+            carry_gp(c, j, nc, w, g);
+            gp = g | ((w == 0xFFFF ? 1u : 0u) << 1);
+        }
+        acc = gp_comb(acc, gp);
+    }
+    // reduce over the block (inclusive scan, take the last)
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = gp_comb(y, x);
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t v = 2u;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) v = gp_comb(v, sh[w]);
+        agg[blockIdx.x] = v;
+    }
+}
+
+// sequential-in-chunks scan of block aggregates -> carry-in per block
+__global__ void k_carry_scan(uint32_t* agg, long long nblk) {
+    __shared__ uint32_t sh[64];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < nblk; base += blockDim.x) {
+        long long i = base + threadIdx.x;
+        uint32_t mine = i < nblk ? agg[i] : 2u;
+        uint32_t cin = block_carry_in(mine, carry, sh);
+        __syncthreads();
+        if (i < nblk) agg[i] = cin;     // carry into block i
+        // carry out of this chunk = carry-in of last + its own
+        if (threadIdx.x == blockDim.x - 1) carry = (mine & 1) | ((mine >> 1) & cin);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(CARRY_T) k_carry_apply(const uint64_t* __restrict__ c, long long nc, long long nout,
+                                                         const uint32_t* __restrict__ cin_blk,
+                                                         uint16_t* __restrict__ out) {
+    __shared__ uint32_t sh[64];
+    long long j0 = (long long)blockIdx.x * CARRY_B + (long long)threadIdx.x * CARRY_E;
+    uint32_t w[CARRY_E], g[CARRY_E];
+    uint32_t acc = 2u;
+#pragma unroll
+    for (int e = 0; e < CARRY_E; e++) {
+        long long j = j0 + e;
+        w[e] = 0; g[e] = 0;
+        uint32_t gp = 2u;
+        if (j < nout) {
+            carry_gp(c, j, nc, w[e], g[e]);
+            gp = g[e] | ((w[e] == 0xFFFF ? 1u : 0u) << 1);
+        }
+        acc = gp_comb(acc, gp);
+    }
+    uint32_t C = block_carry_in(acc, cin_blk[blockIdx.x], sh);
+#pragma unroll
+    for (int e = 0; e < CARRY_E; e++) {
+        long long j = j0 + e;
+        if (j < nout) out[j] = (uint16_t)((w[e] + C) & 0xFFFF);
+        C = g[e] | ((w[e] == 0xFFFF) & C);
+    }
+}
+
+}  // namespace mm
+
+using namespace mm;
+
+// ====================================================================== plans
+struct mm_ntt_plan {
+    int word_bits;
+    uint64_t p, omega;
+    int k, k1, k2;           // n = 2^k = n2 * n1, n1 = 2^k1 (rows), n2 = 2^k2 (cols)
+    size_t batch;
+    void* lvl_f1 = nullptr;  // level tables for n1 (or n when single pass)
+    void* lvl_i1 = nullptr;
+    void* lvl_f2 = nullptr;  // level tables for n2
+    void* lvl_i2 = nullptr;
+    void* fs_lo_f = nullptr; // four-step twiddles w^e split at fs_h bits
+    void* fs_hi_f = nullptr;
+    void* fs_lo_i = nullptr;
+    void* fs_hi_i = nullptr;
+    int fs_h = 0;
+    uint64_t ninv;           // n^-1 mod p
+    uint64_t ninv_r;         // n^-1 2^32 mod p (32-bit: after REDC)
+    uint32_t pinv;           // p^-1 mod 2^32
+    void* ws = nullptr;      // lazily allocated workspace (bit-mirror permutations)
+    size_t ws_bytes = 0;
+    std::mutex mu;
+};
+
+namespace mm {
+
+template <class F> static F make_field(const mm_ntt_plan* P);
+template <> Fp32 make_field<Fp32>(const mm_ntt_plan* P) {
+    Fp32 f;
+    f.p = (uint32_t)P->p;
+    f.p2 = 2 * (uint32_t)P->p;
+    f.pinv = P->pinv;
+    return f;
+}
+template <> FpG make_field<FpG>(const mm_ntt_plan*) { return FpG(); }
+
+static inline uint2 mkw32(uint64_t w, uint64_t p) {
+    return make_uint2((uint32_t)w, (uint32_t)(((u128)w << 32) / p));
+}
+template <class W> static W host_w(uint64_t w, uint64_t p);
+template <> uint2 host_w<uint2>(uint64_t w, uint64_t p) { return mkw32(w, p); }
+template <> uint64_t host_w<uint64_t>(uint64_t w, uint64_t) { return w; }
+
+static size_t esize(int word_bits) { return word_bits == 32 ? 4 : 8; }
+
+template <class K> static mm_status set_smem(K kern, size_t bytes) {
+    static std::mutex m;
+    std::lock_guard<std::mutex> g(m);
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return MM_OK;
+}
+
+template <class K> static int grid_for(K kern, size_t smem, long long tiles) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    long long cap = (long long)num_sms() * per_sm;
+    return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+}
+
+template <class T> static int rows_per_tile(int k) {
+    int budget = sizeof(T) == 4 ? 8192 : 4096;   // elements per tile
+    int L = 1 << k;
+    return L >= budget ? 1 : budget / L;
+}
+template <class T> static int cols_per_tile(int k) {
+    int minc = 32 / (int)sizeof(T);             // one 32-byte sector per row
+    int maxc = 128 / (int)sizeof(T);            // one 128-byte line per row
+    int budget = sizeof(T) == 4 ? 8192 : 4096;
+    int c = budget >> k;
+    if (c < minc) c = minc;
+    if (c > maxc) c = maxc;
+    return c;
+}
+
+
+// ---- launchers
+template <class F, bool INV, class TIn, class TOut>
+static mm_status launch_rows(const F& f, RowArgs<F>& a, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    int L = 1 << a.k;
+    size_t data = (size_t)a.C * srow_len<T>(L, false) * sizeof(T);
+    a.tw_smem = data + (size_t)L * sizeof(W) <= SMEM_MAX;
+    size_t smem = data + (a.tw_smem ? (size_t)L * sizeof(W) : 0);
+    auto kern = k_rows<F, INV, TIn, TOut>;
+    mm_status s = set_smem(kern, smem);
+    if (s != MM_OK) return s;
+    long long tiles = (a.nrows + a.C - 1) / a.C;
+    {
+        LaunchScope ls(INV ? "ntt_rows_inv" : "ntt_rows_fwd", st);
+        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+template <class F, bool INV, class TIn, class TOut>
+static mm_status launch_cols(const F& f, ColArgs<F>& a, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    int L = 1 << a.k;
+    size_t data = (size_t)a.C * srow_len<T>(L, true) * sizeof(T);
+    a.tw_smem = data + (size_t)L * sizeof(W) <= SMEM_MAX;
+    size_t smem = data + (a.tw_smem ? (size_t)L * sizeof(W) : 0);
+    auto kern = k_cols<F, INV, TIn, TOut>;
+    mm_status s = set_smem(kern, smem);
+    if (s != MM_OK) return s;
+    long long tiles = (a.ncols + a.C - 1) / a.C * a.nbatch;
+    {
+        LaunchScope ls(INV ? "ntt_cols_inv" : "ntt_cols_fwd", st);
+        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+template <class F, class TIn, class TOut>
+static mm_status launch_pmul(const F& f, PmulArgs<F>& a, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    int L = 1 << a.k;
+    size_t data = 2 * (size_t)a.C * srow_len<T>(L, false) * sizeof(T);
+    a.tw_smem = data + 2 * (size_t)L * sizeof(W) <= SMEM_MAX;
+    size_t smem = data + (a.tw_smem ? 2 * (size_t)L * sizeof(W) : 0);
+    auto kern = k_rows_pmul<F, TIn, TOut>;
+    mm_status s = set_smem(kern, smem);
+    if (s != MM_OK) return s;
+    long long tiles = (a.nrows + a.C - 1) / a.C;
+    {
+        LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
+        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+// ---- plan construction
+template <class W, class E>
+static mm_status build_level(void** dst, int k, E w, uint64_t p) {
+    size_t L = (size_t)1 << k;
+    MM_CUDA_TRY(cudaMalloc(dst, L * sizeof(W)));
+    int grid = (int)((L + 255) / 256 < 4096 ? (L + 255) / 256 : 4096);
+    {
+        LaunchScope ls("twiddle_level_table", 0);
+        k_level_table<W, E><<<grid, 256>>>((W*)*dst, k, w, p);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+template <class W, class E>
+static mm_status build_pow(void** dst, long long cnt, E w, uint64_t step, uint64_t p) {
+    MM_CUDA_TRY(cudaMalloc(dst, (size_t)cnt * sizeof(W)));
+    int grid = (int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096);
+    {
+        LaunchScope ls("twiddle_pow_table", 0);
+        k_pow_table<W, E><<<grid, 256>>>((W*)*dst, cnt, w, step, p);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+template <class W, class E>
+static mm_status build_tables(mm_ntt_plan* P) {
+    uint64_t p = P->p, w = P->omega;
+    uint64_t winv = hpowmod(w, p - 2, p);
+    int k = P->k;
+    mm_status s;
+    if (P->k2 == 0) {
+        if ((s = build_level<W, E>(&P->lvl_f1, k, (E)w, p)) != MM_OK) return s;
+        if ((s = build_level<W, E>(&P->lvl_i1, k, (E)winv, p)) != MM_OK) return s;
+    } else {
+        // rows: length n1 with root w^n2; columns: length n2 with root w^n1 (Algorithm 1 steps 1, 3)
+        uint64_t n1 = 1ull << P->k1, n2 = 1ull << P->k2;
+        if ((s = build_level<W, E>(&P->lvl_f1, P->k1, (E)hpowmod(w, n2, p), p)) != MM_OK) return s;
+        if ((s = build_level<W, E>(&P->lvl_i1, P->k1, (E)hpowmod(winv, n2, p), p)) != MM_OK) return s;
+        if ((s = build_level<W, E>(&P->lvl_f2, P->k2, (E)hpowmod(w, n1, p), p)) != MM_OK) return s;
+        if ((s = build_level<W, E>(&P->lvl_i2, P->k2, (E)hpowmod(winv, n1, p), p)) != MM_OK) return s;
+        // step 2 twiddles w^e, e < n, e = e_lo + 2^h e_hi
+        int h = (k + 1) / 2;
+        P->fs_h = h;
+        long long nlo = 1ll << h, nhi = 1ll << (k - h);
+        if ((s = build_pow<W, E>(&P->fs_lo_f, nlo, (E)w, 1, p)) != MM_OK) return s;
+        if ((s = build_pow<W, E>(&P->fs_hi_f, nhi, (E)w, 1ull << h, p)) != MM_OK) return s;
+        if ((s = build_pow<W, E>(&P->fs_lo_i, nlo, (E)winv, 1, p)) != MM_OK) return s;
+        if ((s = build_pow<W, E>(&P->fs_hi_i, nhi, (E)winv, 1ull << h, p)) != MM_OK) return s;
+    }
+    MM_CUDA_TRY(cudaDeviceSynchronize());
+    return MM_OK;
+}
+
+static void free_plan(mm_ntt_plan* P) {
+    if (!P) return;
+    void* bufs[] = {P->lvl_f1, P->lvl_i1, P->lvl_f2, P->lvl_i2, P->fs_lo_f, P->fs_hi_f, P->fs_lo_i, P->fs_hi_i, P->ws};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    delete P;
+}
+
+static mm_status check_modulus(int word_bits, uint64_t p, int log2n) {
+    if (word_bits == 32) {
+        if (p < 3 || !(p & 1) || !hprime(p)) return set_err(MM_E_INVALID_MODULUS, "p=%llu is not an odd prime", (unsigned long long)p);
+        if (p >= (1ull << 30)) return set_err(MM_E_PROFILE, "32-bit NTT needs p < 2^30 (lazy butterflies in [0,4p)), got %llu", (unsigned long long)p);
+        if (log2n < 1 || log2n > 24) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,24]", log2n);
+    } else if (word_bits == 64) {
+        if (p != FpG::P) return set_err(MM_E_INVALID_MODULUS, "64-bit NTT supports only p = 2^64 - 2^32 + 1");
+        if (log2n < 1 || log2n > 26) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,26]", log2n);
+    } else {
+        return set_err(MM_E_ARG, "word_bits must be 32 or 64");
+    }
+    if (log2n > two_adicity(p)) return set_err(MM_E_UNSUPPORTED_SIZE, "2^%d does not divide p-1", log2n);
+    return MM_OK;
+}
+
+static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch, mm_ntt_plan** out) {
+    mm_status s = check_modulus(word_bits, p, log2n);
+    if (s != MM_OK) return s;
+    uint64_t n = 1ull << log2n;
+    omega %= p;
+    if (hpowmod(omega, n / 2, p) != p - 1)
+        return set_err(MM_E_BAD_ROOT, "omega^(n/2) != p-1: omega is not a primitive 2^%d-th root", log2n);
+    mm_ntt_plan* P = new (std::nothrow) mm_ntt_plan;
+    if (!P) return set_err(MM_E_ARG, "out of host memory");
+    P->word_bits = word_bits;
+    P->p = p;
+    P->omega = omega;
+    P->k = log2n;
+    P->batch = batch;
+    if (log2n <= MAX_BLOCK_LOG) {
+        P->k1 = log2n;
+        P->k2 = 0;
+    } else {
+        // n1 (row length, contiguous) >= n2 (column length, strided)
+        P->k2 = log2n / 2;
+        P->k1 = log2n - P->k2;
+    }
+    P->ninv = hpowmod(n % p, p - 2, p);
+    P->ninv_r = word_bits == 32 ? hmulmod(P->ninv, ((u128)1 << 32) % p, p) : P->ninv;
+    P->pinv = word_bits == 32 ? inv_mod_2_32((uint32_t)p) : 0;
+    s = word_bits == 32 ? build_tables<uint2, uint32_t>(P) : build_tables<uint64_t, uint64_t>(P);
+    if (s != MM_OK) {
+        free_plan(P);
+        return s;
+    }
+    *out = P;
+    return MM_OK;
+}
+
+static mm_status ensure_ws(mm_ntt_plan* P, size_t bytes) {
+    std::lock_guard<std::mutex> g(P->mu);
+    if (P->ws_bytes >= bytes) return MM_OK;
+    if (P->ws) {
+        cudaDeviceSynchronize();
+        cudaFree(P->ws);
+        P->ws = nullptr;
+        P->ws_bytes = 0;
+    }
+    MM_CUDA_TRY(cudaMalloc(&P->ws, bytes));
+    P->ws_bytes = bytes;
+    return MM_OK;
+}
+
+// ---- forward / inverse drivers ------------------------------------------------------
+template <class F>
+static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order order, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    const long long n = 1ll << P->k;
+    if (P->k2 == 0) {
+        RowArgs<F> a{};
+        a.in = in; a.out = out;
+        a.nrows = (long long)P->batch;
+        a.in_rs = a.out_rs = n;
+        a.in_len = a.out_len = n;
+        a.k = P->k;
+        a.C = rows_per_tile<T>(P->k);
+        a.perm = order == MM_ORDER_NATURAL;
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_f1;
+        return launch_rows<F, false, T, T>(f, a, st);
+    }
+    // column pass: in -> out, then row pass: out -> out (bit-mirrored result)
+    ColArgs<F> c{};
+    c.in = in; c.out = out;
+    c.ncols = 1ll << P->k1;
+    c.nbatch = (long long)P->batch;
+    c.in_rs = c.out_rs = 1ll << P->k1;
+    c.in_bs = c.out_bs = n;
+    c.in_len = c.out_len = n;
+    c.col0 = 0;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.C = cols_per_tile<T>(P->k2);
+    c.fs = 1;
+    c.lvl = (const W*)P->lvl_f2;
+    c.fs_lo = (const W*)P->fs_lo_f;
+    c.fs_hi = (const W*)P->fs_hi_f;
+    c.fs_h = P->fs_h;
+    mm_status s = launch_cols<F, false, T, T>(f, c, st);
+    if (s != MM_OK) return s;
+    RowArgs<F> a{};
+    a.in = out; a.out = out;
+    a.nrows = (long long)P->batch << P->k2;
+    a.in_rs = a.out_rs = 1ll << P->k1;
+    a.in_len = a.out_len = 1ll << P->k1;
+    a.k = P->k1;
+    a.C = rows_per_tile<T>(P->k1);
+    a.canon = 1;
+    a.lvl = (const W*)P->lvl_f1;
+    if ((s = launch_rows<F, false, T, T>(f, a, st)) != MM_OK) return s;
+    if (order == MM_ORDER_NATURAL) {
+        size_t bytes = (size_t)n * P->batch * sizeof(T);
+        if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
+        {
+            LaunchScope ls("bitrev_permute", st);
+            k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)out, (T*)P->ws, P->k, (long long)P->batch);
+        }
+        MM_LAUNCH_CHECK();
+        MM_CUDA_TRY(cudaMemcpyAsync(out, P->ws, bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    return MM_OK;
+}
+
+template <class F>
+static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order order, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    const long long n = 1ll << P->k;
+    W sc = host_w<W>(P->ninv, P->p);
+    if (P->k2 == 0) {
+        RowArgs<F> a{};
+        a.in = in; a.out = out;
+        a.nrows = (long long)P->batch;
+        a.in_rs = a.out_rs = n;
+        a.in_len = a.out_len = n;
+        a.k = P->k;
+        a.C = rows_per_tile<T>(P->k);
+        a.perm = order == MM_ORDER_NATURAL;
+        a.scale = 1; a.sc = sc;
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_i1;
+        return launch_rows<F, true, T, T>(f, a, st);
+    }
+    mm_status s;
+    const void* src = in;
+    if (order == MM_ORDER_NATURAL) {
+        size_t bytes = (size_t)n * P->batch * sizeof(T);
+        if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
+        {
+            LaunchScope ls("bitrev_permute", st);
+            k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)P->ws, P->k, (long long)P->batch);
+        }
+        MM_LAUNCH_CHECK();
+        src = P->ws;
+    }
+    // inverse row pass (DIT over j1 + twiddle w^-(j1 [i2])): src -> out
+    RowArgs<F> a{};
+    a.in = src; a.out = out;
+    a.nrows = (long long)P->batch << P->k2;
+    a.in_rs = a.out_rs = 1ll << P->k1;
+    a.in_len = a.out_len = 1ll << P->k1;
+    a.k = P->k1;
+    a.C = rows_per_tile<T>(P->k1);
+    a.fs = 1; a.k2 = P->k2; a.row0 = 0;
+    a.lvl = (const W*)P->lvl_i1;
+    a.fs_lo = (const W*)P->fs_lo_i;
+    a.fs_hi = (const W*)P->fs_hi_i;
+    a.fs_h = P->fs_h;
+    if ((s = launch_rows<F, true, T, T>(f, a, st)) != MM_OK) return s;
+    // inverse column pass (DIT over i2, n^-1, canonical): out -> out
+    ColArgs<F> c{};
+    c.in = out; c.out = out;
+    c.ncols = 1ll << P->k1;
+    c.nbatch = (long long)P->batch;
+    c.in_rs = c.out_rs = 1ll << P->k1;
+    c.in_bs = c.out_bs = n;
+    c.in_len = c.out_len = n;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.C = cols_per_tile<T>(P->k2);
+    c.scale = 1; c.sc = sc; c.canon = 1;
+    c.lvl = (const W*)P->lvl_i2;
+    return launch_cols<F, true, T, T>(f, c, st);
+}
+
+// ---- dist building blocks ---------------------------------------------------------
+template <class F>
+static mm_status fwd_cols_impl(mm_ntt_plan* P, const void* in, void* out, size_t col0, size_t ncols, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    ColArgs<F> c{};
+    c.in = in; c.out = out;
+    c.ncols = (long long)ncols;
+    c.nbatch = 1;
+    c.in_rs = c.out_rs = (long long)ncols;
+    c.in_bs = c.out_bs = 0;
+    c.in_len = c.out_len = 1ll << P->k;
+    c.col0 = (long long)col0;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.C = cols_per_tile<T>(P->k2);
+    c.fs = 1;
+    c.lvl = (const W*)P->lvl_f2;
+    c.fs_lo = (const W*)P->fs_lo_f;
+    c.fs_hi = (const W*)P->fs_hi_f;
+    c.fs_h = P->fs_h;
+    return launch_cols<F, false, T, T>(f, c, st);
+}
+template <class F>
+static mm_status rows_impl(mm_ntt_plan* P, const void* in, void* out, size_t row0, size_t nrows, bool inv,
+                           cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    RowArgs<F> a{};
+    a.in = in; a.out = out;
+    a.nrows = (long long)nrows;
+    a.in_rs = a.out_rs = 1ll << P->k1;
+    a.in_len = a.out_len = 1ll << P->k1;
+    a.k = P->k1;
+    a.C = rows_per_tile<T>(P->k1);
+    a.row0 = (long long)row0;
+    a.k2 = P->k2;
+    if (!inv) {
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_f1;
+        return launch_rows<F, false, T, T>(f, a, st);
+    }
+    a.fs = 1;
+    a.lvl = (const W*)P->lvl_i1;
+    a.fs_lo = (const W*)P->fs_lo_i;
+    a.fs_hi = (const W*)P->fs_hi_i;
+    a.fs_h = P->fs_h;
+    return launch_rows<F, true, T, T>(f, a, st);
+}
+template <class F>
+static mm_status inv_cols_impl(mm_ntt_plan* P, const void* in, void* out, size_t col0, size_t ncols, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    ColArgs<F> c{};
+    c.in = in; c.out = out;
+    c.ncols = (long long)ncols;
+    c.nbatch = 1;
+    c.in_rs = c.out_rs = (long long)ncols;
+    c.in_len = c.out_len = 1ll << P->k;
+    c.col0 = (long long)col0;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.C = cols_per_tile<T>(P->k2);
+    c.scale = 1; c.sc = host_w<W>(P->ninv, P->p); c.canon = 1;
+    c.lvl = (const W*)P->lvl_i2;
+    return launch_cols<F, true, T, T>(f, c, st);
+}
+
+// ---- cached plans + workspaces for poly_mul / int_mul ----------------------------
+static std::mutex g_cache_mu;
+static std::map<std::tuple<int, uint64_t, int, uint64_t, int>, mm_ntt_plan*> g_plans;   // (bits,p,k,omega,dev)
+struct WsKey { int dev; cudaStream_t st; bool operator<(const WsKey& o) const { return dev != o.dev ? dev < o.dev : st < o.st; } };
+static std::map<WsKey, std::pair<void*, size_t>> g_ws;
+
+static mm_status cached_plan(int bits, uint64_t p, int k, uint64_t omega, mm_ntt_plan** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto key = std::make_tuple(bits, p, k, omega, dev);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) { *out = it->second; return MM_OK; }
+    mm_ntt_plan* P = nullptr;
+    mm_status s = plan_create(bits, p, k, omega, 1, &P);
+    if (s != MM_OK) return s;
+    g_plans[key] = P;
+    *out = P;
+    return MM_OK;
+}
+
+static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto& e = g_ws[WsKey{dev, st}];
+    if (e.second < bytes) {
+        if (e.first) {
+            MM_CUDA_TRY(cudaStreamSynchronize(st));
+            cudaFree(e.first);
+            e.first = nullptr;
+            e.second = 0;
+        }
+        MM_CUDA_TRY(cudaMalloc(&e.first, bytes));
+        e.second = bytes;
+    }
+    *out = e.first;
+    return MM_OK;
+}
+
+// c = a * b for `batch` rows; TIn = input element type (uint16 limbs for int_mul)
+template <class F, class TIn, class TOut>
+static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const TIn* b, long long lb, TOut* c,
+                              long long lc, long long batch, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    W sc = host_w<W>(P->ninv_r, P->p);   // n^-1 (x 2^32 for the 32-bit REDC product)
+    if (P->k2 == 0) {
+        PmulArgs<F> m{};
+        m.a = a; m.b = b; m.c = c;
+        m.nrows = batch;
+        m.a_rs = la; m.b_rs = lb; m.c_rs = lc;
+        m.la = la; m.lb = lb; m.lc = lc;
+        m.k = P->k;
+        m.C = rows_per_tile<T>(P->k) / 2 > 0 ? rows_per_tile<T>(P->k) / 2 : 1;
+        m.sc = sc;
+        m.canon = 1;
+        m.lvl_f = (const W*)P->lvl_f1;
+        m.lvl_i = (const W*)P->lvl_i1;
+        return launch_pmul<F, TIn, TOut>(f, m, st);
+    }
+    const long long n = 1ll << P->k, n1 = 1ll << P->k1;
+    void* ws = nullptr;
+    mm_status s = stream_ws(st, (size_t)(2 * n * batch) * sizeof(T), &ws);
+    if (s != MM_OK) return s;
+    T* WA = (T*)ws;
+    T* WB = WA + n * batch;
+    // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb
+    for (int op = 0; op < 2; op++) {
+        ColArgs<F> cc{};
+        cc.in = op == 0 ? (const void*)a : (const void*)b;
+        cc.out = op == 0 ? WA : WB;
+        cc.ncols = n1;
+        cc.nbatch = batch;
+        cc.in_rs = n1; cc.out_rs = n1;
+        cc.in_bs = op == 0 ? la : lb; cc.out_bs = n;
+        cc.in_len = op == 0 ? la : lb; cc.out_len = n;
+        cc.n1 = n1;
+        cc.k = P->k2;
+        cc.C = cols_per_tile<T>(P->k2);
+        cc.fs = 1;
+        cc.lvl = (const W*)P->lvl_f2;
+        cc.fs_lo = (const W*)P->fs_lo_f;
+        cc.fs_hi = (const W*)P->fs_hi_f;
+        cc.fs_h = P->fs_h;
+        if ((s = launch_cols<F, false, TIn, T>(f, cc, st)) != MM_OK) return s;
+    }
+    // fused row pass: steps 3-4 for both, pointwise product * n^-1, inverse step 4-3, inverse twiddle
+    PmulArgs<F> m{};
+    m.a = WA; m.b = WB; m.c = WA;
+    m.nrows = batch << P->k2;
+    m.a_rs = m.b_rs = m.c_rs = n1;
+    m.la = m.lb = m.lc = n1;
+    m.k = P->k1;
+    m.C = rows_per_tile<T>(P->k1) / 2 > 0 ? rows_per_tile<T>(P->k1) / 2 : 1;
+    m.fs = 1; m.k2 = P->k2; m.row0 = 0;
+    m.sc = sc;
+    m.lvl_f = (const W*)P->lvl_f1;
+    m.lvl_i = (const W*)P->lvl_i1;
+    m.fs_lo = (const W*)P->fs_lo_i;
+    m.fs_hi = (const W*)P->fs_hi_i;
+    m.fs_h = P->fs_h;
+    if ((s = launch_pmul<F, T, T>(f, m, st)) != MM_OK) return s;
+    // inverse column pass (step 1 inverse), canonical, truncated to lc
+    ColArgs<F> ci{};
+    ci.in = WA; ci.out = c;
+    ci.ncols = n1;
+    ci.nbatch = batch;
+    ci.in_rs = n1; ci.out_rs = n1;
+    ci.in_bs = n; ci.out_bs = lc;
+    ci.in_len = n; ci.out_len = lc;
+    ci.n1 = n1;
+    ci.k = P->k2;
+    ci.C = cols_per_tile<T>(P->k2);
+    ci.canon = 1;
+    ci.lvl = (const W*)P->lvl_i2;
+    return launch_cols<F, true, T, TOut>(f, ci, st);
+}
+
+}  // namespace mm
+
+// ====================================================================== C ABI
+extern "C" mm_status mm_ntt_plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch,
+                                        mm_ntt_plan** plan) {
+    if (!plan) return set_err(MM_E_ARG, "plan is null");
+    *plan = nullptr;
+    if (batch == 0) return set_err(MM_E_ARG, "batch must be >= 1");
+    return plan_create(word_bits, p, log2n, omega, batch, plan);
+}
+
+extern "C" void mm_ntt_plan_destroy(mm_ntt_plan* plan) {
+    if (plan) cudaDeviceSynchronize();
+    free_plan(plan);
+}
+
+extern "C" mm_status mm_ntt_plan_info(const mm_ntt_plan* P, uint64_t out[4]) {
+    if (!P || !out) return set_err(MM_E_ARG, "null argument");
+    out[0] = 1ull << P->k1;
+    out[1] = 1ull << P->k2;
+    out[2] = P->k2 ? 2 : 1;
+    out[3] = P->ws_bytes;
+    return MM_OK;
+}
+
+extern "C" mm_status mm_ntt_forward(const mm_ntt_plan* plan, const void* in, void* out, mm_order order, void* stream) {
+    if (!plan || !in || !out) return set_err(MM_E_ARG, "null argument");
+    if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? fwd_impl<Fp32>(P, in, out, order, st) : fwd_impl<FpG>(P, in, out, order, st);
+}
+
+extern "C" mm_status mm_ntt_inverse(const mm_ntt_plan* plan, const void* in, void* out, mm_order order, void* stream) {
+    if (!plan || !in || !out) return set_err(MM_E_ARG, "null argument");
+    if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? inv_impl<Fp32>(P, in, out, order, st) : inv_impl<FpG>(P, in, out, order, st);
+}
+
+static mm_status dist_check(const mm_ntt_plan* P, const void* in, void* out, size_t off, size_t cnt, bool cols) {
+    if (!P || !in || !out) return set_err(MM_E_ARG, "null argument");
+    if (P->k2 == 0) return set_err(MM_E_UNSUPPORTED_SIZE, "four-step blocks need log2n > %d", MAX_BLOCK_LOG);
+    size_t lim = cols ? (1ull << P->k1) : (1ull << P->k2);
+    if (cnt == 0 || off + cnt > lim) return set_err(MM_E_ARG, "block [%zu, %zu) out of range %zu", off, off + cnt, lim);
+    return MM_OK;
+}
+
+extern "C" mm_status mm_ntt_fwd_cols(const mm_ntt_plan* plan, const void* in, void* out, size_t col0, size_t ncols,
+                                     void* stream) {
+    mm_status s = dist_check(plan, in, out, col0, ncols, true);
+    if (s != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? fwd_cols_impl<Fp32>(P, in, out, col0, ncols, st)
+                              : fwd_cols_impl<FpG>(P, in, out, col0, ncols, st);
+}
+extern "C" mm_status mm_ntt_fwd_rows(const mm_ntt_plan* plan, const void* in, void* out, size_t row0, size_t nrows,
+                                     void* stream) {
+    mm_status s = dist_check(plan, in, out, row0, nrows, false);
+    if (s != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? rows_impl<Fp32>(P, in, out, row0, nrows, false, st)
+                              : rows_impl<FpG>(P, in, out, row0, nrows, false, st);
+}
+extern "C" mm_status mm_ntt_inv_rows(const mm_ntt_plan* plan, const void* in, void* out, size_t row0, size_t nrows,
+                                     void* stream) {
+    mm_status s = dist_check(plan, in, out, row0, nrows, false);
+    if (s != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? rows_impl<Fp32>(P, in, out, row0, nrows, true, st)
+                              : rows_impl<FpG>(P, in, out, row0, nrows, true, st);
+}
+extern "C" mm_status mm_ntt_inv_cols(const mm_ntt_plan* plan, const void* in, void* out, size_t col0, size_t ncols,
+                                     void* stream) {
+    mm_status s = dist_check(plan, in, out, col0, ncols, true);
+    if (s != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? inv_cols_impl<Fp32>(P, in, out, col0, ncols, st)
+                              : inv_cols_impl<FpG>(P, in, out, col0, ncols, st);
+}
+
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, const void* b,
+                                 size_t lb, void* c, size_t batch, void* stream) {
+    if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
+    if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
+    size_t lc = la + lb - 1;
+    size_t es = esize(word_bits);
+    if (overlaps(a, la * batch * es, c, lc * batch * es) || overlaps(b, lb * batch * es, c, lc * batch * es))
+        return set_err(MM_E_ALIAS, "c aliases a or b");
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k == 0) k = 1;
+    mm_status s = check_modulus(word_bits, p, k);
+    if (s != MM_OK) return s;
+    uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
+    mm_ntt_plan* P = nullptr;
+    if ((s = cached_plan(word_bits, p, k, omega, &P)) != MM_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (word_bits == 32)
+        return product_impl<Fp32, uint32_t, uint32_t>(P, (const uint32_t*)a, (long long)la, (const uint32_t*)b,
+                                                      (long long)lb, (uint32_t*)c, (long long)lc, (long long)batch, st);
+    return product_impl<FpG, uint64_t, uint64_t>(P, (const uint64_t*)a, (long long)la, (const uint64_t*)b, (long long)lb,
+                                                 (uint64_t*)c, (long long)lc, (long long)batch, st);
+}
+
+extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t* b, size_t nb, uint16_t* c,
+                                    void* stream) {
+    if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
+    if (na == 0 || nb == 0) return set_err(MM_E_ARG, "empty operands");
+    size_t nout = na + nb, lc = na + nb - 1;
+    if (overlaps(a, na * 2, c, nout * 2) || overlaps(b, nb * 2, c, nout * 2))
+        return set_err(MM_E_ALIAS, "c aliases a or b");
+    size_t mn = na < nb ? na : nb;
+    if ((u128)mn * 0xFFFE0001ull >= FpG::P) return set_err(MM_E_SIZE_OVERFLOW, "min(na,nb)(2^16-1)^2 >= p");
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k == 0) k = 1;
+    if (k > 26) return set_err(MM_E_SIZE_OVERFLOW, "na + nb - 1 > 2^26");
+    uint64_t p = FpG::P;
+    uint64_t omega = hpowmod(7, (p - 1) >> k, p);    // 7 generates (Z/pZ)^*
+    mm_ntt_plan* P = nullptr;
+    mm_status s = cached_plan(64, p, k, omega, &P);
+    if (s != MM_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    // coefficient buffer (lc u64) lives after the 2 n transform buffers of the workspace
+    size_t n = 1ull << k;
+    void* ws = nullptr;
+    if ((s = stream_ws(st, (2 * n + lc) * 8 + 16 * 1024 * 8, &ws)) != MM_OK) return s;
+    uint64_t* coef = (uint64_t*)ws + 2 * n;
+    if ((s = product_impl<FpG, uint16_t, uint64_t>(P, a, (long long)na, b, (long long)nb, coef, (long long)lc, 1, st)) !=
+        MM_OK)
+        return s;
+    // carry propagation (evaluation at 2^16)
+    long long nblk = ((long long)nout + CARRY_B - 1) / CARRY_B;
+    uint32_t* agg = (uint32_t*)(coef + lc);
+    if (nblk > 16 * 1024 * 2) return set_err(MM_E_SIZE_OVERFLOW, "too many carry blocks");
+    {
+        LaunchScope ls("carry_reduce", st);
+        k_carry_reduce<<<(int)nblk, CARRY_T, 0, st>>>(coef, (long long)lc, (long long)nout, agg);
+    }
+    MM_LAUNCH_CHECK();
+    {
+        LaunchScope ls("carry_scan", st);
+        k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
+    }
+    MM_LAUNCH_CHECK();
+    {
+        LaunchScope ls("carry_apply", st);
+        k_carry_apply<<<(int)nblk, CARRY_T, 0, st>>>(coef, (long long)lc, (long long)nout, agg, c);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}

@@ -1,0 +1,105 @@
+// probe.cu -- measurement helpers (not part of the method): integer-issue
+// probes that give the ALU roofline of the NTT kernels on this GPU.
+//
+// mm_probe_butterfly32: every thread keeps 16 residues in registers and runs
+// radix-16 DIF groups (the exact Fp32::dif butterfly of the NTT kernels, with
+// twiddles held in registers) `iters` times -- no memory traffic, so the rate
+// is the integer-pipe ceiling for the 32-bit butterfly.
+// mm_probe_butterfly64: the same for the Goldilocks butterfly (radix 8).
+#include "common.h"
+#include "arith.cuh"
+
+namespace mm {
+
+template <int R>
+__global__ void __launch_bounds__(256) k_probe_bfly32(Fp32 f, uint2 w0, int iters, uint32_t* sink) {
+    uint32_t v[R];
+    uint2 w[R / 2];
+#pragma unroll
+    for (int t = 0; t < R; t++) v[t] = (threadIdx.x * 2654435761u + t * 40503u + blockIdx.x) % f.p;
+#pragma unroll
+    for (int t = 0; t < R / 2; t++) w[t] = make_uint2(w0.x + t, w0.y + t);   // distinct twiddles (values irrelevant)
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+            for (int t = 0; t < R; t++) {
+                if (t & h) continue;
+                f.dif(v[t], v[t + h], w[(t & (h - 1)) % (R / 2)]);
+            }
+        }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < R; t++) acc ^= v[t];
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_probe_bfly64(int iters, uint64_t* sink) {
+    FpG f;
+    uint64_t v[R];
+    uint64_t w[R / 2];
+#pragma unroll
+    for (int t = 0; t < R; t++) v[t] = (uint64_t)(threadIdx.x * 2654435761u + t) * 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int t = 0; t < R / 2; t++) w[t] = 0x123456789ull * (t + 3 + blockIdx.x);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+            for (int t = 0; t < R; t++) {
+                if (t & h) continue;
+                f.dif(v[t], v[t + h], w[(t & (h - 1)) % (R / 2)]);
+            }
+        }
+    }
+    uint64_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < R; t++) acc ^= v[t];
+    if (acc == 0x12345678ull) sink[0] = acc;
+}
+
+}  // namespace mm
+
+using namespace mm;
+
+// Runs the probe once on `stream` and returns the kernel time in ms through
+// *ms (events on the launching stream) and the butterfly count through *bfly.
+extern "C" mm_status mm_probe_butterfly(int word_bits, int iters, double* ms, double* bfly, void* stream) {
+    if (!ms || !bfly || iters <= 0) return set_err(MM_E_ARG, "bad probe arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int blocks = num_sms() * 8, threads = 256;
+    void* sink = nullptr;
+    MM_CUDA_TRY(cudaMalloc(&sink, 16));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double per_iter;
+    cudaEventRecord(a, st);
+    {
+        LaunchScope ls("probe_butterfly", st);
+        if (word_bits == 32) {
+            Fp32 f;
+            f.p = 998244353u;
+            f.p2 = 2 * f.p;
+            f.pinv = inv_mod_2_32(f.p);
+            k_probe_bfly32<16><<<blocks, threads, 0, st>>>(f, make_uint2(12345u, 67890u), iters, (uint32_t*)sink);
+            per_iter = 32.0;
+        } else {
+            k_probe_bfly64<8><<<blocks, threads, 0, st>>>(iters, (uint64_t*)sink);
+            per_iter = 12.0;
+        }
+    }
+    cudaEventRecord(b, st);
+    cudaError_t e = cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return set_err(MM_E_CUDA, "probe failed: %s", cudaGetErrorString(e));
+    *ms = t;
+    *bfly = (double)blocks * threads * iters * per_iter;
+    return MM_OK;
+}

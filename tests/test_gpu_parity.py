@@ -1,0 +1,355 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Inputs come from gen/ (seeded, shared by both sides).  Sizes span several
+tiles and a ragged tail; the BASELINE full-size configs are checked on
+sampled outputs (or properties that hold at any size) in the launch
+configuration bench.py uses.
+"""
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import gen
+from gen import config_seed, limbs16, residues
+
+pytestmark = pytest.mark.gpu
+
+P30 = 998244353
+P32 = 3221225473
+PG = (1 << 64) - (1 << 32) + 1
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def mm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1407_3383_b200 as m
+    m.lib()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def u64(a):
+    return np.asarray(a).astype(np.uint64)
+
+
+# ------------------------------------------------------------------ C2 elementwise
+def test_mod32_info(mm, O):
+    for p in (P32, P30, 65537, 2147483647, 7):
+        info = mm.Mod32(p).info()
+        prof = 2 if info["r"] <= 30 else (1 if info["r"] <= 31 else 0)
+        bp = O.barrett_params(p, 32, prof)
+        assert (info["s"], info["t"], info["h"], info["q"]) == (bp["s"], bp["t"], bp["h"], bp["q"])
+        mp = O.montgomery_params(p, 32)
+        assert (info["pinv"] * p) % (1 << 32) == 1
+        assert (mp["chi"] * p + 1) % (1 << 32) == 0          # chi = -p^-1 mod 2^32
+        assert info["r2"] == pow(2, 64, p)
+
+
+def _ew_check(mm, O, p, x, y, offset=0):
+    M = mm.Mod32(p)
+    xt, yt = dev(x), dev(y)
+    if offset:
+        xt, yt = xt[offset:], yt[offset:]
+        x, y = x[offset:], y[offset:]
+    xs, ys = u64(x), u64(y)
+    assert np.array_equal(u64(host(M.add(xt, yt))), O.vec_addmod(xs, ys, p))
+    assert np.array_equal(u64(host(M.sub(xt, yt))), O.vec_submod(xs, ys, p))
+    ref = O.vec_mulmod(xs, ys, p)
+    assert np.array_equal(u64(host(M.mul(xt, yt, mm.MUL_BARRETT))), ref)
+    ysh = M.shoup_precompute(yt)
+    assert np.array_equal(u64(host(ysh)), O.vec_shoup_psi(ys, p, 32))
+    assert np.array_equal(u64(host(M.mul(xt, yt, mm.MUL_SHOUP, y_shoup=ysh))), ref)
+    assert np.array_equal(u64(host(M.mul(xt, yt, mm.MUL_MONTGOMERY))), O.vec_montmul(xs, ys, p, 32))
+    xm = M.to_mont(xt)
+    assert np.array_equal(u64(host(xm)), O.vec_to_mont(xs, p, 32))
+    assert np.array_equal(host(M.from_mont(xm)), host(xt))
+
+
+@pytest.mark.parametrize("p", [P32, P30, 2147483647, 65537])
+def test_elementwise_random(mm, O, p):
+    n = (1 << 20) + 3                         # many CTAs + ragged tail
+    x = residues(config_seed(2), 1, n, p)
+    y = residues(config_seed(2), 2, n, p)
+    _ew_check(mm, O, p, x, y)
+    _ew_check(mm, O, p, x, y, offset=1)        # unaligned pointers: scalar path
+
+
+@pytest.mark.parametrize("p", [P32, P30, 7])
+def test_elementwise_boundary(mm, O, p):
+    B = sorted({0, 1, 2, (p - 1) // 2, (p + 1) // 2, p - 2, p - 1, min(p - 1, 1 << 31), min(p - 1, (1 << 32) // 3)})
+    x = np.array([a for a in B for _ in B], dtype=np.uint32)
+    y = np.array([b for _ in B for b in B], dtype=np.uint32)
+    _ew_check(mm, O, p, x, y)
+
+
+def test_elementwise_inplace_and_empty(mm, O):
+    M = mm.Mod32(P32)
+    x = residues(3, 1, 1000, P32)
+    y = residues(3, 2, 1000, P32)
+    xt, yt = dev(x), dev(y)
+    M.add(xt, yt, out=xt)
+    assert np.array_equal(u64(host(xt)), O.vec_addmod(u64(x), u64(y), P32))
+    e = torch.empty(0, dtype=torch.uint32, device=DEV)
+    M.mul(e, e)
+
+
+def test_elementwise_full_c2_sampled(mm, O):
+    # BASELINE C2: 2^28 uint32 pairs, p = 3221225473, bench launch config
+    p, n = P32, 1 << 28
+    x = gen.residues_torch(config_seed(2), 1, n, p, DEV).view(torch.uint32)
+    y = gen.residues_torch(config_seed(2), 2, n, p, DEV).view(torch.uint32)
+    M = mm.Mod32(p)
+    idx = np.sort(np.random.default_rng(0).choice(n, 1 << 16, replace=False))
+    it = torch.from_numpy(idx).to(DEV)
+
+    def pick(t):      # gather sampled outputs (int32 view: indexing is not defined for uint32 on CUDA)
+        return u64(host(t.view(torch.int32)[it]).view(np.uint32))
+
+    xs = pick(x)
+    ys = pick(y)
+    assert np.array_equal(xs, u64(residues(config_seed(2), 1, n, p)[idx]))   # generator parity host/device
+    for name, z, ref in [("add", M.add(x, y), O.vec_addmod(xs, ys, p)),
+                         ("sub", M.sub(x, y), O.vec_submod(xs, ys, p)),
+                         ("mont", M.mul(x, y, mm.MUL_MONTGOMERY), O.vec_montmul(xs, ys, p, 32)),
+                         ("barrett", M.mul(x, y, mm.MUL_BARRETT), O.vec_mulmod(xs, ys, p))]:
+        assert np.array_equal(pick(z), ref), name
+        del z
+    ysh = M.shoup_precompute(y)
+    assert np.array_equal(pick(ysh), O.vec_shoup_psi(ys, p, 32))
+    z = M.mul(x, y, mm.MUL_SHOUP, y_shoup=ysh)
+    assert np.array_equal(pick(z), O.vec_mulmod(xs, ys, p))
+
+
+# ------------------------------------------------------------------ NTT
+def _ntt_roundtrip(mm, O, bits, p, g, k, batch, seed=5):
+    w = O.root_of_unity(g, k, p)
+    x = residues(seed, k, batch << k, p).reshape(batch, 1 << k)
+    plan = mm.NttPlan(bits, p, k, w, batch)
+    xt = dev(x)
+    nat = O.ntt_rows(x, w, p)
+    bit = np.stack([O.to_bitrev(r) for r in nat])
+    yb = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    assert np.array_equal(u64(host(yb)), bit), (bits, k, "bitrev")
+    yn = plan.forward(xt, out=torch.empty_like(xt), order=mm.NATURAL)
+    assert np.array_equal(u64(host(yn)), nat), (bits, k, "natural")
+    assert np.array_equal(host(plan.inverse(yb.clone(), order=mm.BITREV)), x)
+    assert np.array_equal(host(plan.inverse(yn.clone(), order=mm.NATURAL)), x)
+    # in place
+    xt2 = xt.clone()
+    plan.forward(xt2, order=mm.BITREV)
+    assert np.array_equal(u64(host(xt2)), bit)
+
+
+@pytest.mark.parametrize("k", list(range(1, 17)) + [18, 20])
+def test_ntt32_sizes(mm, O, k):
+    _ntt_roundtrip(mm, O, 32, P30, 3, k, batch=3 if k < 18 else 1)
+
+
+@pytest.mark.parametrize("k", list(range(1, 17)) + [18, 20])
+def test_ntt64_sizes(mm, O, k):
+    _ntt_roundtrip(mm, O, 64, PG, 7, k, batch=3 if k < 18 else 1)
+
+
+@pytest.mark.parametrize("bits,p,g", [(32, P30, 3), (32, 469762049, 3), (64, PG, 7)])
+def test_ntt_edge_rows(mm, O, bits, p, g):
+    for k in (4, 10, 14):
+        n = 1 << k
+        w = O.root_of_unity(g, k, p)
+        x = np.zeros((4, n), dtype=np.uint32 if bits == 32 else np.uint64)
+        x[0, 0] = 1                 # delta -> all ones (BASELINE)
+        x[1, :] = p - 1             # constant p-1 -> (n (p-1), 0, ...)
+        x[3, 1] = 1                 # delta_1 -> w^i
+        plan = mm.NttPlan(bits, p, k, w, 4)
+        y = u64(host(plan.forward(dev(x), order=mm.NATURAL)))
+        assert (y[0] == 1).all()
+        assert y[1, 0] == (n * (p - 1)) % p and not y[1, 1:].any()
+        assert not y[2].any()
+        assert [int(v) for v in y[3, :8]] == [pow(w, i, p) for i in range(8)]
+
+
+def test_ntt_c1_batch(mm, O):
+    # BASELINE C1: 16 independent fwd+inv NTTs of length 2^10 over 998244353
+    p, k = P30, 10
+    w = O.root_of_unity(3, k, p)
+    assert O.order_pow2(w, k, p) == 1 << k
+    x = residues(config_seed(1), 1, 16 << k, p).reshape(16, 1 << k)
+    plan = mm.NttPlan(32, p, k, w, 16)
+    y = plan.forward(dev(x), order=mm.NATURAL)
+    assert np.array_equal(u64(host(y)), O.ntt_rows(x, w, p))
+    assert np.array_equal(host(plan.inverse(y, order=mm.NATURAL)), x)
+
+
+def test_ntt_c3_forward_sampled(mm, O):
+    # BASELINE C3 forward: 4096 x 2^16 over 998244353, sampled rows vs oracle
+    p, k, B = P30, 16, 4096
+    w = O.root_of_unity(3, k, p)
+    x = gen.residues_torch(config_seed(3), 1, B << k, p, DEV).view(torch.uint32).reshape(B, 1 << k)
+    plan = mm.NttPlan(32, p, k, w, B)
+    y = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
+    for r in (0, 1, 1234, 4095):
+        xr = u64(host(x[r]))
+        assert np.array_equal(u64(host(y[r])), O.to_bitrev(O.ntt(xr, w, p))), r
+
+
+def test_ntt_c4_sampled(mm, O):
+    # BASELINE C4: 8 transforms of 2^24 over Goldilocks, four-step 2^12 x 2^12
+    k, B = 24, 8
+    w = O.root_of_unity(7, k, PG)
+    x = gen.residues_torch(config_seed(4), 1, B << k, PG, DEV).view(torch.uint64).reshape(B, 1 << k)
+    plan = mm.NttPlan(64, PG, k, w, B)
+    assert plan.info()["n1"] == 1 << 12 and plan.info()["n2"] == 1 << 12
+    y = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
+    rng = np.random.default_rng(4)
+    for b in (0, 7):
+        xb = host(x[b])
+        for pos in [0, 1, (1 << k) - 1] + list(rng.integers(0, 1 << k, 2)):
+            i = O.bitrev(int(pos), k)
+            assert int(host(y[b, int(pos)])) == O.dft_point(xb, w, i, PG), (b, pos)
+    z = plan.inverse(y, order=mm.BITREV)
+    assert torch.equal(z.view(torch.int64), x.view(torch.int64))
+
+
+# ------------------------------------------------------------------ poly_mul
+def test_poly_mul_c1(mm, O):
+    p, g = P30, 3
+    a = residues(config_seed(1), 1, 512, p)
+    b = residues(config_seed(1), 2, 512, p)
+    c = mm.poly_mul(dev(a), dev(b), p, g)
+    assert np.array_equal(u64(host(c)), O.poly_mul_schoolbook(a, b, p))
+
+
+@pytest.mark.parametrize("bits,p,g", [(32, P30, 3), (32, 469762049, 3), (64, PG, 7)])
+def test_poly_mul_ragged(mm, O, bits, p, g):
+    rng = random.Random(bits)
+    cases = [(1, 1, 1), (1, 7, 2), (3, 2, 5), (511, 513, 3), (1000, 24, 2), (2049, 2048, 2), (3000, 5000, 2),
+             (1 << 13, 1 << 13, 1), (12345, 777, 1)]
+    for la, lb, batch in cases:
+        a = residues(rng.randrange(1 << 30), 1, la * batch, p).reshape(batch, la)
+        b = residues(rng.randrange(1 << 30), 2, lb * batch, p).reshape(batch, lb)
+        c = u64(host(mm.poly_mul(dev(a), dev(b), p, g, word_bits=bits)))
+        for r in range(batch):
+            ref = O.poly_mul_schoolbook(a[r], b[r], p) if la * lb <= 1 << 22 else O.poly_mul_ntt(a[r], b[r], p, g)
+            assert np.array_equal(c[r], ref), (la, lb, r)
+
+
+def test_poly_mul_c3_small_batch(mm, O):
+    p, g = P30, 3
+    B, d = 8, 1 << 15
+    a = residues(config_seed(3), 1, B * d, p).reshape(B, d)
+    b = residues(config_seed(3), 2, B * d, p).reshape(B, d)
+    c = u64(host(mm.poly_mul(dev(a), dev(b), p, g)))
+    for r in range(B):
+        assert np.array_equal(c[r], O.poly_mul_ntt(a[r], b[r], p, g)), r
+
+
+def test_poly_mul_c3_full_sampled(mm, O):
+    # BASELINE C3 product: 4096 pairs of degree < 2^15 (bench launch config);
+    # every row checked by c(r) = a(r) b(r) at a random point, 3 rows in full.
+    p, g, B, d = P30, 3, 4096, 1 << 15
+    a = gen.residues_torch(config_seed(3), 1, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    b = gen.residues_torch(config_seed(3), 2, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    c = mm.poly_mul(a, b, p, g)
+    ah, bh, ch = host(a), host(b), host(c)
+    rng = random.Random(3)
+    for r in range(0, B, 1):
+        x = rng.randrange(1, p)
+        assert O.poly_eval(ch[r], x, p) == O.mulmod(O.poly_eval(ah[r], x, p), O.poly_eval(bh[r], x, p), p), r
+    for r in (0, 2047, 4095):
+        assert np.array_equal(u64(ch[r]), O.poly_mul_ntt(ah[r], bh[r], p, g)), r
+
+
+# ------------------------------------------------------------------ int_mul
+def _to_int(limbs):
+    return int.from_bytes(np.asarray(limbs, dtype="<u2").tobytes(), "little")
+
+
+@pytest.mark.parametrize("na,nb", [(1, 1), (2, 2), (3, 1), (300, 257), (2048, 2049), (4096, 4096),
+                                   (5000, 3), (10000, 12345)])
+def test_int_mul_random(mm, O, na, nb):
+    a, b = limbs16(na, 1, na), limbs16(nb, 2, nb)
+    c = host(mm.int_mul_u16(dev(a), dev(b)))
+    assert _to_int(c) == _to_int(a) * _to_int(b)
+    if na * nb <= 1 << 24:
+        assert np.array_equal(c, O.int_mul_schoolbook_u16(a, b))
+
+
+@pytest.mark.parametrize("N", [1, 2, 4095, 4097, 1 << 16])
+def test_int_mul_all_ffff(mm, O, N):
+    # (2^(16N) - 1)^2 = [1, 0 x (N-1), 0xFFFE, 0xFFFF x (N-1)]: max carries & coefficients
+    a = np.full(N, 0xFFFF, dtype=np.uint16)
+    c = host(mm.int_mul_u16(dev(a), dev(a)))
+    expect = np.array([1] + [0] * (N - 1) + [0xFFFE] + [0xFFFF] * (N - 1), dtype=np.uint16)
+    assert np.array_equal(c, expect)
+
+
+def test_int_mul_medium_vs_oracle(mm, O):
+    n = 1 << 18
+    a, b = limbs16(7, 1, n), limbs16(7, 2, n)
+    c = host(mm.int_mul_u16(dev(a), dev(b)))
+    assert np.array_equal(c, O.int_mul_ntt_u16(a, b))
+
+
+def test_int_mul_c5_full_sampled(mm, O):
+    # BASELINE C5: two 2^28-bit integers (2^24 limbs) -> 2^25 limbs
+    n = 1 << 24
+    a = gen.limbs16_torch(config_seed(5), 1, n, DEV).view(torch.uint16)
+    b = gen.limbs16_torch(config_seed(5), 2, n, DEV).view(torch.uint16)
+    c = host(mm.int_mul_u16(a, b))
+    ah, bh = host(a), host(b)
+    assert np.array_equal(ah[:100], limbs16(config_seed(5), 1, 100))
+    # (i) low-limb exactness: c mod 2^(16K) = (a mod 2^16K)(b mod 2^16K) mod 2^16K
+    K = 4096
+    low = O.int_mul_schoolbook_u16(ah[:K], bh[:K])[:K]
+    assert np.array_equal(c[:K], low)
+    # (ii) casting out primes: c = a b (mod q) for 61-bit primes q
+    for q in ((1 << 61) - 1, 2305843009213693921, 1152921504606846883):
+        assert O.limbs_mod(c, q) == O.mulmod(O.limbs_mod(ah, q), O.limbs_mod(bh, q), q)
+    # (iii) the top limb is consistent with the exact bit length bound
+    assert c.size == 2 * n
+
+
+# ------------------------------------------------------------------ four-step blocks
+@pytest.mark.parametrize("bits,p,g,k", [(32, P30, 3, 16), (64, PG, 7, 20)])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_fourstep_blocks_loopback(mm, O, bits, p, g, k, G):
+    """Distributed layout on one GPU: G virtual ranks, column-block shards, a
+    loopback all-to-all; equals the single-GPU transform slice by slice."""
+    w = O.root_of_unity(g, k, p)
+    plan = mm.NttPlan(bits, p, k, w, 1)
+    inf = plan.info()
+    n1, n2 = inf["n1"], inf["n2"]
+    x = residues(11, k, 1 << k, p)
+    xt = dev(x).reshape(n2, n1)
+    ref = plan.forward(dev(x), out=dev(x).clone(), order=mm.BITREV).reshape(n2, n1)
+    c1, r2 = n1 // G, n2 // G
+    colout = []
+    for r in range(G):
+        blk = xt[:, r * c1:(r + 1) * c1].contiguous()
+        colout.append(plan.fwd_cols(blk, torch.empty_like(blk), r * c1, c1))
+    rows = []
+    for h in range(G):   # rank h receives rows [h r2, (h+1) r2) of every rank's columns
+        full = torch.cat([colout[g_][h * r2:(h + 1) * r2] for g_ in range(G)], dim=1).contiguous()
+        rows.append(plan.fwd_rows(full, full, h * r2, r2))
+    got = torch.cat(rows, dim=0)
+    assert torch.equal(got.view(torch.int64 if bits == 64 else torch.int32),
+                       ref.view(torch.int64 if bits == 64 else torch.int32))
+    # inverse: rows -> loopback all-to-all back -> cols
+    inv_rows = [plan.inv_rows(rows[h], torch.empty_like(rows[h]), h * r2, r2) for h in range(G)]
+    back = []
+    for r in range(G):
+        blk = torch.cat([inv_rows[h][:, r * c1:(r + 1) * c1] for h in range(G)], dim=0).contiguous()
+        back.append(plan.inv_cols(blk, torch.empty_like(blk), r * c1, c1))
+    xr = torch.cat(back, dim=1)
+    assert np.array_equal(host(xr).reshape(-1), x)

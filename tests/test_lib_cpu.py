@@ -1,0 +1,70 @@
+"""CPU-side checks of the C-ABI library (no GPU): it builds for sm_100a,
+loads, exports every symbol include/mmntt.h declares, and its host-side
+argument validation returns the documented statuses without touching a GPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import torch  # noqa: F401  (loads libcudart before libmmntt)
+    from paper_1407_3383_b200._build import build
+    build()
+    import paper_1407_3383_b200 as m
+    m.lib()
+    return m
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "mmntt.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mm_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(mm):
+    names = _header_functions()
+    assert len(names) >= 20
+    L = mm.lib()
+    for n in names:
+        assert hasattr(L, n), n
+        assert n in mm.EXPORTS, n
+    out = subprocess.run(["nm", "-D", "--defined-only", mm._LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_sass_is_sm100a(mm):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", mm._LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_codes_host_side(mm):
+    L = mm.lib()
+    h = ctypes.c_void_p()
+    assert L.mm_mod32_create(4, ctypes.byref(h)) == 1          # even -> invalid modulus
+    assert L.mm_mod32_create(2, ctypes.byref(h)) == 1
+    assert L.mm_mod32_create(91, ctypes.byref(h)) == 1         # 7 * 13 composite
+    assert b"prime" in L.mm_last_error()
+    # NTT plan argument validation happens before any device work
+    P30 = 998244353
+    assert L.mm_ntt_plan_create(32, 3221225473, 10, 5, 1, ctypes.byref(h)) == 2   # p >= 2^30: profile
+    assert L.mm_ntt_plan_create(32, P30, 24, 3, 1, ctypes.byref(h)) == 3          # 2^24 does not divide p-1
+    assert L.mm_ntt_plan_create(32, P30, 10, 2, 1, ctypes.byref(h)) == 4          # 2 is not a 2^10-th root
+    assert L.mm_ntt_plan_create(64, P30, 10, 2, 1, ctypes.byref(h)) == 1          # 64-bit: Goldilocks only
+    assert L.mm_ntt_plan_create(16, P30, 10, 2, 1, ctypes.byref(h)) == 10
+    assert L.mm_ntt_plan_create(32, P30, 10, 3, 0, ctypes.byref(h)) == 10         # batch 0
+    assert L.mm_poly_mul(32, P30, 3, None, 1, None, 1, None, 1, None) == 10
+    # int_mul coefficient bound: min(na, nb) (2^16-1)^2 must stay below p
+    dummy = ctypes.c_void_p(1 << 40)
+    dummy2 = ctypes.c_void_p(1 << 41)
+    dummy3 = ctypes.c_void_p(1 << 42)
+    assert L.mm_int_mul_u16(dummy, 1 << 33, dummy2, 1 << 33, dummy3, None) == 6
+    # aliasing is rejected
+    assert L.mm_int_mul_u16(dummy, 100, dummy2, 100, dummy, None) == 7
