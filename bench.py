@@ -146,7 +146,7 @@ def max_over_ranks(world, value: float) -> float:
     return float(t.item())
 
 
-def timed(fn, steps, warmup, world, stream=None):
+def timed(fn, steps, warmup, world, stream=None, on_start=None, on_stop=None):
     """W untimed steps, then K steps bracketed by barrier + synchronize; CUDA
     events on the launching stream; returns max-over-ranks ms for K steps."""
     import torch
@@ -155,12 +155,16 @@ def timed(fn, steps, warmup, world, stream=None):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
+    if on_start:
+        on_start()
     st = stream or torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(steps):
         fn()
     e1.record(st)
+    if on_stop:
+        on_stop()
     torch.cuda.synchronize()
     barrier(world)
     return max_over_ranks(world, e0.elapsed_time(e1))
@@ -339,12 +343,12 @@ def run_ours(args, world, rank, local):
 
     step()   # plan + workspace creation outside the timed region
     torch.cuda.synchronize()
-    n0 = mm.launch_count()
+    cnt = {}
     with ClockSampler(local) as clk:
-        mm.prof_enable(True)
-        ms_total = timed(step, args.steps, args.warmup, world)
-        mm.prof_enable(False)
-    launches = (mm.launch_count() - n0) // (args.steps + args.warmup) * args.steps
+        ms_total = timed(step, args.steps, args.warmup, world,
+                         on_start=lambda: (cnt.__setitem__("n0", mm.launch_count()), mm.prof_enable(True)),
+                         on_stop=lambda: (mm.prof_enable(False), cnt.__setitem__("n1", mm.launch_count())))
+    launches = cnt["n1"] - cnt["n0"]
     prof = mm.prof_collect()
     ms_step = ms_total / args.steps
     bfly_step = c3_butterflies(B)

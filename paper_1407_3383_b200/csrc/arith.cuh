@@ -121,6 +121,19 @@ struct Fp32 {
         x = xx + t;
         y = xx - t + p2;
     }
+    // butterflies with twiddle w^0 = 1 (no product)
+    __device__ __forceinline__ void dif1(uint32_t& x, uint32_t& y) const {
+        uint32_t s = x + y;
+        uint32_t d = x - y + p2;
+        x = umin32(s, s - p2);
+        y = umin32(d, d - p2);
+    }
+    __device__ __forceinline__ void dit1(uint32_t& x, uint32_t& y) const {
+        uint32_t xx = umin32(x, x - p2);
+        uint32_t yy = umin32(y, y - p2);
+        x = xx + yy;
+        y = xx - yy + p2;
+    }
     // [0, 4p) -> [0, p)
     __device__ __forceinline__ uint32_t canon(uint32_t x) const {
         x = umin32(x, x - p2);
@@ -188,6 +201,12 @@ struct FpG {
         y = sub(x, t);
         x = s;
     }
+    __device__ __forceinline__ void dif1(uint64_t& x, uint64_t& y) const {
+        uint64_t s = add(x, y);
+        y = sub(x, y);
+        x = s;
+    }
+    __device__ __forceinline__ void dit1(uint64_t& x, uint64_t& y) const { dif1(x, y); }
     __device__ __forceinline__ uint64_t mul_redc(uint64_t x, uint64_t y) const { return mul(x, y); }
 };
 

@@ -11,7 +11,7 @@
 //   Proposition 15), i.e. the TFT order with no transposition at all.
 //   The inverse runs the steps backwards with w^-1.
 #include "common.h"
-#include "ntt_core.cuh"
+#include "ntt_kernels.cuh"
 #include <new>
 #include <map>
 #include <mutex>
@@ -19,249 +19,6 @@
 #include <vector>
 
 namespace mm {
-
-constexpr int NT = 256;            // threads per CTA for tile kernels
-constexpr int MAX_BLOCK_LOG = 12;
-constexpr size_t SMEM_MAX = 227 * 1024;   // max dynamic shared memory per CTA on sm_100  // single-pass limit / four-step sub-transform limit (rows may be 13)
-
-template <class F> struct Radix { enum { R = 16 }; };
-template <> struct Radix<FpG> { enum { R = 8 }; };
-
-// ---------------------------------------------------------------- loaders
-template <class TIn, class T> __device__ __forceinline__ T ld_conv(const TIn* p) { return (T)__ldg(p); }
-
-template <class T> __host__ __device__ __forceinline__ int srow_len(int L, bool odd) {
-    // padded row length; for the column pass additionally odd in bank units so
-    // that column-wise (c-fastest) accesses spread over all banks
-    int s = sizeof(T) == 4 ? L + (L >> 5) : L + (L >> 4);
-    if (!odd) return s;
-    const int B = sizeof(T) == 4 ? 32 : 16;
-    return s + ((1 - s % B) + B) % B;
-}
-
-template <class F> __device__ __forceinline__ typename F::T fs_twiddle(const F& f, typename F::T v,
-                                                                       const typename F::W* lo,
-                                                                       const typename F::W* hi, int h,
-                                                                       uint64_t e) {
-    // w^e = w^(e mod 2^h) * w^(2^h (e >> h)) -- two fixed-multiplicand products
-    v = f.mulw(v, lo[e & ((1ull << h) - 1)]);
-    return f.mulw(v, hi[e >> h]);
-}
-
-template <class W> __device__ __forceinline__ void stage_twiddles(W* dst, const W* src, int L) {
-    for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = src[i];
-}
-
-// ---------------------------------------------------------------- row pass
-template <class F> struct RowArgs {
-    typedef typename F::W W;
-    const void* in;
-    void* out;
-    long long nrows, in_rs, out_rs, in_len, out_len, row0;
-    int k, C, perm, fs, k2, scale, canon;
-    W sc;
-    const W* lvl;
-    const W* fs_lo;
-    const W* fs_hi;
-    int fs_h;
-    int tw_smem;          // 1: stage the level table in shared memory; 0: read it via L1/L2
-};
-
-// Forward (INV=false): DIF along each row; perm=1 writes natural order.
-// Inverse (INV=true): DIT along each row (input bit-mirrored positions; perm=1
-// means the input is in natural order and is permuted on load); fs=1 applies
-// the four-step twiddle w^-(j1 [i2]) with i2 = (row0 + r) mod 2^k2.
-template <class F, bool INV, class TIn, class TOut>
-__global__ void __launch_bounds__(NT) k_rows(F f, RowArgs<F> a) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int L = 1 << a.k;
-    W* tws = (W*)smem_raw;
-    T* s = (T*)(tws + (a.tw_smem ? L : 0));
-    const int srow = srow_len<T>(L, false);
-    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
-    const W* tw = a.tw_smem ? tws : a.lvl;
-    const TIn* in = (const TIn*)a.in;
-    TOut* out = (TOut*)a.out;
-    const long long ntiles = (a.nrows + a.C - 1) / a.C;
-    const int per = a.C * L;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long r0 = tile * a.C;
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int c = e >> a.k, j = e & (L - 1);
-            long long r = r0 + c;
-            T v = 0;
-            if (r < a.nrows && j < a.in_len) v = ld_conv<TIn, T>(in + r * a.in_rs + j);
-            int pos = (INV && a.perm) ? brev(j, a.k) : j;
-            s[c * srow + spad<T>(pos)] = v;
-        }
-        __syncthreads();
-        if (INV) tile_dit<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
-        else tile_dif<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int c = e >> a.k, j = e & (L - 1);
-            long long r = r0 + c;
-            if (r >= a.nrows || j >= a.out_len) continue;
-            int pos = (!INV && a.perm) ? brev(j, a.k) : j;
-            T v = s[c * srow + spad<T>(pos)];
-            if (INV && a.fs) {
-                long long i2 = (a.row0 + r) & ((1ll << a.k2) - 1);
-                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)j * (uint64_t)brev((int)i2, a.k2));
-            }
-            if (a.scale) v = f.mulw(v, a.sc);
-            if (a.canon) v = f.canon(v);
-            out[r * a.out_rs + j] = (TOut)v;
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------- column pass
-template <class F> struct ColArgs {
-    typedef typename F::W W;
-    const void* in;
-    void* out;
-    long long ncols, nbatch, in_rs, out_rs, in_bs, out_bs, in_len, out_len, col0, n1;
-    int k, C, fs, scale, canon;
-    W sc;
-    const W* lvl;
-    const W* fs_lo;
-    const W* fs_hi;
-    int fs_h;
-    int tw_smem;
-};
-
-// Forward: DIF along columns (length 2^k, stride in_rs), output rows in
-// bit-mirrored order with twiddle w^(j1 [i2]) (Algorithm 1 steps 1-2).
-// Inverse: DIT along columns (input rows i2 bit-mirrored), natural output,
-// optional n^-1 scaling and canonicalisation.
-template <class F, bool INV, class TIn, class TOut>
-__global__ void __launch_bounds__(NT) k_cols(F f, ColArgs<F> a) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int L = 1 << a.k;
-    W* tws = (W*)smem_raw;
-    T* s = (T*)(tws + (a.tw_smem ? L : 0));
-    const int srow = srow_len<T>(L, true);
-    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
-    const W* tw = a.tw_smem ? tws : a.lvl;
-    const TIn* in = (const TIn*)a.in;
-    TOut* out = (TOut*)a.out;
-    const long long cgroups = (a.ncols + a.C - 1) / a.C;
-    const long long ntiles = cgroups * a.nbatch;
-    const int per = a.C * L;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long b = tile / cgroups;
-        const long long cl0 = (tile - b * cgroups) * a.C;    // local column of this tile
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int t = e / a.C, c = e - t * a.C;
-            long long cl = cl0 + c;
-            T v = 0;
-            if (cl < a.ncols && (long long)t * a.n1 + a.col0 + cl < a.in_len)
-                v = ld_conv<TIn, T>(in + b * a.in_bs + (long long)t * a.in_rs + cl);
-            s[c * srow + spad<T>(t)] = v;
-        }
-        __syncthreads();
-        if (INV) tile_dit<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
-        else tile_dif<F, Radix<F>::R>(f, s, srow, a.C, a.k, tw);
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int t = e / a.C, c = e - t * a.C;
-            long long cl = cl0 + c;
-            if (cl >= a.ncols || (long long)t * a.n1 + a.col0 + cl >= a.out_len) continue;
-            T v = s[c * srow + spad<T>(t)];
-            if (!INV && a.fs)
-                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)(a.col0 + cl) * (uint64_t)brev(t, a.k));
-            if (a.scale) v = f.mulw(v, a.sc);
-            if (a.canon) v = f.canon(v);
-            out[b * a.out_bs + (long long)t * a.out_rs + cl] = (TOut)v;
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------- fused product rows
-template <class F> struct PmulArgs {
-    typedef typename F::W W;
-    const void* a;
-    const void* b;
-    void* c;
-    long long nrows, a_rs, b_rs, c_rs, la, lb, lc, row0;
-    int k, C, fs, k2;
-    W sc;                 // pointwise post-multiplier (n^-1, times 2^32 for REDC)
-    const W* lvl_f;
-    const W* lvl_i;
-    const W* fs_lo;       // inverse four-step twiddles
-    const W* fs_hi;
-    int fs_h;
-    int canon;
-    int tw_smem;
-};
-
-// For each row r: A = DIF(a_r), B = DIF(b_r) (inputs zero-padded to 2^k),
-// C = A .* B * sc, c_r = DIT(C) [* w^-(j1 [i2]) when fs] -- P:952 "two
-// direct TFT and one inverse TFT ... and the entry-wise vector product".
-template <class F, class TIn, class TOut>
-__global__ void __launch_bounds__(NT) k_rows_pmul(F f, PmulArgs<F> a) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int L = 1 << a.k;
-    W* twfs = (W*)smem_raw;
-    W* twis = twfs + (a.tw_smem ? L : 0);
-    T* sa = (T*)(twis + (a.tw_smem ? L : 0));
-    const int srow = srow_len<T>(L, false);
-    T* sb = sa + a.C * srow;
-    if (a.tw_smem) {
-        stage_twiddles(twfs, a.lvl_f, L);
-        stage_twiddles(twis, a.lvl_i, L);
-    }
-    const W* twf = a.tw_smem ? twfs : a.lvl_f;
-    const W* twi = a.tw_smem ? twis : a.lvl_i;
-    const TIn* A = (const TIn*)a.a;
-    const TIn* B = (const TIn*)a.b;
-    TOut* Cp = (TOut*)a.c;
-    const long long ntiles = (a.nrows + a.C - 1) / a.C;
-    const int per = a.C * L;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long r0 = tile * a.C;
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int c = e >> a.k, j = e & (L - 1);
-            long long r = r0 + c;
-            T va = 0, vb = 0;
-            if (r < a.nrows) {
-                if (j < a.la) va = ld_conv<TIn, T>(A + r * a.a_rs + j);
-                if (j < a.lb) vb = ld_conv<TIn, T>(B + r * a.b_rs + j);
-            }
-            sa[c * srow + spad<T>(j)] = va;
-            sb[c * srow + spad<T>(j)] = vb;
-        }
-        __syncthreads();
-        tile_dif<F, Radix<F>::R>(f, sa, srow, a.C, a.k, twf);
-        tile_dif<F, Radix<F>::R>(f, sb, srow, a.C, a.k, twf);
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int c = e >> a.k, j = e & (L - 1);
-            int ix = c * srow + spad<T>(j);
-            sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
-        }
-        __syncthreads();
-        tile_dit<F, Radix<F>::R>(f, sa, srow, a.C, a.k, twi);
-        for (int e = threadIdx.x; e < per; e += NT) {
-            int c = e >> a.k, j = e & (L - 1);
-            long long r = r0 + c;
-            if (r >= a.nrows || j >= a.lc) continue;
-            T v = sa[c * srow + spad<T>(j)];
-            if (a.fs) {
-                long long i2 = (a.row0 + r) & ((1ll << a.k2) - 1);
-                v = fs_twiddle(f, v, a.fs_lo, a.fs_hi, a.fs_h, (uint64_t)j * (uint64_t)brev((int)i2, a.k2));
-            }
-            if (a.canon) v = f.canon(v);
-            Cp[r * a.c_rs + j] = (TOut)v;
-        }
-        __syncthreads();
-    }
-}
 
 // ---------------------------------------------------------------- bit-mirror permutation
 template <class T>
@@ -322,6 +79,17 @@ template <class W, class E>
 __global__ void k_pow_table(W* t, long long cnt, E w, uint64_t step, uint64_t p) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
         tw_set(t, i, (E)tw_pow(w, (uint64_t)i * step, p), p);
+}
+
+// full step-2 table: t[i2 n1 + j1] = w^(j1 [i2]_k2)
+template <class W, class E>
+__global__ void k_fs_table(W* t, int k1, int k2, E w, uint64_t p) {
+    const long long cnt = 1ll << (k1 + k2);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
+        long long i2 = i >> k1, j1 = i & ((1ll << k1) - 1);
+        uint64_t e = (uint64_t)j1 * (uint64_t)brev((int)i2, k2);
+        tw_set(t, i, (E)tw_pow(w, e, p), p);
+    }
 }
 
 // ---------------------------------------------------------------- carries (int_mul)
@@ -479,6 +247,8 @@ struct mm_ntt_plan {
     void* fs_hi_f = nullptr;
     void* fs_lo_i = nullptr;
     void* fs_hi_i = nullptr;
+    void* fs_full_f = nullptr; // full step-2 tables [i2][j1] (small n only)
+    void* fs_full_i = nullptr;
     int fs_h = 0;
     uint64_t ninv;           // n^-1 mod p
     uint64_t ninv_r;         // n^-1 2^32 mod p (32-bit: after REDC)
@@ -509,95 +279,22 @@ template <> uint64_t host_w<uint64_t>(uint64_t w, uint64_t) { return w; }
 
 static size_t esize(int word_bits) { return word_bits == 32 ? 4 : 8; }
 
-template <class K> static mm_status set_smem(K kern, size_t bytes) {
-    static std::mutex m;
-    std::lock_guard<std::mutex> g(m);
-    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    return MM_OK;
-}
 
-template <class K> static int grid_for(K kern, size_t smem, long long tiles) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
-    if (per_sm < 1) per_sm = 1;
-    long long cap = (long long)num_sms() * per_sm;
-    return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
-}
+constexpr int MAX_BLOCK_LOG = 12;   // single-pass limit (longer transforms use Algorithm 1)
 
-template <class T> static int rows_per_tile(int k) {
-    int budget = sizeof(T) == 4 ? 8192 : 4096;   // elements per tile
-    int L = 1 << k;
-    return L >= budget ? 1 : budget / L;
-}
-template <class T> static int cols_per_tile(int k) {
-    int minc = 32 / (int)sizeof(T);             // one 32-byte sector per row
-    int maxc = 128 / (int)sizeof(T);            // one 128-byte line per row
-    int budget = sizeof(T) == 4 ? 8192 : 4096;
-    int c = budget >> k;
-    if (c < minc) c = minc;
-    if (c > maxc) c = maxc;
-    return c;
-}
-
-
-// ---- launchers
-template <class F, bool INV, class TIn, class TOut>
-static mm_status launch_rows(const F& f, RowArgs<F>& a, cudaStream_t st) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    int L = 1 << a.k;
-    size_t data = (size_t)a.C * srow_len<T>(L, false) * sizeof(T);
-    a.tw_smem = data + (size_t)L * sizeof(W) <= SMEM_MAX;
-    size_t smem = data + (a.tw_smem ? (size_t)L * sizeof(W) : 0);
-    auto kern = k_rows<F, INV, TIn, TOut>;
-    mm_status s = set_smem(kern, smem);
-    if (s != MM_OK) return s;
-    long long tiles = (a.nrows + a.C - 1) / a.C;
-    {
-        LaunchScope ls(INV ? "ntt_rows_inv" : "ntt_rows_fwd", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
-    }
-    MM_LAUNCH_CHECK();
-    return MM_OK;
-}
-template <class F, bool INV, class TIn, class TOut>
-static mm_status launch_cols(const F& f, ColArgs<F>& a, cudaStream_t st) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    int L = 1 << a.k;
-    size_t data = (size_t)a.C * srow_len<T>(L, true) * sizeof(T);
-    a.tw_smem = data + (size_t)L * sizeof(W) <= SMEM_MAX;
-    size_t smem = data + (a.tw_smem ? (size_t)L * sizeof(W) : 0);
-    auto kern = k_cols<F, INV, TIn, TOut>;
-    mm_status s = set_smem(kern, smem);
-    if (s != MM_OK) return s;
-    long long tiles = (a.ncols + a.C - 1) / a.C * a.nbatch;
-    {
-        LaunchScope ls(INV ? "ntt_cols_inv" : "ntt_cols_fwd", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
-    }
-    MM_LAUNCH_CHECK();
-    return MM_OK;
-}
-template <class F, class TIn, class TOut>
-static mm_status launch_pmul(const F& f, PmulArgs<F>& a, cudaStream_t st) {
-    typedef typename F::T T;
-    typedef typename F::W W;
-    int L = 1 << a.k;
-    size_t data = 2 * (size_t)a.C * srow_len<T>(L, false) * sizeof(T);
-    a.tw_smem = data + 2 * (size_t)L * sizeof(W) <= SMEM_MAX;
-    size_t smem = data + (a.tw_smem ? 2 * (size_t)L * sizeof(W) : 0);
-    auto kern = k_rows_pmul<F, TIn, TOut>;
-    mm_status s = set_smem(kern, smem);
-    if (s != MM_OK) return s;
-    long long tiles = (a.nrows + a.C - 1) / a.C;
-    {
-        LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
-    }
-    MM_LAUNCH_CHECK();
-    return MM_OK;
-}
+// explicit instantiations live in ntt_inst32.cu / ntt_inst64.cu
+extern template mm_status launch_rows<Fp32, false, uint32_t, uint32_t>(const Fp32&, const RowArgs<Fp32>&, cudaStream_t);
+extern template mm_status launch_rows<Fp32, true, uint32_t, uint32_t>(const Fp32&, const RowArgs<Fp32>&, cudaStream_t);
+extern template mm_status launch_cols<Fp32, false, uint32_t, uint32_t>(const Fp32&, const ColArgs<Fp32>&, cudaStream_t);
+extern template mm_status launch_cols<Fp32, true, uint32_t, uint32_t>(const Fp32&, const ColArgs<Fp32>&, cudaStream_t);
+extern template mm_status launch_pmul<Fp32, uint32_t, uint32_t>(const Fp32&, const PmulArgs<Fp32>&, cudaStream_t);
+extern template mm_status launch_rows<FpG, false, uint64_t, uint64_t>(const FpG&, const RowArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_rows<FpG, true, uint64_t, uint64_t>(const FpG&, const RowArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_cols<FpG, false, uint64_t, uint64_t>(const FpG&, const ColArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_cols<FpG, true, uint64_t, uint64_t>(const FpG&, const ColArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_cols<FpG, false, uint16_t, uint64_t>(const FpG&, const ColArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_pmul<FpG, uint64_t, uint64_t>(const FpG&, const PmulArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_pmul<FpG, uint16_t, uint64_t>(const FpG&, const PmulArgs<FpG>&, cudaStream_t);
 
 // ---- plan construction
 template <class W, class E>
@@ -619,6 +316,19 @@ static mm_status build_pow(void** dst, long long cnt, E w, uint64_t step, uint64
     {
         LaunchScope ls("twiddle_pow_table", 0);
         k_pow_table<W, E><<<grid, 256>>>((W*)*dst, cnt, w, step, p);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+template <class W, class E>
+static mm_status build_fs_full(void** dst, int k1, int k2, E w, uint64_t p) {
+    long long cnt = 1ll << (k1 + k2);
+    MM_CUDA_TRY(cudaMalloc(dst, (size_t)cnt * sizeof(W)));
+    int grid = (int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096);
+    {
+        LaunchScope ls("twiddle_fs_table", 0);
+        k_fs_table<W, E><<<grid, 256>>>((W*)*dst, k1, k2, w, p);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
@@ -648,6 +358,11 @@ static mm_status build_tables(mm_ntt_plan* P) {
         if ((s = build_pow<W, E>(&P->fs_hi_f, nhi, (E)w, 1ull << h, p)) != MM_OK) return s;
         if ((s = build_pow<W, E>(&P->fs_lo_i, nlo, (E)winv, 1, p)) != MM_OK) return s;
         if ((s = build_pow<W, E>(&P->fs_hi_i, nhi, (E)winv, 1ull << h, p)) != MM_OK) return s;
+        // full tables TW[i2 n1 + j1] = w^(+-j1 [i2]) when they stay L2-resident (<= 2 MiB)
+        if (((size_t)1 << k) * sizeof(W) <= (2u << 20)) {
+            if ((s = build_fs_full<W, E>(&P->fs_full_f, P->k1, P->k2, (E)w, p)) != MM_OK) return s;
+            if ((s = build_fs_full<W, E>(&P->fs_full_i, P->k1, P->k2, (E)winv, p)) != MM_OK) return s;
+        }
     }
     MM_CUDA_TRY(cudaDeviceSynchronize());
     return MM_OK;
@@ -655,7 +370,8 @@ static mm_status build_tables(mm_ntt_plan* P) {
 
 static void free_plan(mm_ntt_plan* P) {
     if (!P) return;
-    void* bufs[] = {P->lvl_f1, P->lvl_i1, P->lvl_f2, P->lvl_i2, P->fs_lo_f, P->fs_hi_f, P->fs_lo_i, P->fs_hi_i, P->ws};
+    void* bufs[] = {P->lvl_f1,  P->lvl_i1,  P->lvl_f2,    P->lvl_i2,    P->fs_lo_f, P->fs_hi_f,
+                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->ws};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -668,7 +384,7 @@ static mm_status check_modulus(int word_bits, uint64_t p, int log2n) {
         if (log2n < 1 || log2n > 24) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,24]", log2n);
     } else if (word_bits == 64) {
         if (p != FpG::P) return set_err(MM_E_INVALID_MODULUS, "64-bit NTT supports only p = 2^64 - 2^32 + 1");
-        if (log2n < 1 || log2n > 26) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,26]", log2n);
+        if (log2n < 1 || log2n > 25) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,25]", log2n);
     } else {
         return set_err(MM_E_ARG, "word_bits must be 32 or 64");
     }
@@ -694,9 +410,14 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
         P->k1 = log2n;
         P->k2 = 0;
     } else {
-        // n1 (row length, contiguous) >= n2 (column length, strided)
-        P->k2 = log2n / 2;
-        P->k1 = log2n - P->k2;
+        // n1 (row length, contiguous) >= n2 (column length, strided); the
+        // column pass keeps <= 2^10 (32-bit) / 2^11 (64-bit) points per column
+        // tile so that several CTAs share an SM; rows go up to 2^13.
+        int cap = word_bits == 32 ? 10 : 11;
+        int k2 = log2n / 2 < cap ? log2n / 2 : cap;
+        if (log2n - k2 > 13) k2 = log2n - 13;
+        P->k2 = k2;
+        P->k1 = log2n - k2;
     }
     P->ninv = hpowmod(n % p, p - 2, p);
     P->ninv_r = word_bits == 32 ? hmulmod(P->ninv, ((u128)1 << 32) % p, p) : P->ninv;
@@ -738,7 +459,6 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         a.in_rs = a.out_rs = n;
         a.in_len = a.out_len = n;
         a.k = P->k;
-        a.C = rows_per_tile<T>(P->k);
         a.perm = order == MM_ORDER_NATURAL;
         a.canon = 1;
         a.lvl = (const W*)P->lvl_f1;
@@ -755,11 +475,11 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     c.col0 = 0;
     c.n1 = 1ll << P->k1;
     c.k = P->k2;
-    c.C = cols_per_tile<T>(P->k2);
     c.fs = 1;
     c.lvl = (const W*)P->lvl_f2;
     c.fs_lo = (const W*)P->fs_lo_f;
     c.fs_hi = (const W*)P->fs_hi_f;
+    c.fs_full = (const W*)P->fs_full_f;
     c.fs_h = P->fs_h;
     mm_status s = launch_cols<F, false, T, T>(f, c, st);
     if (s != MM_OK) return s;
@@ -769,7 +489,6 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     a.in_rs = a.out_rs = 1ll << P->k1;
     a.in_len = a.out_len = 1ll << P->k1;
     a.k = P->k1;
-    a.C = rows_per_tile<T>(P->k1);
     a.canon = 1;
     a.lvl = (const W*)P->lvl_f1;
     if ((s = launch_rows<F, false, T, T>(f, a, st)) != MM_OK) return s;
@@ -800,7 +519,6 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         a.in_rs = a.out_rs = n;
         a.in_len = a.out_len = n;
         a.k = P->k;
-        a.C = rows_per_tile<T>(P->k);
         a.perm = order == MM_ORDER_NATURAL;
         a.scale = 1; a.sc = sc;
         a.canon = 1;
@@ -826,11 +544,11 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     a.in_rs = a.out_rs = 1ll << P->k1;
     a.in_len = a.out_len = 1ll << P->k1;
     a.k = P->k1;
-    a.C = rows_per_tile<T>(P->k1);
     a.fs = 1; a.k2 = P->k2; a.row0 = 0;
     a.lvl = (const W*)P->lvl_i1;
     a.fs_lo = (const W*)P->fs_lo_i;
     a.fs_hi = (const W*)P->fs_hi_i;
+    a.fs_full = (const W*)P->fs_full_i;
     a.fs_h = P->fs_h;
     if ((s = launch_rows<F, true, T, T>(f, a, st)) != MM_OK) return s;
     // inverse column pass (DIT over i2, n^-1, canonical): out -> out
@@ -843,7 +561,6 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     c.in_len = c.out_len = n;
     c.n1 = 1ll << P->k1;
     c.k = P->k2;
-    c.C = cols_per_tile<T>(P->k2);
     c.scale = 1; c.sc = sc; c.canon = 1;
     c.lvl = (const W*)P->lvl_i2;
     return launch_cols<F, true, T, T>(f, c, st);
@@ -865,11 +582,11 @@ static mm_status fwd_cols_impl(mm_ntt_plan* P, const void* in, void* out, size_t
     c.col0 = (long long)col0;
     c.n1 = 1ll << P->k1;
     c.k = P->k2;
-    c.C = cols_per_tile<T>(P->k2);
     c.fs = 1;
     c.lvl = (const W*)P->lvl_f2;
     c.fs_lo = (const W*)P->fs_lo_f;
     c.fs_hi = (const W*)P->fs_hi_f;
+    c.fs_full = (const W*)P->fs_full_f;
     c.fs_h = P->fs_h;
     return launch_cols<F, false, T, T>(f, c, st);
 }
@@ -885,7 +602,6 @@ static mm_status rows_impl(mm_ntt_plan* P, const void* in, void* out, size_t row
     a.in_rs = a.out_rs = 1ll << P->k1;
     a.in_len = a.out_len = 1ll << P->k1;
     a.k = P->k1;
-    a.C = rows_per_tile<T>(P->k1);
     a.row0 = (long long)row0;
     a.k2 = P->k2;
     if (!inv) {
@@ -897,6 +613,7 @@ static mm_status rows_impl(mm_ntt_plan* P, const void* in, void* out, size_t row
     a.lvl = (const W*)P->lvl_i1;
     a.fs_lo = (const W*)P->fs_lo_i;
     a.fs_hi = (const W*)P->fs_hi_i;
+    a.fs_full = (const W*)P->fs_full_i;
     a.fs_h = P->fs_h;
     return launch_rows<F, true, T, T>(f, a, st);
 }
@@ -914,7 +631,6 @@ static mm_status inv_cols_impl(mm_ntt_plan* P, const void* in, void* out, size_t
     c.col0 = (long long)col0;
     c.n1 = 1ll << P->k1;
     c.k = P->k2;
-    c.C = cols_per_tile<T>(P->k2);
     c.scale = 1; c.sc = host_w<W>(P->ninv, P->p); c.canon = 1;
     c.lvl = (const W*)P->lvl_i2;
     return launch_cols<F, true, T, T>(f, c, st);
@@ -975,7 +691,6 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         m.a_rs = la; m.b_rs = lb; m.c_rs = lc;
         m.la = la; m.lb = lb; m.lc = lc;
         m.k = P->k;
-        m.C = rows_per_tile<T>(P->k) / 2 > 0 ? rows_per_tile<T>(P->k) / 2 : 1;
         m.sc = sc;
         m.canon = 1;
         m.lvl_f = (const W*)P->lvl_f1;
@@ -1000,11 +715,11 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         cc.in_len = op == 0 ? la : lb; cc.out_len = n;
         cc.n1 = n1;
         cc.k = P->k2;
-        cc.C = cols_per_tile<T>(P->k2);
         cc.fs = 1;
         cc.lvl = (const W*)P->lvl_f2;
         cc.fs_lo = (const W*)P->fs_lo_f;
         cc.fs_hi = (const W*)P->fs_hi_f;
+        cc.fs_full = (const W*)P->fs_full_f;
         cc.fs_h = P->fs_h;
         if ((s = launch_cols<F, false, TIn, T>(f, cc, st)) != MM_OK) return s;
     }
@@ -1015,13 +730,13 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     m.a_rs = m.b_rs = m.c_rs = n1;
     m.la = m.lb = m.lc = n1;
     m.k = P->k1;
-    m.C = rows_per_tile<T>(P->k1) / 2 > 0 ? rows_per_tile<T>(P->k1) / 2 : 1;
     m.fs = 1; m.k2 = P->k2; m.row0 = 0;
     m.sc = sc;
     m.lvl_f = (const W*)P->lvl_f1;
     m.lvl_i = (const W*)P->lvl_i1;
     m.fs_lo = (const W*)P->fs_lo_i;
     m.fs_hi = (const W*)P->fs_hi_i;
+    m.fs_full = (const W*)P->fs_full_i;
     m.fs_h = P->fs_h;
     if ((s = launch_pmul<F, T, T>(f, m, st)) != MM_OK) return s;
     // inverse column pass (step 1 inverse), canonical, truncated to lc
@@ -1034,7 +749,6 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     ci.in_len = n; ci.out_len = lc;
     ci.n1 = n1;
     ci.k = P->k2;
-    ci.C = cols_per_tile<T>(P->k2);
     ci.canon = 1;
     ci.lvl = (const W*)P->lvl_i2;
     return launch_cols<F, true, T, TOut>(f, ci, st);
