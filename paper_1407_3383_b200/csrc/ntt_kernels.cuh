@@ -24,23 +24,24 @@ template <class F> struct Cfg;
 template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, COLC = 32, V = 4 }; };
 template <> struct Cfg<FpG> { enum { RL = 3, BUDGET = 4096, COLC = 16, V = 2 }; };
 
-// Tiles of L <= 512 points use the interleaved layout [j][c] with C transforms
-// of 128 bytes per row (lane = transform: every access of every group is
-// conflict-free without padding); longer transforms use one padded row per
-// transform (RowLayout, pitch = 16 banks mod 32).
+// Column tiles of L <= 512 points use the interleaved layout [j][c] with C
+// transforms of 128 bytes per row (the global row-major order of the column
+// block; lane = transform: every access of every group is conflict-free
+// without padding); longer columns use one padded row per transform.
 template <class F, int LOGL> struct InterOK {
     enum { v = (size_t)Cfg<F>::COLC * (1u << LOGL) * sizeof(typename F::T) <= 64 * 1024 };
 };
+// Row tiles keep one padded row per transform: global accesses stay fully
+// coalesced (the interleaved layout made every warp access touch 32 lines).
 template <class F, int LOGL> struct RowsTile {
     typedef typename F::T T;
-    enum { C = InterOK<F, LOGL>::v ? Cfg<F>::COLC : ((Cfg<F>::BUDGET >> LOGL) > 0 ? (Cfg<F>::BUDGET >> LOGL) : 1) };
-    typedef typename std::conditional<InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>, RowLayout<T, LOGL, C>>::type Lay;
+    enum { C = (Cfg<F>::BUDGET >> LOGL) > 0 ? (Cfg<F>::BUDGET >> LOGL) : 1 };
+    typedef RowLayout<T, LOGL, C> Lay;
 };
 template <class F, int LOGL> struct PmulTile {
     typedef typename F::T T;
-    enum { C = InterOK<F, LOGL>::v ? Cfg<F>::COLC
-                                   : (((Cfg<F>::BUDGET / 2) >> LOGL) > 0 ? ((Cfg<F>::BUDGET / 2) >> LOGL) : 1) };
-    typedef typename std::conditional<InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>, RowLayout<T, LOGL, C>>::type Lay;
+    enum { C = ((Cfg<F>::BUDGET / 2) >> LOGL) > 0 ? ((Cfg<F>::BUDGET / 2) >> LOGL) : 1 };
+    typedef RowLayout<T, LOGL, C> Lay;
 };
 // column tiles: one 128-byte line per matrix row when it fits in 64 KiB
 // (ColLayout), else a 32-byte sector per row transposed into padded rows.
@@ -68,7 +69,7 @@ template <class F> struct RowArgs {
     const void* in;
     void* out;
     long long nrows, in_rs, out_rs, in_len, out_len, row0;
-    int k, k2, perm, fs, scale, canon, vec_in, vec_out, tw_smem;
+    int k, k2, perm, fs, scale, canon, vec_in, vec_out;
     W sc;
     const W* lvl;
     const W* fs_lo;
@@ -81,7 +82,7 @@ template <class F> struct ColArgs {
     const void* in;
     void* out;
     long long ncols, nbatch, in_rs, out_rs, in_bs, out_bs, in_len, out_len, col0, n1;
-    int k, fs, scale, canon, vec_in, vec_out, tw_smem;
+    int k, fs, scale, canon, vec_in, vec_out;
     W sc;
     const W* lvl;
     const W* fs_lo;
@@ -95,7 +96,7 @@ template <class F> struct PmulArgs {
     const void* b;
     void* c;
     long long nrows, a_rs, b_rs, c_rs, la, lb, lc, row0;
-    int k, k2, fs, canon, vec_in, vec_out, tw_smem;
+    int k, k2, fs, canon, vec_in, vec_out;
     W sc;                 // pointwise post-multiplier (n^-1, times 2^32 for the 32-bit REDC)
     const W* lvl_f;
     const W* lvl_i;
@@ -105,22 +106,16 @@ template <class F> struct PmulArgs {
     int fs_h;
 };
 
+// Epilogue selector (compile time): bits 0-1 = step-2 twiddle (0 none, 1 full
+// table, 2 two-level split table), bit 2 = multiply by a constant (n^-1),
+// bit 3 = canonicalise to [0, p).
+enum { EPI_FS_FULL = 1, EPI_FS_SPLIT = 2, EPI_SCALE = 4, EPI_CANON = 8 };
+
 // ---------------------------------------------------------------- helpers
 template <class TIn, class T> __device__ __forceinline__ T ld_conv(const TIn* p) { return (T)__ldg(p); }
 
 template <class W> __device__ __forceinline__ void stage_twiddles(W* dst, const W* src, int L) {
     for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = src[i];
-}
-
-// step-2 twiddle w^(j1 [i2]) (sign folded in the tables): full table or two-level split
-template <class F>
-__device__ __forceinline__ typename F::T fs_apply(const F& f, typename F::T v, const typename F::W* full,
-                                                  const typename F::W* lo, const typename F::W* hi, int h,
-                                                  long long i2, int k2, long long j1, long long n1) {
-    if (full) return f.mulw(v, __ldg(full + i2 * n1 + j1));
-    uint64_t e = (uint64_t)j1 * (uint64_t)brev((int)i2, k2);
-    v = f.mulw(v, __ldg(lo + (e & ((1ull << h) - 1))));
-    return f.mulw(v, __ldg(hi + (e >> h)));
 }
 
 template <class T> struct Vec;
@@ -138,155 +133,181 @@ template <class T> __device__ __forceinline__ typename Vec<T>::type vmake(const 
 template <> __device__ __forceinline__ uint4 vmake<uint32_t>(const uint32_t* i) { return make_uint4(i[0], i[1], i[2], i[3]); }
 template <> __device__ __forceinline__ ulonglong2 vmake<uint64_t>(const uint64_t* i) { return make_ulonglong2(i[0], i[1]); }
 
-// ---------------------------------------------------------------- row-tile I/O
-// Rows [r0, r0 + C) of a row-major array (row stride rs, valid prefix len per
-// row, zeros beyond) <-> a tile.  For the interleaved layout the lane index
-// runs over rows (one 16-byte vector per lane; the sector's other half is the
-// same lane's next vector, an L1 hit), so shared accesses are conflict-free;
-// for the padded row layout consecutive lanes take consecutive vectors of a
-// row.  Loads of a thread are issued in batches of up to 8 vectors before any
-// shared store (memory-level parallelism).
-template <class Lay, int LOGL, int NTH> struct RowIO {
-    static constexpr int L = 1 << LOGL;
-    static constexpr int C = Lay::C;
-    template <int V> __device__ __forceinline__ static void map(int e, int& c, int& j) {
-        if (Lay::COL) { c = e % C; j = (e / C) * V; }
-        else { c = (e * V) >> LOGL; j = (e * V) & (L - 1); }
+// V consecutive twiddles (8 bytes each) with 16-byte loads
+template <class W, int V> __device__ __forceinline__ void ld_wvec(const W* p, W* w) {
+    static_assert(sizeof(W) == 8, "twiddles are 8 bytes");
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+        uint4 u = __ldg((const uint4*)(p + i));
+        w[i] = *reinterpret_cast<const W*>(&u.x);
+        w[i + 1] = *reinterpret_cast<const W*>(&u.z);
+    }
+}
+
+template <class F, int EPIV> struct Epi {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    static constexpr int FS = EPIV & 3;
+    static constexpr bool SC = (EPIV & EPI_SCALE) != 0, CN = (EPIV & EPI_CANON) != 0;
+    __device__ __forceinline__ static T apply(const F& f, T x, W wf, const W* lo, const W* hi, int h, uint32_t e,
+                                              const W& sc) {
+        if (FS == 1) x = f.mulw(x, wf);
+        if (FS == 2) {
+            x = f.mulw(x, __ldg(lo + (e & ((1u << h) - 1))));
+            x = f.mulw(x, __ldg(hi + (e >> h)));
+        }
+        if (SC) x = f.mulw(x, sc);
+        if (CN) x = f.canon(x);
+        return x;
     }
 };
 
+// twiddles in shared memory when the CTA stays under ~100 KiB
+template <class F, int LOGL, int ELEMS, int NTAB> struct TwPlace {
+    enum { SMEM = (size_t)ELEMS * sizeof(typename F::T) + (size_t)NTAB * (1u << LOGL) * sizeof(typename F::W) <= 100 * 1024 };
+};
+
+// ---------------------------------------------------------------- row-tile I/O
+// Rows [r0, r0 + C) of a row-major array (row stride rs, valid prefix len per
+// row, zeros beyond) -> padded row tile; consecutive lanes take consecutive
+// 16-byte vectors of a row (fully coalesced).  A thread issues up to 4
+// vector loads before its shared stores.
 template <class F, class Lay, int LOGL, class TIn>
 __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long long r0, long long nrows, long long rs,
                                           long long len, bool vec, bool perm) {
     typedef typename F::T T;
     typedef typename Vec<T>::type TV;
     constexpr int L = 1 << LOGL, C = Lay::C, V = Vec<T>::N;
-    typedef RowIO<Lay, LOGL, NT> IO;
+    const long long rlim = nrows - r0;                        // rows of this tile that exist
     if (L >= V && sizeof(TIn) == sizeof(T) && vec && !perm) {
-        constexpr int TOT = C * L / V;                       // vectors in the tile
-        constexpr int NV = (TOT + NT - 1) / NT;              // per thread
+        constexpr int TOT = C * L / V;
+        constexpr int NV = (TOT + NT - 1) / NT;
         constexpr int B = NV < 4 ? NV : 4;
+        const T* tb = (const T*)in + r0 * rs;
 #pragma unroll
         for (int u0 = 0; u0 < NV; u0 += B) {
             TV buf[B];
+            int mode[B];                                      // 0 zero, 1 full, 2 partial
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
-                int c, j;
-                IO::template map<V>(e, c, j);
-                const bool ok = e < TOT && r0 + c < nrows;
-                const TV* src = (const TV*)(ok ? (const T*)in + (r0 + c) * rs + j : (const T*)in);
-                buf[u] = __ldg(src);
-                if (!ok) buf[u] = TV{};
+                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                const bool rowok = e < TOT && c < rlim;
+                mode[u] = !rowok || j >= len ? 0 : (j + V <= len ? 1 : 2);
+                buf[u] = __ldg((const TV*)(mode[u] == 1 ? tb + (unsigned)c * (unsigned)rs + j : (const T*)in));
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
                 if (e >= TOT) continue;
-                int c, j;
-                IO::template map<V>(e, c, j);
+                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
                 T v[V];
                 vget<T>(buf[u], v);
+                if (mode[u] != 1) {
+#pragma unroll
+                    for (int i = 0; i < V; i++)
+                        v[i] = (mode[u] == 2 && j + i < len) ? __ldg(tb + (unsigned)c * (unsigned)rs + j + i) : (T)0;
+                }
 #pragma unroll
                 for (int i = 0; i < V; i++) s[Lay::addr(c, j + i)] = v[i];
             }
         }
     } else {
         for (int e = threadIdx.x; e < C * L; e += NT) {
-            int c, j;
-            IO::template map<1>(e, c, j);
-            const long long r = r0 + c;
+            const int c = e >> LOGL, j = e & (L - 1);
             T v = 0;
-            if (r < nrows && j < len) v = ld_conv<TIn, T>(in + r * rs + j);
+            if (c < rlim && j < len) v = ld_conv<TIn, T>(in + (r0 + c) * rs + j);
             s[Lay::addr(c, perm ? brev(j, LOGL) : j)] = v;
         }
     }
 }
 
-// epilogue of a row tile: optional step-2 twiddle w^(+-j [i2]) (full table
-// rows are contiguous: one 8- or 16-byte vector per element group), n^-1
-// scaling and canonicalisation, then vector stores.
-template <class F, class Lay, int LOGL, class TOut>
+// epilogue + stores of a row tile (step-2 twiddle rows are contiguous in the
+// full table: one or two 16-byte loads per vector)
+template <class F, class Lay, int LOGL, class TOut, int EPIV>
 __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, TOut* out, long long r0, long long nrows,
-                                           long long rs, long long len, bool vec, bool perm, int fs,
-                                           const typename F::W* fs_full, const typename F::W* fs_lo,
-                                           const typename F::W* fs_hi, int fs_h, long long row0, int k2, int scale,
-                                           typename F::W sc, int canon) {
+                                           long long rs, long long len, bool vec, bool perm, const typename F::W* fs_full,
+                                           const typename F::W* fs_lo, const typename F::W* fs_hi, int fs_h,
+                                           long long row0, int k2, const typename F::W& sc) {
     typedef typename F::T T;
     typedef typename F::W W;
     typedef typename Vec<T>::type TV;
+    typedef Epi<F, EPIV> E;
     constexpr int L = 1 << LOGL, C = Lay::C, V = Vec<T>::N;
-    typedef RowIO<Lay, LOGL, NT> IO;
+    const long long rlim = nrows - r0;
+    const unsigned i2mask = (1u << k2) - 1;
+    const unsigned i2b = (unsigned)((row0 + r0) & i2mask);
     if (L >= V && sizeof(TOut) == sizeof(T) && vec && !perm) {
         constexpr int TOT = C * L / V;
         constexpr int NV = (TOT + NT - 1) / NT;
         constexpr int B = NV < 2 ? NV : 2;
+        T* ob = (T*)out + r0 * rs;
 #pragma unroll
         for (int u0 = 0; u0 < NV; u0 += B) {
             T v[B][V];
             W w[B][V];
 #pragma unroll
             for (int u = 0; u < B; u++) {
-                const int e = threadIdx.x + (u0 + u) * NT;
-                int c, j;
-                IO::template map<V>(e < TOT ? e : 0, c, j);      // idle lanes read a valid slot
+                const int e0 = threadIdx.x + (u0 + u) * NT;
+                const int e = e0 < TOT ? e0 : 0;                  // idle lanes read a valid slot
+                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
 #pragma unroll
                 for (int i = 0; i < V; i++) v[u][i] = s[Lay::addr(c, j + i)];
-                if (fs && fs_full) {
-                    const long long i2 = (row0 + r0 + (e < TOT ? c : 0)) & ((1ll << k2) - 1);
-#pragma unroll
-                    for (int i = 0; i < V; i++) w[u][i] = __ldg(fs_full + i2 * L + j + i);
-                }
+                if (E::FS == 1) ld_wvec<W, V>(fs_full + ((i2b + c) & i2mask) * L + j, w[u]);
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
-                int c, j;
-                IO::template map<V>(e, c, j);
-                const long long r = r0 + c;
-                if (e >= TOT || r >= nrows) continue;
+                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                if (e >= TOT || c >= rlim || j >= len) continue;
+                const unsigned i2r = brev((int)((i2b + c) & i2mask), k2);
 #pragma unroll
-                for (int i = 0; i < V; i++) {
-                    T x = v[u][i];
-                    if (fs) {
-                        if (fs_full) x = f.mulw(x, w[u][i]);
-                        else x = fs_apply(f, x, nullptr, fs_lo, fs_hi, fs_h, (row0 + r) & ((1ll << k2) - 1), k2, j + i, L);
-                    }
-                    if (scale) x = f.mulw(x, sc);
-                    if (canon) x = f.canon(x);
-                    v[u][i] = x;
+                for (int i = 0; i < V; i++) v[u][i] = E::apply(f, v[u][i], w[u][i], fs_lo, fs_hi, fs_h, (unsigned)(j + i) * i2r, sc);
+                if (j + V <= len) {
+                    *(TV*)(ob + (unsigned)c * (unsigned)rs + j) = vmake<T>(v[u]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < V; i++)
+                        if (j + i < len) ob[(unsigned)c * (unsigned)rs + j + i] = v[u][i];
                 }
-                *(TV*)((T*)out + r * rs + j) = vmake<T>(v[u]);
             }
         }
     } else {
         for (int e = threadIdx.x; e < C * L; e += NT) {
-            int c, j;
-            IO::template map<1>(e, c, j);
-            const long long r = r0 + c;
-            if (r >= nrows || j >= len) continue;
-            T x = s[Lay::addr(c, perm ? brev(j, LOGL) : j)];
-            if (fs) x = fs_apply(f, x, fs_full, fs_lo, fs_hi, fs_h, (row0 + r) & ((1ll << k2) - 1), k2, j, L);
-            if (scale) x = f.mulw(x, sc);
-            if (canon) x = f.canon(x);
-            out[r * rs + j] = (TOut)x;
+            const int c = e >> LOGL, j = e & (L - 1);
+            if (c >= rlim || j >= len) continue;
+            const unsigned i2 = (i2b + c) & i2mask;
+            W wf{};
+            if (E::FS == 1) wf = __ldg(fs_full + i2 * L + j);
+            T x = E::apply(f, s[Lay::addr(c, perm ? brev(j, LOGL) : j)], wf, fs_lo, fs_hi, fs_h,
+                           (unsigned)j * (unsigned)brev((int)i2, k2), sc);
+            out[(r0 + c) * rs + j] = (TOut)x;
         }
     }
 }
 
 // ---------------------------------------------------------------- row pass
-template <class F, int LOGL, bool INV, class TIn, class TOut>
+template <class F, int LOGL> struct RowsK {
+    typedef typename RowsTile<F, LOGL>::Lay Lay;
+    enum { TWS = TwPlace<F, LOGL, Lay::ELEMS, 1>::SMEM };
+    static constexpr size_t smem() {
+        return (size_t)Lay::ELEMS * sizeof(typename F::T) + (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
+    }
+};
+
+template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
 __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
     typedef typename F::T T;
     typedef typename F::W W;
-    typedef typename RowsTile<F, LOGL>::Lay Lay;
+    typedef RowsK<F, LOGL> K;
+    typedef typename K::Lay Lay;
     constexpr int L = 1 << LOGL;
     constexpr int C = Lay::C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* tws = (W*)smem_raw;
-    T* s = (T*)(tws + (a.tw_smem ? L : 0));
-    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
-    const W* tw = a.tw_smem ? tws : a.lvl;
+    T* s = (T*)(tws + (K::TWS ? L : 0));
+    if (K::TWS) stage_twiddles(tws, a.lvl, L);
+    const W* tw = K::TWS ? (const W*)tws : a.lvl;
     const long long ntiles = (a.nrows + C - 1) / C;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
@@ -294,20 +315,41 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
         __syncthreads();
         if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
         else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
-        store_rows<F, Lay, LOGL, TOut>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
-                                       !INV && a.perm, INV ? a.fs : 0, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0,
-                                       a.k2, a.scale, a.sc, a.canon);
+        store_rows<F, Lay, LOGL, TOut, EPIV>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
+                                             !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc);
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------- column pass
-template <class F, int LOGL, bool INV, class TIn, class TOut>
+template <class F, int LOGL> struct ColsK {
+    typedef typename ColsTile<F, LOGL>::Lay Lay;
+    enum { TWS = TwPlace<F, LOGL, Lay::ELEMS, 1>::SMEM };
+    static constexpr size_t smem() {
+        return (size_t)Lay::ELEMS * sizeof(typename F::T) + (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
+    }
+};
+
+// rows t of a column tile with linear index t n1 + lin0 + [0, C): fully valid for
+// t < *full, fully beyond the valid prefix for t >= *zero
+__device__ __forceinline__ void col_rows_valid(long long len, long long lin0, long long n1, int C, int L, int* full,
+                                               int* zero) {
+    long long f = len - lin0 - C;
+    long long fr = f < 0 ? 0 : f / n1 + 1;
+    long long z = len - lin0;
+    long long zr = z <= 0 ? 0 : (z + n1 - 1) / n1;
+    *full = (int)(fr < L ? fr : L);
+    *zero = (int)(zr < L ? zr : L);
+}
+
+template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
 __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
     typedef typename F::T T;
     typedef typename F::W W;
     typedef typename Vec<T>::type TV;
-    typedef typename ColsTile<F, LOGL>::Lay Lay;
+    typedef ColsK<F, LOGL> K;
+    typedef typename K::Lay Lay;
+    typedef Epi<F, EPIV> E;
     constexpr int L = 1 << LOGL;
     constexpr int C = Lay::C;
     constexpr int V = Vec<T>::N;
@@ -316,34 +358,30 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
     constexpr int NV = (TOT + NT - 1) / NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* tws = (W*)smem_raw;
-    T* s = (T*)(tws + (a.tw_smem ? L : 0));
-    if (a.tw_smem) stage_twiddles(tws, a.lvl, L);
-    const W* tw = a.tw_smem ? tws : a.lvl;
-    const TIn* in = (const TIn*)a.in;
-    TOut* out = (TOut*)a.out;
-    const long long cgroups = (a.ncols + C - 1) / C;
+    T* s = (T*)(tws + (K::TWS ? L : 0));
+    if (K::TWS) stage_twiddles(tws, a.lvl, L);
+    const W* tw = K::TWS ? (const W*)tws : a.lvl;
+    const long long cgroups = a.ncols / C;                 // host guarantees ncols % C == 0
     const long long ntiles = cgroups * a.nbatch;
+    const unsigned irs = (unsigned)a.in_rs, ors = (unsigned)a.out_rs, n1 = (unsigned)a.n1;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long b = tile / cgroups;
         const long long cl0 = (tile - b * cgroups) * C;
-        const TIn* inb = in + b * a.in_bs + cl0;
         const long long lin0 = a.col0 + cl0;        // logical column of c = 0
-        if (a.vec_in) {
+        const TIn* inb = (const TIn*)a.in + b * a.in_bs + cl0;
+        int tfull, tzero;
+        col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
+        if (a.vec_in && sizeof(TIn) == sizeof(T)) {
             constexpr int B = NV < 4 ? NV : 4;
+            const T* tb = (const T*)inb;
 #pragma unroll
             for (int u0 = 0; u0 < NV; u0 += B) {
                 TV buf[B];
-                int nval[B];
 #pragma unroll
                 for (int u = 0; u < B; u++) {
                     const int e = threadIdx.x + (u0 + u) * NT;
                     const int t = e / CV, c = (e % CV) * V;
-                    const long long lin = (long long)t * a.n1 + lin0 + c;
-                    long long lim = a.in_len - lin;
-                    if (a.ncols - cl0 - c < lim) lim = a.ncols - cl0 - c;
-                    nval[u] = e >= TOT ? 0 : (lim >= V ? V : (lim > 0 ? (int)lim : 0));
-                    const TV* src = (const TV*)(nval[u] == V ? (const T*)inb + (long long)t * a.in_rs + c : (const T*)in);
-                    buf[u] = __ldg(src);
+                    buf[u] = __ldg((const TV*)(e < TOT && t < tfull ? tb + (unsigned)t * irs + c : (const T*)a.in));
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
@@ -352,10 +390,11 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                     const int t = e / CV, c = (e % CV) * V;
                     T v[V];
                     vget<T>(buf[u], v);
-                    if (nval[u] < V) {
+                    if (t >= tfull) {
 #pragma unroll
                         for (int i = 0; i < V; i++)
-                            v[i] = i < nval[u] ? ld_conv<TIn, T>(inb + (long long)t * a.in_rs + c + i) : (T)0;
+                            v[i] = (t < tzero && (long long)t * a.n1 + lin0 + c + i < a.in_len)
+                                       ? __ldg(tb + (unsigned)t * irs + c + i) : (T)0;
                     }
                     if (Lay::COL) {
                         *(TV*)(s + Lay::addr(c, t)) = vmake<T>(v);
@@ -369,74 +408,64 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
             for (int e = threadIdx.x; e < L * C; e += NT) {
                 const int t = e / C, c = e % C;
                 T v = 0;
-                if (cl0 + c < a.ncols && (long long)t * a.n1 + lin0 + c < a.in_len)
-                    v = ld_conv<TIn, T>(inb + (long long)t * a.in_rs + c);
+                if (t < tfull || (t < tzero && (long long)t * a.n1 + lin0 + c < a.in_len))
+                    v = ld_conv<TIn, T>(inb + (unsigned)t * irs + c);
                 s[Lay::addr(c, t)] = v;
             }
         }
         __syncthreads();
         if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
         else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
-        TOut* outb = out + b * a.out_bs + cl0;
-        const int fs = INV ? 0 : a.fs;
-        if (a.vec_out) {
+        col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
+        TOut* outb = (TOut*)a.out + b * a.out_bs + cl0;
+        if (a.vec_out && sizeof(TOut) == sizeof(T)) {
             constexpr int B = NV < 2 ? NV : 2;
+            T* ob = (T*)outb;
 #pragma unroll
             for (int u0 = 0; u0 < NV; u0 += B) {
                 T v[B][V];
                 W w[B][V];
 #pragma unroll
                 for (int u = 0; u < B; u++) {
-                    const int e = threadIdx.x + (u0 + u) * NT;
-                    const int t = (e < TOT ? e : 0) / CV, c = (e % CV) * V;
+                    const int e0 = threadIdx.x + (u0 + u) * NT;
+                    const int e = e0 < TOT ? e0 : 0;
+                    const int t = e / CV, c = (e % CV) * V;
                     if (Lay::COL) vget<T>(*(const TV*)(s + Lay::addr(c, t)), v[u]);
                     else {
 #pragma unroll
                         for (int i = 0; i < V; i++) v[u][i] = s[Lay::addr(c + i, t)];
                     }
-                    if (fs && a.fs_full) {
-                        long long j1 = lin0 + c;
-                        if (j1 + V > a.n1) j1 = a.n1 - V;               // ragged column tail: any valid entry
-#pragma unroll
-                        for (int i = 0; i < V; i++) w[u][i] = __ldg(a.fs_full + (long long)t * a.n1 + j1 + i);
-                    }
+                    if (E::FS == 1) ld_wvec<W, V>(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
                     const int e = threadIdx.x + (u0 + u) * NT;
                     if (e >= TOT) continue;
                     const int t = e / CV, c = (e % CV) * V;
-                    const long long lin = (long long)t * a.n1 + lin0 + c;
+                    if (t >= tzero) continue;
+                    const unsigned bt = (unsigned)brev(t, LOGL);
 #pragma unroll
-                    for (int i = 0; i < V; i++) {
-                        T x = v[u][i];
-                        if (fs) {
-                            if (a.fs_full) x = f.mulw(x, w[u][i]);
-                            else x = fs_apply(f, x, nullptr, a.fs_lo, a.fs_hi, a.fs_h, t, LOGL, lin0 + c + i, a.n1);
-                        }
-                        if (a.scale) x = f.mulw(x, a.sc);
-                        if (a.canon) x = f.canon(x);
-                        v[u][i] = x;
-                    }
-                    if (cl0 + c + V <= a.ncols && lin + V <= a.out_len) {
-                        *(TV*)((T*)outb + (long long)t * a.out_rs + c) = vmake<T>(v[u]);
+                    for (int i = 0; i < V; i++)
+                        v[u][i] = E::apply(f, v[u][i], w[u][i], a.fs_lo, a.fs_hi, a.fs_h,
+                                           ((unsigned)lin0 + c + i) * bt, a.sc);
+                    if (t < tfull) {
+                        *(TV*)(ob + (unsigned)t * ors + c) = vmake<T>(v[u]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < V; i++)
-                            if (cl0 + c + i < a.ncols && lin + i < a.out_len)
-                                outb[(long long)t * a.out_rs + c + i] = (TOut)v[u][i];
+                            if ((long long)t * a.n1 + lin0 + c + i < a.out_len) ob[(unsigned)t * ors + c + i] = v[u][i];
                     }
                 }
             }
         } else {
             for (int e = threadIdx.x; e < L * C; e += NT) {
                 const int t = e / C, c = e % C;
-                if (cl0 + c >= a.ncols || (long long)t * a.n1 + lin0 + c >= a.out_len) continue;
-                T x = s[Lay::addr(c, t)];
-                if (fs) x = fs_apply(f, x, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, t, LOGL, lin0 + c, a.n1);
-                if (a.scale) x = f.mulw(x, a.sc);
-                if (a.canon) x = f.canon(x);
-                outb[(long long)t * a.out_rs + c] = (TOut)x;
+                if (t >= tzero || (t >= tfull && (long long)t * a.n1 + lin0 + c >= a.out_len)) continue;
+                W wf{};
+                if (E::FS == 1) wf = __ldg(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c);
+                T x = E::apply(f, s[Lay::addr(c, t)], wf, a.fs_lo, a.fs_hi, a.fs_h,
+                               ((unsigned)lin0 + c) * (unsigned)brev(t, LOGL), a.sc);
+                outb[(unsigned)t * ors + c] = (TOut)x;
             }
         }
         __syncthreads();
@@ -444,24 +473,34 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
 }
 
 // ---------------------------------------------------------------- fused product rows
-template <class F, int LOGL, class TIn, class TOut>
+template <class F, int LOGL> struct PmulK {
+    typedef typename PmulTile<F, LOGL>::Lay Lay;
+    enum { TWS = TwPlace<F, LOGL, 2 * Lay::ELEMS, 2>::SMEM };
+    static constexpr size_t smem() {
+        return 2 * (size_t)Lay::ELEMS * sizeof(typename F::T) +
+               (TWS ? 2 * (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
+    }
+};
+
+template <class F, int LOGL, class TIn, class TOut, int EPIV>
 __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
     typedef typename F::T T;
     typedef typename F::W W;
-    typedef typename PmulTile<F, LOGL>::Lay Lay;
+    typedef PmulK<F, LOGL> K;
+    typedef typename K::Lay Lay;
     constexpr int L = 1 << LOGL;
     constexpr int C = Lay::C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* twfs = (W*)smem_raw;
-    W* twis = twfs + (a.tw_smem ? L : 0);
-    T* sa = (T*)(twis + (a.tw_smem ? L : 0));
+    W* twis = twfs + (K::TWS ? L : 0);
+    T* sa = (T*)(twis + (K::TWS ? L : 0));
     T* sb = sa + Lay::ELEMS;
-    if (a.tw_smem) {
+    if (K::TWS) {
         stage_twiddles(twfs, a.lvl_f, L);
         stage_twiddles(twis, a.lvl_i, L);
     }
-    const W* twf = a.tw_smem ? twfs : a.lvl_f;
-    const W* twi = a.tw_smem ? twis : a.lvl_i;
+    const W* twf = K::TWS ? (const W*)twfs : a.lvl_f;
+    const W* twi = K::TWS ? (const W*)twis : a.lvl_i;
     const long long ntiles = (a.nrows + C - 1) / C;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
@@ -471,13 +510,13 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
         tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twf);
         tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sb, twf);
         for (int e = threadIdx.x; e < C * L; e += NT) {
-            const int ix = Lay::COL ? e : Lay::addr(e >> LOGL, e & (L - 1));   // the interleaved tile is dense
+            const int ix = Lay::addr(e >> LOGL, e & (L - 1));
             sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
         }
         __syncthreads();
         tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twi);
-        store_rows<F, Lay, LOGL, TOut>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs, a.fs_full,
-                                       a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, 0, a.sc, a.canon);
+        store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
+                                             a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc);
         __syncthreads();
     }
 }
@@ -494,54 +533,46 @@ template <class K> static int grid_for(K kern, size_t smem, long long tiles) {
     long long cap = (long long)num_sms() * per_sm;
     return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
 }
-// twiddles go to shared memory unless they would push the CTA past ~100 KiB
-static inline bool tw_in_smem(size_t data, size_t tw) {
-    return data + tw <= 100 * 1024 || (data > 100 * 1024 && data + tw <= SMEM_MAX && tw <= 8 * 1024);
-}
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-template <class F, int LOGL, bool INV, class TIn, class TOut>
-static mm_status launch_rows_k(const F& f, RowArgs<F> a, cudaStream_t st) {
+template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
+static mm_status launch_rows_e(const F& f, RowArgs<F> a, cudaStream_t st) {
     typedef typename F::T T;
-    typedef typename F::W W;
-    typedef typename RowsTile<F, LOGL>::Lay Lay;
+    typedef RowsK<F, LOGL> K;
     constexpr int L = 1 << LOGL;
     constexpr int V = Vec<T>::N;
-    size_t data = (size_t)Lay::ELEMS * sizeof(T), twb = (size_t)L * sizeof(W);
-    a.tw_smem = tw_in_smem(data, twb);
-    size_t smem = data + (a.tw_smem ? twb : 0);
-    a.vec_in = sizeof(TIn) == sizeof(T) && !(INV && a.perm) && a.in_len >= L && a.in_rs % V == 0 && aligned16(a.in);
-    a.vec_out = sizeof(TOut) == sizeof(T) && !(!INV && a.perm) && a.out_len >= L && a.out_rs % V == 0 &&
-                aligned16(a.out) && !(INV && a.fs && !a.fs_full && false);
-    auto kern = k_rows<F, LOGL, INV, TIn, TOut>;
+    const size_t smem = K::smem();
+    a.vec_in = sizeof(TIn) == sizeof(T) && !(INV && a.perm) && a.in_rs % V == 0 && aligned16(a.in);
+    a.vec_out = sizeof(TOut) == sizeof(T) && !(!INV && a.perm) && a.out_rs % V == 0 && aligned16(a.out);
+    auto kern = k_rows<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
-    long long tiles = (a.nrows + Lay::C - 1) / Lay::C;
+    long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
     {
         LaunchScope ls(INV ? "ntt_rows_inv" : "ntt_rows_fwd", st);
         kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
+    (void)L;
     return MM_OK;
 }
 
-template <class F, int LOGL, bool INV, class TIn, class TOut>
-static mm_status launch_cols_k(const F& f, ColArgs<F> a, cudaStream_t st) {
+template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
+static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     typedef typename F::T T;
-    typedef typename F::W W;
-    typedef typename ColsTile<F, LOGL>::Lay Lay;
-    constexpr int L = 1 << LOGL;
+    typedef ColsK<F, LOGL> K;
     constexpr int V = Vec<T>::N;
-    size_t data = (size_t)Lay::ELEMS * sizeof(T), twb = (size_t)L * sizeof(W);
-    a.tw_smem = tw_in_smem(data, twb);
-    size_t smem = data + (a.tw_smem ? twb : 0);
+    const size_t smem = K::smem();
+    if (a.ncols % K::Lay::C != 0)
+        return set_err(MM_E_UNSUPPORTED_SIZE, "column block of %lld columns is not a multiple of the tile width %d",
+                       a.ncols, (int)K::Lay::C);
     a.vec_in = sizeof(TIn) == sizeof(T) && a.in_rs % V == 0 && (a.in_bs % V == 0 || a.nbatch == 1) && aligned16(a.in);
     a.vec_out = sizeof(TOut) == sizeof(T) && a.out_rs % V == 0 && (a.out_bs % V == 0 || a.nbatch == 1) &&
                 aligned16(a.out);
-    auto kern = k_cols<F, LOGL, INV, TIn, TOut>;
+    auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
-    long long tiles = (a.ncols + Lay::C - 1) / Lay::C * a.nbatch;
+    long long tiles = a.ncols / K::Lay::C * a.nbatch;
     {
         LaunchScope ls(INV ? "ntt_cols_inv" : "ntt_cols_fwd", st);
         kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
@@ -550,29 +581,62 @@ static mm_status launch_cols_k(const F& f, ColArgs<F> a, cudaStream_t st) {
     return MM_OK;
 }
 
-template <class F, int LOGL, class TIn, class TOut>
-static mm_status launch_pmul_k(const F& f, PmulArgs<F> a, cudaStream_t st) {
+template <class F, int LOGL, class TIn, class TOut, int EPIV>
+static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
     typedef typename F::T T;
-    typedef typename F::W W;
-    typedef typename PmulTile<F, LOGL>::Lay Lay;
-    constexpr int L = 1 << LOGL;
+    typedef PmulK<F, LOGL> K;
     constexpr int V = Vec<T>::N;
-    size_t data = 2 * (size_t)Lay::ELEMS * sizeof(T), twb = 2 * (size_t)L * sizeof(W);
-    a.tw_smem = tw_in_smem(data, twb);
-    size_t smem = data + (a.tw_smem ? twb : 0);
-    a.vec_in = sizeof(TIn) == sizeof(T) && a.la >= L && a.lb >= L && a.a_rs % V == 0 && a.b_rs % V == 0 &&
-               aligned16(a.a) && aligned16(a.b);
-    a.vec_out = sizeof(TOut) == sizeof(T) && a.lc >= L && a.c_rs % V == 0 && aligned16(a.c);
-    auto kern = k_rows_pmul<F, LOGL, TIn, TOut>;
+    const size_t smem = K::smem();
+    a.vec_in = sizeof(TIn) == sizeof(T) && a.a_rs % V == 0 && a.b_rs % V == 0 && aligned16(a.a) && aligned16(a.b);
+    a.vec_out = sizeof(TOut) == sizeof(T) && a.c_rs % V == 0 && aligned16(a.c);
+    auto kern = k_rows_pmul<F, LOGL, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
-    long long tiles = (a.nrows + Lay::C - 1) / Lay::C;
+    long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
     {
         LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
         kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
+}
+
+static inline int epi_code(int fs, bool full, int scale, int canon) {
+    return (fs ? (full ? EPI_FS_FULL : EPI_FS_SPLIT) : 0) | (scale ? EPI_SCALE : 0) | (canon ? EPI_CANON : 0);
+}
+
+// epilogue variants actually used by the drivers (others return an error)
+template <class F, int LOGL, bool INV, class TIn, class TOut>
+static mm_status launch_rows_k(const F& f, const RowArgs<F>& a, cudaStream_t st) {
+    const int e = epi_code(INV ? a.fs : 0, a.fs_full != nullptr, a.scale, a.canon);
+    if (!INV) {
+        if (e == EPI_CANON) return launch_rows_e<F, LOGL, INV, TIn, TOut, EPI_CANON>(f, a, st);
+    } else {
+        if (e == (EPI_SCALE | EPI_CANON)) return launch_rows_e<F, LOGL, INV, TIn, TOut, EPI_SCALE | EPI_CANON>(f, a, st);
+        if (e == EPI_FS_FULL) return launch_rows_e<F, LOGL, INV, TIn, TOut, EPI_FS_FULL>(f, a, st);
+        if (e == EPI_FS_SPLIT) return launch_rows_e<F, LOGL, INV, TIn, TOut, EPI_FS_SPLIT>(f, a, st);
+    }
+    return set_err(MM_E_ARG, "unsupported row-pass epilogue %d", e);
+}
+template <class F, int LOGL, bool INV, class TIn, class TOut>
+static mm_status launch_cols_k(const F& f, const ColArgs<F>& a, cudaStream_t st) {
+    const int e = epi_code(INV ? 0 : a.fs, a.fs_full != nullptr, a.scale, a.canon);
+    if (!INV) {
+        if (e == EPI_FS_FULL) return launch_cols_e<F, LOGL, INV, TIn, TOut, EPI_FS_FULL>(f, a, st);
+        if (e == EPI_FS_SPLIT) return launch_cols_e<F, LOGL, INV, TIn, TOut, EPI_FS_SPLIT>(f, a, st);
+    } else {
+        if (e == EPI_CANON) return launch_cols_e<F, LOGL, INV, TIn, TOut, EPI_CANON>(f, a, st);
+        if (e == (EPI_SCALE | EPI_CANON)) return launch_cols_e<F, LOGL, INV, TIn, TOut, EPI_SCALE | EPI_CANON>(f, a, st);
+    }
+    return set_err(MM_E_ARG, "unsupported column-pass epilogue %d", e);
+}
+template <class F, int LOGL, class TIn, class TOut>
+static mm_status launch_pmul_k(const F& f, const PmulArgs<F>& a, cudaStream_t st) {
+    const int e = epi_code(a.fs, a.fs_full != nullptr, 0, a.canon);
+    if (e == EPI_CANON) return launch_pmul_e<F, LOGL, TIn, TOut, EPI_CANON>(f, a, st);
+    if (e == EPI_FS_FULL) return launch_pmul_e<F, LOGL, TIn, TOut, EPI_FS_FULL>(f, a, st);
+    if (e == EPI_FS_SPLIT) return launch_pmul_e<F, LOGL, TIn, TOut, EPI_FS_SPLIT>(f, a, st);
+    return set_err(MM_E_ARG, "unsupported product epilogue %d", e);
 }
 
 // runtime log2 length -> compile-time kernel (cases outside [LO, HI] are not instantiated)
@@ -600,7 +664,7 @@ mm_status launch_rows(const F& f, const RowArgs<F>& a, cudaStream_t st) {
 template <class F, bool INV, class TIn, class TOut>
 mm_status launch_cols(const F& f, const ColArgs<F>& a, cudaStream_t st) {
 #define MM_CALLC(K) launch_cols_k<F, K, INV, TIn, TOut>(f, a, st)
-    MM_DISPATCH_K(a.k, 3, 13, MM_CALLC)
+    MM_DISPATCH_K(a.k, 5, 12, MM_CALLC)
 #undef MM_CALLC
 }
 template <class F, class TIn, class TOut>
