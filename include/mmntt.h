@@ -190,6 +190,20 @@ mm_status mm_probe_butterfly(int word_bits, int iters, double *ms, double *bfly,
 void mm_prof_enable(int on);
 int mm_prof_collect(char *buf, size_t len);
 
+/* Segmented-row variants for the distributed transform (no reshuffle copy):
+ * a segmented row block of nrows rows stores element j of row r at
+ *   (j / seg_len) * seg_stride + r * seg_len + (j mod seg_len),
+ * i.e. n1 / seg_len segments of [nrows][seg_len] each -- exactly the
+ * receive buffer of an equal-split all-to-all where segment g came from the
+ * rank owning columns [g seg_len, (g+1) seg_len).  seg_len must be a power of
+ * two dividing n1 and seg_stride >= nrows * seg_len.
+ * mm_ntt_fwd_rows_seg: segmented input -> plain rows output.
+ * mm_ntt_inv_rows_seg: plain rows input -> segmented output. */
+mm_status mm_ntt_fwd_rows_seg(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
+                              size_t in_seg_len, size_t in_seg_stride, void *stream);
+mm_status mm_ntt_inv_rows_seg(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
+                              size_t out_seg_len, size_t out_seg_stride, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,8 @@ EXPORTS = {
     "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ntt_fwd_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
+    "mm_ntt_inv_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_launch_count": (ctypes.c_ulonglong, []),
     "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_prof_enable": (None, [_i32]),
@@ -219,6 +221,16 @@ class NttPlan:
 
     def inv_rows(self, x, out, row0, nrows):
         _check(lib().mm_ntt_inv_rows(self._h, _ptr(x), _ptr(out), row0, nrows, _stream(x)))
+        return out
+
+    def fwd_rows_seg(self, x, out, row0, nrows, seg_len, seg_stride):
+        """Row pass reading segmented rows (an all-to-all receive buffer)."""
+        _check(lib().mm_ntt_fwd_rows_seg(self._h, _ptr(x), _ptr(out), row0, nrows, seg_len, seg_stride, _stream(x)))
+        return out
+
+    def inv_rows_seg(self, x, out, row0, nrows, seg_len, seg_stride):
+        """Inverse row pass writing segmented rows (an all-to-all send buffer)."""
+        _check(lib().mm_ntt_inv_rows_seg(self._h, _ptr(x), _ptr(out), row0, nrows, seg_len, seg_stride, _stream(x)))
         return out
 
     def inv_cols(self, x, out, col0, ncols):

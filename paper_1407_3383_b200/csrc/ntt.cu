@@ -592,7 +592,7 @@ static mm_status fwd_cols_impl(mm_ntt_plan* P, const void* in, void* out, size_t
 }
 template <class F>
 static mm_status rows_impl(mm_ntt_plan* P, const void* in, void* out, size_t row0, size_t nrows, bool inv,
-                           cudaStream_t st) {
+                           cudaStream_t st, int seg_log = 0, long long seg_stride = 0) {
     typedef typename F::T T;
     typedef typename F::W W;
     F f = make_field<F>(P);
@@ -600,6 +600,11 @@ static mm_status rows_impl(mm_ntt_plan* P, const void* in, void* out, size_t row
     a.in = in; a.out = out;
     a.nrows = (long long)nrows;
     a.in_rs = a.out_rs = 1ll << P->k1;
+    // segmented side: forward reads segmented rows, inverse writes them (row stride = segment length)
+    if (seg_log) {
+        if (!inv) { a.in_seg_log = seg_log; a.in_seg_stride = seg_stride; a.in_rs = 1ll << seg_log; }
+        else { a.out_seg_log = seg_log; a.out_seg_stride = seg_stride; a.out_rs = 1ll << seg_log; }
+    }
     a.in_len = a.out_len = 1ll << P->k1;
     a.k = P->k1;
     a.row0 = (long long)row0;
@@ -838,6 +843,39 @@ extern "C" mm_status mm_ntt_inv_cols(const mm_ntt_plan* plan, const void* in, vo
     cudaStream_t st = (cudaStream_t)stream;
     return P->word_bits == 32 ? inv_cols_impl<Fp32>(P, in, out, col0, ncols, st)
                               : inv_cols_impl<FpG>(P, in, out, col0, ncols, st);
+}
+
+static mm_status seg_check(const mm_ntt_plan* P, size_t seg_len, size_t seg_stride, size_t nrows, int* seg_log) {
+    int l = 0;
+    while ((1ull << l) < seg_len) l++;
+    if (seg_len == 0 || (1ull << l) != seg_len || seg_len > (1ull << P->k1) || ((1ull << P->k1) % seg_len) != 0)
+        return set_err(MM_E_ARG, "segment length %zu must be a power of two dividing n1", seg_len);
+    if (seg_stride < nrows * seg_len) return set_err(MM_E_ARG, "segment stride %zu < rows x segment length", seg_stride);
+    *seg_log = l;
+    return MM_OK;
+}
+
+extern "C" mm_status mm_ntt_fwd_rows_seg(const mm_ntt_plan* plan, const void* in, void* out, size_t row0, size_t nrows,
+                                         size_t in_seg_len, size_t in_seg_stride, void* stream) {
+    mm_status s = dist_check(plan, in, out, row0, nrows, false);
+    if (s != MM_OK) return s;
+    int sl = 0;
+    if ((s = seg_check(plan, in_seg_len, in_seg_stride, nrows, &sl)) != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? rows_impl<Fp32>(P, in, out, row0, nrows, false, st, sl, (long long)in_seg_stride)
+                              : rows_impl<FpG>(P, in, out, row0, nrows, false, st, sl, (long long)in_seg_stride);
+}
+extern "C" mm_status mm_ntt_inv_rows_seg(const mm_ntt_plan* plan, const void* in, void* out, size_t row0, size_t nrows,
+                                         size_t out_seg_len, size_t out_seg_stride, void* stream) {
+    mm_status s = dist_check(plan, in, out, row0, nrows, false);
+    if (s != MM_OK) return s;
+    int sl = 0;
+    if ((s = seg_check(plan, out_seg_len, out_seg_stride, nrows, &sl)) != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? rows_impl<Fp32>(P, in, out, row0, nrows, true, st, sl, (long long)out_seg_stride)
+                              : rows_impl<FpG>(P, in, out, row0, nrows, true, st, sl, (long long)out_seg_stride);
 }
 
 static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {

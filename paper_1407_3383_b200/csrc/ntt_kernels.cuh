@@ -70,6 +70,8 @@ template <class F> struct RowArgs {
     void* out;
     long long nrows, in_rs, out_rs, in_len, out_len, row0;
     int k, k2, perm, fs, scale, canon, vec_in, vec_out;
+    int in_seg_log, out_seg_log;           // segmented rows: element j of row r at
+    long long in_seg_stride, out_seg_stride; // (j >> log) * stride + r * rs + (j mod 2^log); log 0 = plain
     W sc;
     const W* lvl;
     const W* fs_lo;
@@ -97,6 +99,8 @@ template <class F> struct PmulArgs {
     void* c;
     long long nrows, a_rs, b_rs, c_rs, la, lb, lc, row0;
     int k, k2, fs, canon, vec_in, vec_out;
+    int in_seg_log, out_seg_log;           // segmented rows for a, b (in) and c (out), as RowArgs
+    long long in_seg_stride, out_seg_stride;
     W sc;                 // pointwise post-multiplier (n^-1, times 2^32 for the 32-bit REDC)
     const W* lvl_f;
     const W* lvl_i;
@@ -168,13 +172,51 @@ template <class F, int LOGL, int ELEMS, int NTAB> struct TwPlace {
 };
 
 // ---------------------------------------------------------------- row-tile I/O
+// Vector index e -> (row c, first element j) of a row tile.  For 32-bit rows of
+// >= 64 points and an even number of rows, a warp takes 16 vectors of row c
+// and 16 of row c+1: with the j + (j >> 4) padding and a row pitch of 16 banks
+// mod 32 every 4-byte shared access of the warp then hits a distinct bank
+// (the plain mapping gave 2-way conflicts).  Global accesses stay 256-byte
+// contiguous per half-warp.
+template <class T, class Lay, int LOGL> struct RowVecMap {
+    static constexpr int L = 1 << LOGL, V = Vec<T>::N, VR = L / V, C = Lay::C;
+    static constexpr bool PAIRED = sizeof(T) == 4 && VR >= 16 && (C % 2) == 0;
+    __device__ __forceinline__ static void map(int e, int& c, int& j) {
+        if constexpr (PAIRED) {
+            constexpr int NCH = VR / 16;
+            const int hl = e & 15, hw = (e >> 4) & 1, rest = e >> 5;
+            const int rp = rest / NCH, k = rest % NCH;
+            c = 2 * rp + hw;
+            j = (16 * k + hl) * V;
+        } else {
+            c = (e * V) >> LOGL;
+            j = (e * V) & (L - 1);
+        }
+    }
+};
+
+// offset of element j within a (possibly segmented) row
+__device__ __forceinline__ long long seg_j(int j, int seglog, long long segstride) {
+    return seglog ? (long long)(j >> seglog) * segstride + (j & ((1 << seglog) - 1)) : (long long)j;
+}
+
+// cp.async (LDGSTS) helpers: 16-byte copies global -> shared, zero-filling the
+// bytes beyond src_bytes (0 -> the destination is zeroed, nothing is read)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 // Rows [r0, r0 + C) of a row-major array (row stride rs, valid prefix len per
 // row, zeros beyond) -> padded row tile; consecutive lanes take consecutive
 // 16-byte vectors of a row (fully coalesced).  A thread issues up to 4
 // vector loads before its shared stores.
 template <class F, class Lay, int LOGL, class TIn>
 __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long long r0, long long nrows, long long rs,
-                                          long long len, bool vec, bool perm) {
+                                          long long len, bool vec, bool perm, int seglog = 0, long long segstride = 0) {
     typedef typename F::T T;
     typedef typename Vec<T>::type TV;
     constexpr int L = 1 << LOGL, C = Lay::C, V = Vec<T>::N;
@@ -191,22 +233,26 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
-                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                int c, j;
+                RowVecMap<T, Lay, LOGL>::map(e, c, j);
                 const bool rowok = e < TOT && c < rlim;
                 mode[u] = !rowok || j >= len ? 0 : (j + V <= len ? 1 : 2);
-                buf[u] = __ldg((const TV*)(mode[u] == 1 ? tb + (unsigned)c * (unsigned)rs + j : (const T*)in));
+                buf[u] = __ldg((const TV*)(mode[u] == 1 ? tb + (unsigned)c * (unsigned)rs + seg_j(j, seglog, segstride)
+                                                        : (const T*)in));
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
                 if (e >= TOT) continue;
-                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                int c, j;
+                RowVecMap<T, Lay, LOGL>::map(e, c, j);
                 T v[V];
                 vget<T>(buf[u], v);
                 if (mode[u] != 1) {
 #pragma unroll
                     for (int i = 0; i < V; i++)
-                        v[i] = (mode[u] == 2 && j + i < len) ? __ldg(tb + (unsigned)c * (unsigned)rs + j + i) : (T)0;
+                        v[i] = (mode[u] == 2 && j + i < len)
+                                   ? __ldg(tb + (unsigned)c * (unsigned)rs + seg_j(j + i, seglog, segstride)) : (T)0;
                 }
 #pragma unroll
                 for (int i = 0; i < V; i++) s[Lay::addr(c, j + i)] = v[i];
@@ -216,7 +262,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
         for (int e = threadIdx.x; e < C * L; e += NT) {
             const int c = e >> LOGL, j = e & (L - 1);
             T v = 0;
-            if (c < rlim && j < len) v = ld_conv<TIn, T>(in + (r0 + c) * rs + j);
+            if (c < rlim && j < len) v = ld_conv<TIn, T>(in + (r0 + c) * rs + seg_j(j, seglog, segstride));
             s[Lay::addr(c, perm ? brev(j, LOGL) : j)] = v;
         }
     }
@@ -228,7 +274,8 @@ template <class F, class Lay, int LOGL, class TOut, int EPIV>
 __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, TOut* out, long long r0, long long nrows,
                                            long long rs, long long len, bool vec, bool perm, const typename F::W* fs_full,
                                            const typename F::W* fs_lo, const typename F::W* fs_hi, int fs_h,
-                                           long long row0, int k2, const typename F::W& sc) {
+                                           long long row0, int k2, const typename F::W& sc, int seglog = 0,
+                                           long long segstride = 0) {
     typedef typename F::T T;
     typedef typename F::W W;
     typedef typename Vec<T>::type TV;
@@ -250,7 +297,8 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
             for (int u = 0; u < B; u++) {
                 const int e0 = threadIdx.x + (u0 + u) * NT;
                 const int e = e0 < TOT ? e0 : 0;                  // idle lanes read a valid slot
-                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                int c, j;
+                RowVecMap<T, Lay, LOGL>::map(e, c, j);
 #pragma unroll
                 for (int i = 0; i < V; i++) v[u][i] = s[Lay::addr(c, j + i)];
                 if (E::FS == 1) ld_wvec<W, V>(fs_full + ((i2b + c) & i2mask) * L + j, w[u]);
@@ -258,17 +306,18 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
 #pragma unroll
             for (int u = 0; u < B; u++) {
                 const int e = threadIdx.x + (u0 + u) * NT;
-                const int c = (e * V) >> LOGL, j = (e * V) & (L - 1);
+                int c, j;
+                RowVecMap<T, Lay, LOGL>::map(e < TOT ? e : 0, c, j);
                 if (e >= TOT || c >= rlim || j >= len) continue;
                 const unsigned i2r = brev((int)((i2b + c) & i2mask), k2);
 #pragma unroll
                 for (int i = 0; i < V; i++) v[u][i] = E::apply(f, v[u][i], w[u][i], fs_lo, fs_hi, fs_h, (unsigned)(j + i) * i2r, sc);
                 if (j + V <= len) {
-                    *(TV*)(ob + (unsigned)c * (unsigned)rs + j) = vmake<T>(v[u]);
+                    *(TV*)(ob + (unsigned)c * (unsigned)rs + seg_j(j, seglog, segstride)) = vmake<T>(v[u]);
                 } else {
 #pragma unroll
                     for (int i = 0; i < V; i++)
-                        if (j + i < len) ob[(unsigned)c * (unsigned)rs + j + i] = v[u][i];
+                        if (j + i < len) ob[(unsigned)c * (unsigned)rs + seg_j(j + i, seglog, segstride)] = v[u][i];
                 }
             }
         }
@@ -281,7 +330,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
             if (E::FS == 1) wf = __ldg(fs_full + i2 * L + j);
             T x = E::apply(f, s[Lay::addr(c, perm ? brev(j, LOGL) : j)], wf, fs_lo, fs_hi, fs_h,
                            (unsigned)j * (unsigned)brev((int)i2, k2), sc);
-            out[(r0 + c) * rs + j] = (TOut)x;
+            out[(r0 + c) * rs + seg_j(j, seglog, segstride)] = (TOut)x;
         }
     }
 }
@@ -311,12 +360,14 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
     const long long ntiles = (a.nrows + C - 1) / C;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
-        load_rows<F, Lay, LOGL, TIn>(s, (const TIn*)a.in, r0, a.nrows, a.in_rs, a.in_len, a.vec_in, INV && a.perm);
+        load_rows<F, Lay, LOGL, TIn>(s, (const TIn*)a.in, r0, a.nrows, a.in_rs, a.in_len, a.vec_in, INV && a.perm,
+                                     a.in_seg_log, a.in_seg_stride);
         __syncthreads();
         if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
         else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
-                                             !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc);
+                                             !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
+                                             a.out_seg_log, a.out_seg_stride);
         __syncthreads();
     }
 }
@@ -324,9 +375,13 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
 // ---------------------------------------------------------------- column pass
 template <class F, int LOGL> struct ColsK {
     typedef typename ColsTile<F, LOGL>::Lay Lay;
-    enum { TWS = TwPlace<F, LOGL, Lay::ELEMS, 1>::SMEM };
+    // interleaved column tiles are double-buffered with cp.async (the next
+    // tile streams in while the current one is transformed)
+    enum { PIPE = Lay::COL ? 1 : 0 };
+    enum { TWS = TwPlace<F, LOGL, (PIPE ? 2 : 1) * Lay::ELEMS, 1>::SMEM };
     static constexpr size_t smem() {
-        return (size_t)Lay::ELEMS * sizeof(typename F::T) + (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
+        return (PIPE ? 2 : 1) * (size_t)Lay::ELEMS * sizeof(typename F::T) +
+               (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
     }
 };
 
@@ -364,14 +419,49 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
     const long long cgroups = a.ncols / C;                 // host guarantees ncols % C == 0
     const long long ntiles = cgroups * a.nbatch;
     const unsigned irs = (unsigned)a.in_rs, ors = (unsigned)a.out_rs, n1 = (unsigned)a.n1;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    constexpr bool PIPE = K::PIPE && sizeof(TIn) == sizeof(T);
+    const bool pipe = PIPE && a.vec_in;
+    // cp.async the whole column tile `tile` into dst (zero-fill beyond in_len)
+    auto issue = [&](long long tile, T* dst) {
+        const long long b = tile / cgroups;
+        const long long cl0 = (tile - b * cgroups) * C;
+        const long long lin0 = a.col0 + cl0;
+        const T* tb = (const T*)a.in + b * a.in_bs + cl0;
+        int tfull, tzero;
+        col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
+#pragma unroll
+        for (int u = 0; u < NV; u++) {
+            const int e = threadIdx.x + u * NT;
+            if (e >= TOT) continue;
+            const int t = e / CV, c = (e % CV) * V;
+            int nb = 16;
+            if (t >= tfull) {
+                long long rem = t < tzero ? a.in_len - ((long long)t * a.n1 + lin0 + c) : 0;
+                nb = rem <= 0 ? 0 : (rem >= V ? 16 : (int)rem * (int)sizeof(T));
+            }
+            cp_async16(dst + Lay::addr(c, t), nb ? (const void*)(tb + (unsigned)t * irs + c) : a.in, nb);
+        }
+    };
+    int it = 0;
+    if (pipe) {
+        if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, s);
+        cp_async_commit();
+    }
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const long long b = tile / cgroups;
         const long long cl0 = (tile - b * cgroups) * C;
         const long long lin0 = a.col0 + cl0;        // logical column of c = 0
         const TIn* inb = (const TIn*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;
-        col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
-        if (a.vec_in && sizeof(TIn) == sizeof(T)) {
+        T* cur = s;
+        if (pipe) {
+            cur = s + (it & 1) * Lay::ELEMS;
+            const long long nxt = tile + gridDim.x;
+            if (nxt < ntiles) issue(nxt, s + ((it + 1) & 1) * Lay::ELEMS);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else if (a.vec_in && sizeof(TIn) == sizeof(T)) {
+            col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
             constexpr int B = NV < 4 ? NV : 4;
             const T* tb = (const T*)inb;
 #pragma unroll
@@ -405,6 +495,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 }
             }
         } else {
+            col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
             for (int e = threadIdx.x; e < L * C; e += NT) {
                 const int t = e / C, c = e % C;
                 T v = 0;
@@ -414,8 +505,8 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
             }
         }
         __syncthreads();
-        if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
-        else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
+        if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, cur, tw);
+        else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, cur, tw);
         col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
         TOut* outb = (TOut*)a.out + b * a.out_bs + cl0;
         if (a.vec_out && sizeof(TOut) == sizeof(T)) {
@@ -430,10 +521,10 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                     const int e0 = threadIdx.x + (u0 + u) * NT;
                     const int e = e0 < TOT ? e0 : 0;
                     const int t = e / CV, c = (e % CV) * V;
-                    if (Lay::COL) vget<T>(*(const TV*)(s + Lay::addr(c, t)), v[u]);
+                    if (Lay::COL) vget<T>(*(const TV*)(cur + Lay::addr(c, t)), v[u]);
                     else {
 #pragma unroll
-                        for (int i = 0; i < V; i++) v[u][i] = s[Lay::addr(c + i, t)];
+                        for (int i = 0; i < V; i++) v[u][i] = cur[Lay::addr(c + i, t)];
                     }
                     if (E::FS == 1) ld_wvec<W, V>(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
                 }
@@ -463,7 +554,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 if (t >= tzero || (t >= tfull && (long long)t * a.n1 + lin0 + c >= a.out_len)) continue;
                 W wf{};
                 if (E::FS == 1) wf = __ldg(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c);
-                T x = E::apply(f, s[Lay::addr(c, t)], wf, a.fs_lo, a.fs_hi, a.fs_h,
+                T x = E::apply(f, cur[Lay::addr(c, t)], wf, a.fs_lo, a.fs_hi, a.fs_h,
                                ((unsigned)lin0 + c) * (unsigned)brev(t, LOGL), a.sc);
                 outb[(unsigned)t * ors + c] = (TOut)x;
             }
@@ -504,19 +595,31 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
     const long long ntiles = (a.nrows + C - 1) / C;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
-        load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false);
-        load_rows<F, Lay, LOGL, TIn>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false);
+        load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false, a.in_seg_log,
+                                     a.in_seg_stride);
+        load_rows<F, Lay, LOGL, TIn>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false, a.in_seg_log,
+                                     a.in_seg_stride);
         __syncthreads();
         tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twf);
         tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sb, twf);
-        for (int e = threadIdx.x; e < C * L; e += NT) {
-            const int ix = Lay::addr(e >> LOGL, e & (L - 1));
-            sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
+        {
+            constexpr int R = L < 16 ? L : 16;
+            constexpr int PER = L / R;
+            for (int ch = threadIdx.x; ch < C * PER; ch += NT) {
+                const int c = ch / PER, b = ch % PER;
+                const int base = Lay::chunk_base(c, b * R);
+#pragma unroll
+                for (int t = 0; t < R; t++) {
+                    const int ix = base + t;          // R consecutive elements never cross a pad
+                    sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
+                }
+            }
         }
         __syncthreads();
         tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twi);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
-                                             a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc);
+                                             a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc, a.out_seg_log,
+                                             a.out_seg_stride);
         __syncthreads();
     }
 }
@@ -542,8 +645,10 @@ static mm_status launch_rows_e(const F& f, RowArgs<F> a, cudaStream_t st) {
     constexpr int L = 1 << LOGL;
     constexpr int V = Vec<T>::N;
     const size_t smem = K::smem();
-    a.vec_in = sizeof(TIn) == sizeof(T) && !(INV && a.perm) && a.in_rs % V == 0 && aligned16(a.in);
-    a.vec_out = sizeof(TOut) == sizeof(T) && !(!INV && a.perm) && a.out_rs % V == 0 && aligned16(a.out);
+    a.vec_in = sizeof(TIn) == sizeof(T) && !(INV && a.perm) && a.in_rs % V == 0 && a.in_seg_stride % V == 0 &&
+               (!a.in_seg_log || (1 << a.in_seg_log) >= V) && aligned16(a.in);
+    a.vec_out = sizeof(TOut) == sizeof(T) && !(!INV && a.perm) && a.out_rs % V == 0 && a.out_seg_stride % V == 0 &&
+                (!a.out_seg_log || (1 << a.out_seg_log) >= V) && aligned16(a.out);
     auto kern = k_rows<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
@@ -587,8 +692,10 @@ static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
     typedef PmulK<F, LOGL> K;
     constexpr int V = Vec<T>::N;
     const size_t smem = K::smem();
-    a.vec_in = sizeof(TIn) == sizeof(T) && a.a_rs % V == 0 && a.b_rs % V == 0 && aligned16(a.a) && aligned16(a.b);
-    a.vec_out = sizeof(TOut) == sizeof(T) && a.c_rs % V == 0 && aligned16(a.c);
+    a.vec_in = sizeof(TIn) == sizeof(T) && a.a_rs % V == 0 && a.b_rs % V == 0 && a.in_seg_stride % V == 0 &&
+               (!a.in_seg_log || (1 << a.in_seg_log) >= V) && aligned16(a.a) && aligned16(a.b);
+    a.vec_out = sizeof(TOut) == sizeof(T) && a.c_rs % V == 0 && a.out_seg_stride % V == 0 &&
+                (!a.out_seg_log || (1 << a.out_seg_log) >= V) && aligned16(a.c);
     auto kern = k_rows_pmul<F, LOGL, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;

@@ -322,35 +322,35 @@ def test_int_mul_c5_full_sampled(mm, O):
 
 
 # ------------------------------------------------------------------ four-step blocks
-@pytest.mark.parametrize("bits,p,g,k", [(32, P30, 3, 16), (64, PG, 7, 20)])
+def _loopback_exchange(sends, G):
+    """Equal-split all-to-all among G virtual ranks on one GPU."""
+    chunk = sends[0].numel() // G
+    return [torch.cat([sends[g][h * chunk:(h + 1) * chunk] for g in range(G)]) for h in range(G)]
+
+
+@pytest.mark.parametrize("bits,p,g,k", [(32, P30, 3, 16), (64, PG, 7, 20), (32, P30, 3, 20)])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_fourstep_blocks_loopback(mm, O, bits, p, g, k, G):
-    """Distributed layout on one GPU: G virtual ranks, column-block shards, a
-    loopback all-to-all; equals the single-GPU transform slice by slice."""
+    """The sharded transform of dist.py on one GPU: G virtual ranks, their
+    column-block shards, a loopback all-to-all; every rank's row block equals
+    its slice of the single-GPU transform, and the inverse restores the input."""
+    from paper_1407_3383_b200.dist import ShardedNtt
     w = O.root_of_unity(g, k, p)
     plan = mm.NttPlan(bits, p, k, w, 1)
-    inf = plan.info()
-    n1, n2 = inf["n1"], inf["n2"]
     x = residues(11, k, 1 << k, p)
-    xt = dev(x).reshape(n2, n1)
-    ref = plan.forward(dev(x), out=dev(x).clone(), order=mm.BITREV).reshape(n2, n1)
-    c1, r2 = n1 // G, n2 // G
-    colout = []
-    for r in range(G):
-        blk = xt[:, r * c1:(r + 1) * c1].contiguous()
-        colout.append(plan.fwd_cols(blk, torch.empty_like(blk), r * c1, c1))
-    rows = []
-    for h in range(G):   # rank h receives rows [h r2, (h+1) r2) of every rank's columns
-        full = torch.cat([colout[g_][h * r2:(h + 1) * r2] for g_ in range(G)], dim=1).contiguous()
-        rows.append(plan.fwd_rows(full, full, h * r2, r2))
-    got = torch.cat(rows, dim=0)
+    xt = dev(x)
+    ref = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    sh = [ShardedNtt(plan, rank=r, world=G) for r in range(G)]
+    n1 = sh[0].n1
+    xv = xt.view(torch.int64 if bits == 64 else torch.int32).reshape(-1, n1)
+    blocks = [xv[:, r * sh[0].c1:(r + 1) * sh[0].c1].contiguous().view(xt.dtype) for r in range(G)]
+    recv = _loopback_exchange([sh[r].forward_cols(blocks[r]) for r in range(G)], G)
+    rows = [sh[h].forward_rows(recv[h]) for h in range(G)]
+    got = torch.cat(rows, dim=0).reshape(-1)
     assert torch.equal(got.view(torch.int64 if bits == 64 else torch.int32),
                        ref.view(torch.int64 if bits == 64 else torch.int32))
-    # inverse: rows -> loopback all-to-all back -> cols
-    inv_rows = [plan.inv_rows(rows[h], torch.empty_like(rows[h]), h * r2, r2) for h in range(G)]
-    back = []
+    recv2 = _loopback_exchange([sh[h].inverse_rows(rows[h]) for h in range(G)], G)
+    back = [sh[r].inverse_cols(recv2[r]) for r in range(G)]
     for r in range(G):
-        blk = torch.cat([inv_rows[h][:, r * c1:(r + 1) * c1] for h in range(G)], dim=0).contiguous()
-        back.append(plan.inv_cols(blk, torch.empty_like(blk), r * c1, c1))
-    xr = torch.cat(back, dim=1)
-    assert np.array_equal(host(xr).reshape(-1), x)
+        assert torch.equal(back[r].view(torch.int64 if bits == 64 else torch.int32),
+                           blocks[r].view(torch.int64 if bits == 64 else torch.int32))
