@@ -362,6 +362,12 @@ def run_ours(args, world, rank, local):
         "ntt_cols_inv": (B * n * 4 + B * lc * 4, B * (1 << 8) * (1 << 7) * 8),
     }
     fam = max(prof, key=lambda k: prof[k][1]) if prof else None
+    # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_c3.json")) as fh:
+            traffic = json.load(fh)
+    except OSError:
+        traffic = {}
     roof = None
     kernels = {}
     sm_mhz_max = peaks.get("sm_max_mhz", 1965.0)
@@ -384,11 +390,12 @@ def run_ours(args, world, rank, local):
         if e["alu_frac"] >= e["hbm_frac"]:
             roof = {"bound": "alu", "kernel": fam, "achieved": e["Gbutterfly_per_s"],
                     "peak": round(alu_bfly_peak / 1e9, 1), "unit": "Gbutterfly/s", "frac": e["alu_frac"],
-                    "traffic": None, "hbm_frac": e["hbm_frac"],
+                    "traffic": traffic.get(fam), "algorithmic_bytes": kb[fam][0], "hbm_frac": e["hbm_frac"],
                     "peak_source": "derived: SMs x 128 int lanes/clk x 1965 MHz / 7 ops per butterfly"}
         else:
             roof = {"bound": "hbm", "kernel": fam, "achieved": e["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
-                    "frac": e["hbm_frac"], "traffic": None, "alu_frac": e["alu_frac"], "peak_source": peak_src}
+                    "frac": e["hbm_frac"], "traffic": traffic.get(fam), "algorithmic_bytes": kb[fam][0],
+                    "alu_frac": e["alu_frac"], "peak_source": peak_src}
 
     # ---- e2e: same step through the public API from pinned host buffers
     e2e_steps = max(1, min(args.steps, 5))

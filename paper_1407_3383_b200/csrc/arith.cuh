@@ -173,18 +173,42 @@ struct FpG {
         }
         return d;
     }
-    // 128-bit product from 32-bit partial products, then
-    // x = lo + 2^64 (h0 + 2^32 h1) = lo - h1 + h0 (2^32 - 1)  (mod p).
+    // 128-bit product from four 32 x 32 partial products (one mul/mad carry
+    // chain: IMAD / IMAD.HI with carry), then with x = r0 + r1 2^32 + r2 2^64
+    // + r3 2^96:  x = (r1:r0) - r3 + r2 (2^32 - 1)  (mod p), evaluated with
+    // carry/borrow flags instead of compares (Python-checked in DESIGN.md).
     __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
-        uint64_t lo = a * b;
-        uint64_t hi = __umul64hi(a, b);
-        uint32_t h0 = (uint32_t)hi, h1 = (uint32_t)(hi >> 32);
-        uint64_t t = lo - h1;
-        if (lo < h1) t -= EPS;
-        uint64_t u = ((uint64_t)h0 << 32) - h0;
-        uint64_t r = t + u;
-        if (r < u) r += EPS;
-        return r;
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
+        const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        uint32_t r0, r1, r2, r3;
+        asm("mul.lo.u32      %0, %4, %6;\n\t"
+            "mul.hi.u32      %1, %4, %6;\n\t"
+            "mad.lo.cc.u32   %1, %4, %7, %1;\n\t"
+            "madc.hi.u32     %2, %4, %7, 0;\n\t"
+            "mad.lo.cc.u32   %1, %5, %6, %1;\n\t"
+            "madc.hi.cc.u32  %2, %5, %6, %2;\n\t"
+            "madc.hi.u32     %3, %5, %7, 0;\n\t"
+            "mad.lo.cc.u32   %2, %5, %7, %2;\n\t"
+            "addc.u32        %3, %3, 0;"
+            : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+            : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+        uint32_t u0, u1, net;
+        asm("{\n\t.reg .u32 t0, t1, bw;\n\t"
+            "sub.cc.u32      t0, %3, %6;\n\t"     // t = (r1:r0) - r3, bw = -borrow
+            "subc.cc.u32     t1, %4, 0;\n\t"
+            "subc.u32        bw, 0, 0;\n\t"
+            "sub.cc.u32      t0, t0, bw;\n\t"     // borrow: t -= EPS (no second borrow)
+            "subc.u32        t1, t1, 0;\n\t"
+            "sub.cc.u32      %0, t0, %5;\n\t"     // u = t - r2, borrow b2
+            "subc.cc.u32     %1, t1, 0;\n\t"
+            "subc.u32        %2, 0, 0;\n\t"
+            "add.cc.u32      %1, %1, %5;\n\t"     // u += r2 2^32, net = carry + b2 in {0,1}
+            "addc.u32        %2, %2, 0;\n\t}"
+            : "=&r"(u0), "=&r"(u1), "=&r"(net)
+            : "r"(r0), "r"(r1), "r"(r2), "r"(r3));
+        // net = 1: one 2^64 wrap, add EPS (cannot overflow again)
+        uint64_t r = ((uint64_t)u1 << 32) | u0;
+        return r + (uint64_t)(0u - net);   // 0u - net = net ? 0xFFFFFFFF : 0
     }
     __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
