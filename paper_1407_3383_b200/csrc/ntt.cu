@@ -12,6 +12,7 @@
 //   The inverse runs the steps backwards with w^-1.
 #include "common.h"
 #include "ntt_kernels.cuh"
+#include "fast32.h"
 #include <new>
 #include <map>
 #include <mutex>
@@ -89,6 +90,16 @@ __global__ void k_fs_table(W* t, int k1, int k2, E w, uint64_t p) {
         long long i2 = i >> k1, j1 = i & ((1ll << k1) - 1);
         uint64_t e = (uint64_t)j1 * (uint64_t)brev((int)i2, k2);
         tw_set(t, i, (E)tw_pow(w, e, p), p);
+    }
+}
+
+// scaled step-2 table for the 32-bit fused product: t[i2 n1 + j1] = w^(j1 [i2]_k2) s mod p
+__global__ void k_fs_table_scaled32(uint2* t, int k1, int k2, uint32_t w, uint32_t s, uint32_t p) {
+    const long long cnt = 1ll << (k1 + k2);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x) {
+        long long i2 = i >> k1, j1 = i & ((1ll << k1) - 1);
+        uint64_t e = (uint64_t)j1 * (uint64_t)brev((int)i2, k2);
+        tw_set(t, i, dmulmod32(dpow32(w, e, p), s, p), p);
     }
 }
 
@@ -253,6 +264,10 @@ struct mm_ntt_plan {
     uint64_t ninv;           // n^-1 mod p
     uint64_t ninv_r;         // n^-1 2^32 mod p (32-bit: after REDC)
     uint32_t pinv;           // p^-1 mod 2^32
+    // specialised 2^16 = 256 x 256 path (ntt_fast32.cu), 32-bit only
+    bool fast16 = false;
+    void* fs_pm_i = nullptr;   // inverse step-2 table times n^-1 2^32
+    mm::f32::Tw15 tw_f1, tw_i1, tw_f2, tw_i2;   // level-table entries 1..15 (host copies)
     void* ws = nullptr;      // lazily allocated workspace (bit-mirror permutations)
     size_t ws_bytes = 0;
     std::mutex mu;
@@ -297,6 +312,12 @@ extern template mm_status launch_pmul<FpG, uint64_t, uint64_t>(const FpG&, const
 extern template mm_status launch_pmul<FpG, uint16_t, uint64_t>(const FpG&, const PmulArgs<FpG>&, cudaStream_t);
 
 // ---- plan construction
+// entries 1..15 of the level table of a length-2^k transform with root r: tw[m + i] = r^(i 2^k / 2m)
+static void tw15(f32::Tw15* T, uint64_t r, int k, uint64_t p) {
+    T->w[0] = make_uint2(0, 0);
+    for (int m = 1; m <= 8; m <<= 1)
+        for (int i = 0; i < m; i++) T->w[m + i] = mkw32(hpowmod(r, (uint64_t)i << (k - 1 - (31 - __builtin_clz(m))), p), p);
+}
 template <class W, class E>
 static mm_status build_level(void** dst, int k, E w, uint64_t p) {
     size_t L = (size_t)1 << k;
@@ -363,6 +384,24 @@ static mm_status build_tables(mm_ntt_plan* P) {
             if ((s = build_fs_full<W, E>(&P->fs_full_f, P->k1, P->k2, (E)w, p)) != MM_OK) return s;
             if ((s = build_fs_full<W, E>(&P->fs_full_i, P->k1, P->k2, (E)winv, p)) != MM_OK) return s;
         }
+        if (P->word_bits == 32 && P->k1 == 8 && P->k2 == 8) {
+            // the specialised 256 x 256 kernels: host copies of the small level-table
+            // entries, and the inverse step-2 table with n^-1 2^32 folded in
+            uint64_t r1 = hpowmod(w, n2, p), r1i = hpowmod(winv, n2, p);
+            uint64_t r2 = hpowmod(w, n1, p), r2i = hpowmod(winv, n1, p);
+            tw15(&P->tw_f1, r1, P->k1, p);
+            tw15(&P->tw_i1, r1i, P->k1, p);
+            tw15(&P->tw_f2, r2, P->k2, p);
+            tw15(&P->tw_i2, r2i, P->k2, p);
+            MM_CUDA_TRY(cudaMalloc(&P->fs_pm_i, ((size_t)1 << k) * sizeof(uint2)));
+            {
+                LaunchScope ls("twiddle_fs_table", 0);
+                k_fs_table_scaled32<<<256, 256>>>((uint2*)P->fs_pm_i, P->k1, P->k2, (uint32_t)winv,
+                                                  (uint32_t)P->ninv_r, (uint32_t)p);
+            }
+            MM_LAUNCH_CHECK();
+            P->fast16 = true;
+        }
     }
     MM_CUDA_TRY(cudaDeviceSynchronize());
     return MM_OK;
@@ -371,7 +410,7 @@ static mm_status build_tables(mm_ntt_plan* P) {
 static void free_plan(mm_ntt_plan* P) {
     if (!P) return;
     void* bufs[] = {P->lvl_f1,  P->lvl_i1,  P->lvl_f2,    P->lvl_i2,    P->fs_lo_f, P->fs_hi_f,
-                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->ws};
+                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->fs_pm_i, P->ws};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -681,6 +720,47 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
     return MM_OK;
 }
 
+// n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
+static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, const uint32_t* b, long long lb,
+                                uint32_t* c, long long lc, long long batch, uint32_t* WA, uint32_t* WB,
+                                cudaStream_t st) {
+    const f32::Fld f{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+    const long long n = 1ll << P->k;
+    mm_status s;
+    for (int op = 0; op < 2; op++) {
+        f32::ColFwdArgs cf{};
+        cf.in = op == 0 ? a : b;
+        cf.out = op == 0 ? WA : WB;
+        cf.nbatch = batch;
+        cf.in_bs = cf.in_len = op == 0 ? la : lb;
+        cf.out_bs = n;
+        cf.lvl = (const uint2*)P->lvl_f2;
+        cf.fs = (const uint2*)P->fs_full_f;
+        cf.tc = P->tw_f2;
+        cf.f = f;
+        if ((s = f32::launch_col_fwd(cf, st)) != MM_OK) return s;
+    }
+    f32::RowPmulArgs rp{};
+    rp.A = WA; rp.B = WB; rp.C = WA;
+    rp.nrows = batch << P->k2;
+    rp.lvl_f = (const uint2*)P->lvl_f1;
+    rp.lvl_i = (const uint2*)P->lvl_i1;
+    rp.fsi = (const uint2*)P->fs_pm_i;
+    rp.tf = P->tw_f1;
+    rp.ti = P->tw_i1;
+    rp.f = f;
+    if ((s = f32::launch_row_pmul(rp, st)) != MM_OK) return s;
+    f32::ColInvArgs ci{};
+    ci.in = WA; ci.out = c;
+    ci.nbatch = batch;
+    ci.in_bs = n;
+    ci.out_bs = ci.out_len = lc;
+    ci.lvl = (const uint2*)P->lvl_i2;
+    ci.tc = P->tw_i2;
+    ci.f = f;
+    return f32::launch_col_inv(ci, st);
+}
+
 // c = a * b for `batch` rows; TIn = input element type (uint16 limbs for int_mul)
 template <class F, class TIn, class TOut>
 static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const TIn* b, long long lb, TOut* c,
@@ -708,6 +788,10 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     if (s != MM_OK) return s;
     T* WA = (T*)ws;
     T* WB = WA + n * batch;
+    if constexpr (sizeof(T) == 4 && sizeof(TIn) == 4 && sizeof(TOut) == 4) {
+        if (P->fast16) return fast16_product(P, (const uint32_t*)a, la, (const uint32_t*)b, lb, (uint32_t*)c, lc,
+                                             batch, (uint32_t*)WA, (uint32_t*)WB, st);
+    }
     // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb
     for (int op = 0; op < 2; op++) {
         ColArgs<F> cc{};

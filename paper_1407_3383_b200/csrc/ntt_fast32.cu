@@ -1,0 +1,413 @@
+// ntt_fast32.cu -- the 2^16-point four-step (n1 = n2 = 256) for p < 2^30,
+// specialised for BASELINE C3 (see fast32.h for the pass structure).
+//
+// Every pass is two radix-16 register groups around one shared-memory
+// exchange.  A "table" group (spans 128..16 of a 256-point transform) works
+// on the 16 elements lo + 16 t of one transform, so its 15 twiddles
+// tw[m + lo + 16 k] depend on lo only; a "constant" group (spans 8..1) works
+// on 16 consecutive elements, so its 15 twiddles are the level-table entries
+// 1..15, passed by value as kernel parameters (constant bank operands, no
+// loads).  Global loads / stores go straight between registers and HBM in
+// the table group's layout (a warp touches whole 128-byte lines).
+//
+// Butterflies (Harvey's lazy forms, values in [0, 2p) / [0, 4p), p < 2^30):
+//   DIF (Gentleman-Sande): (x, y) -> (x + y, (x - y) w)
+//   DIT (Cooley-Tukey)   : (x, y) -> (x + y w, x - y w)
+// with the fixed-multiplicand product of Function 8:
+// c = hi(d psi), d w - c p in [0, 2p).  The DIF sum is written as
+// min(x + y, x + y - 2p) with the second term opaque to ptxas, so it becomes
+// IADD3 + VIADDMNMX on the ALU pipe and the butterfly is 3 ALU + 3 FMA-pipe
+// instructions (the plain form puts the sum on the FMA pipe as IMAD.IADD).
+#include "common.h"
+#include "arith.cuh"
+#include "fast32.h"
+
+namespace mm {
+namespace f32 {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t add_sub(uint32_t x, uint32_t y, uint32_t c) {
+    uint32_t t;
+    asm("{ .reg .u32 r; add.u32 r, %1, %2; sub.u32 %0, r, %3; }" : "=r"(t) : "r"(x), "r"(y), "r"(c));
+    return t;
+}
+// Function 8 (lazy): x w mod p in [0, 2p) for any x < 2^32
+__device__ __forceinline__ uint32_t mulw(uint32_t x, uint2 w, const Fld& f) {
+    uint32_t c = __umulhi(x, w.y);
+    return x * w.x - c * f.p;
+}
+__device__ __forceinline__ void dif(uint32_t& x, uint32_t& y, uint2 w, const Fld& f) {
+    uint32_t t = add_sub(x, y, f.p2);
+    uint32_t d = x - y + f.p2;
+    x = umin(x + y, t);
+    y = mulw(d, w, f);
+}
+__device__ __forceinline__ void dif1(uint32_t& x, uint32_t& y, const Fld& f) {
+    uint32_t t = add_sub(x, y, f.p2);
+    uint32_t d = x - y + f.p2;
+    x = umin(x + y, t);
+    y = umin(d, d - f.p2);
+}
+__device__ __forceinline__ void dit(uint32_t& x, uint32_t& y, uint2 w, const Fld& f) {
+    uint32_t xx = umin(x, x - f.p2);
+    uint32_t t = mulw(y, w, f);
+    x = xx + t;
+    y = xx - t + f.p2;
+}
+__device__ __forceinline__ void dit1(uint32_t& x, uint32_t& y, const Fld& f) {
+    uint32_t xx = umin(x, x - f.p2);
+    uint32_t yy = umin(y, y - f.p2);
+    x = xx + yy;
+    y = xx - yy + f.p2;
+}
+// Montgomery REDC (Function 13), subtractive form, lazy:
+// x y 2^-32 mod p in (0, 2p) for x y < 2^32 p.
+__device__ __forceinline__ uint32_t redc(uint32_t x, uint32_t y, const Fld& f) {
+    uint32_t lo = x * y, hi = __umulhi(x, y);
+    uint32_t m = lo * f.pinv;
+    return hi - __umulhi(m, f.p) + f.p;
+}
+// [0, 4p) -> [0, p)
+__device__ __forceinline__ uint32_t canon4(uint32_t x, const Fld& f) {
+    x = umin(x, x - f.p2);
+    return umin(x, x - f.p);
+}
+
+// ---- register groups on v[16]
+// DIF, elements lo + 16 t: level half-spans 128, 64, 32, 16 (h = 8, 4, 2, 1 in t)
+template <int NV>
+__device__ __forceinline__ void dif_tab(uint32_t (*v)[16], int lo, const uint2* tw, const Fld& f, bool half0) {
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            if (t & h) continue;
+            const uint2 w = tw[16 * h + lo + 16 * (t & (h - 1))];
+#pragma unroll
+            for (int u = 0; u < NV; u++) {
+                if (h == 8 && half0) v[u][t + 8] = mulw(v[u][t], w, f);   // (x, 0) -> (x, x w)
+                else dif(v[u][t], v[u][t + h], w, f);
+            }
+        }
+    }
+}
+// DIF, 16 consecutive elements: half-spans 8, 4, 2, 1 with constant twiddles
+__device__ __forceinline__ void dif_const(uint32_t* v, const Tw15& T, const Fld& f) {
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            if (t & h) continue;
+            const int k = t & (h - 1);
+            if (k == 0) dif1(v[t], v[t + h], f);
+            else dif(v[t], v[t + h], T.w[h + k], f);
+        }
+    }
+}
+// DIT, 16 consecutive elements: half-spans 1, 2, 4, 8 with constant twiddles
+__device__ __forceinline__ void dit_const(uint32_t* v, const Tw15& T, const Fld& f) {
+#pragma unroll
+    for (int h = 1; h <= 8; h <<= 1) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            if (t & h) continue;
+            const int k = t & (h - 1);
+            if (k == 0) dit1(v[t], v[t + h], f);
+            else dit(v[t], v[t + h], T.w[h + k], f);
+        }
+    }
+}
+// DIT, elements lo + 16 t: half-spans 16, 32, 64, 128
+__device__ __forceinline__ void dit_tab(uint32_t* v, int lo, const uint2* tw, const Fld& f) {
+#pragma unroll
+    for (int h = 1; h <= 8; h <<= 1) {
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            if (t & h) continue;
+            dit(v[t], v[t + h], tw[16 * h + lo + 16 * (t & (h - 1))], f);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- column passes
+// Tile = one batch row's 256 x 32 block (32 adjacent columns), shared layout
+// [t][c] (lane = column: every shared access is conflict-free).  Warp w owns
+// the table-group chunks lo in {w, w + 8} and the constant-group chunks
+// (rows 16 b .. 16 b + 15) b in {w, w + 8}.  The next tile streams into
+// shared memory with cp.async (LDGSTS, zero-filled beyond the valid prefix)
+// while the current one is transformed.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// rows [0, RIN) of the 32-column block `tile` -> st[row * 32 + c]; element
+// (row, col) of batch row b is in[b * in_bs + row * 256 + col], valid iff
+// row * 256 + col < len (zeros beyond).  VEC: 16-byte copies (in_bs % 4 == 0).
+template <int RIN, bool MASK, bool VEC>
+__device__ __forceinline__ void issue_cols(uint32_t* st, const uint32_t* in, long long tile, long long in_bs,
+                                           long long len) {
+    const long long b = tile >> 3;
+    const int cg = (int)(tile & 7) << 5;
+    const uint32_t* src = in + b * in_bs + cg;
+    const int lim = (int)(len < (1 << 16) ? len : (1 << 16)) - cg;   // valid iff row * 256 + cc < lim
+    if (VEC) {
+#pragma unroll
+        for (int k = 0; k < RIN * 8 / NT; k++) {
+            const int e = threadIdx.x + NT * k, row = e >> 3, cc = (e & 7) * 4;
+            int nb = 16;
+            if (MASK) {
+                const int rem = lim - row * 256 - cc;
+                nb = rem <= 0 ? 0 : (rem >= 4 ? 16 : 4 * rem);
+            }
+            cp_async16(st + row * 32 + cc, nb ? (const void*)(src + row * 256 + cc) : (const void*)in, nb);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < RIN * 32 / NT; k++) {
+            const int e = threadIdx.x + NT * k, row = e >> 5, cc = e & 31;
+            const int nb = (!MASK || row * 256 + cc < lim) ? 4 : 0;
+            cp_async4(st + row * 32 + cc, nb ? (const void*)(src + row * 256 + cc) : (const void*)in, nb);
+        }
+    }
+}
+
+template <bool HALF> struct ColFwdSmem {
+    static constexpr int RIN = HALF ? 128 : 256;
+    static constexpr size_t bytes = 256 * sizeof(uint2) + (RIN + 256) * 32 * sizeof(uint32_t);
+};
+
+template <bool HALF, bool MASK, bool VEC>
+__global__ void __launch_bounds__(NT, HALF ? 4 : 3) k_col_fwd(ColFwdArgs a) {
+    constexpr int RIN = ColFwdSmem<HALF>::RIN;
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint2* tws = (uint2*)smem;
+    uint32_t* st = (uint32_t*)(tws + 256);     // staging: next tile's input rows
+    uint32_t* s = st + RIN * 32;               // working tile
+    for (int i = threadIdx.x; i < 256; i += NT) tws[i] = a.lvl[i];
+    const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long ntiles = a.nbatch * 8;
+    const Fld f = a.f;
+    if ((long long)blockIdx.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, blockIdx.x, a.in_bs, a.in_len);
+    cp_commit();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long b = tile >> 3;
+        const int col = ((int)(tile & 7) << 5) + c;
+        cp_wait_all();
+        __syncthreads();
+        uint32_t v[2][16];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[u][t] = (HALF && t >= 8) ? 0u : st[(w + 8 * u + 16 * t) * 32 + c];
+        __syncthreads();
+        if (tile + gridDim.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, tile + gridDim.x, a.in_bs, a.in_len);
+        cp_commit();
+        dif_tab<1>(&v[0], w, tws, f, HALF);
+        dif_tab<1>(&v[1], w + 8, tws, f, HALF);
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+            for (int t = 0; t < 16; t++) s[(w + 8 * u + 16 * t) * 32 + c] = v[u][t];
+        __syncthreads();
+        uint32_t* dst = a.out + b * a.out_bs + col;
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int r0 = 16 * (w + 8 * u);
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[u][t] = s[(r0 + t) * 32 + c];
+            dif_const(v[u], a.tc, f);
+            // step 2: row r0 + t holds frequency [r0 + t]_8; times w^(col [i2]_8)
+#pragma unroll
+            for (int t = 0; t < 16; t++) {
+                const int row = r0 + t;
+                dst[row * 256] = mulw(v[u][t], __ldg(a.fs + row * 256 + col), f);
+            }
+        }
+    }
+}
+
+constexpr size_t COL_INV_SMEM = 256 * sizeof(uint2) + 2 * 256 * 32 * sizeof(uint32_t);
+
+template <bool MASK>
+__global__ void __launch_bounds__(NT, 3) k_col_inv(ColInvArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint2* tws = (uint2*)smem;
+    uint32_t* buf = (uint32_t*)(tws + 256);    // two 256 x 32 tiles
+    for (int i = threadIdx.x; i < 256; i += NT) tws[i] = a.lvl[i];
+    const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long ntiles = a.nbatch * 8;
+    const Fld f = a.f;
+    if ((long long)blockIdx.x < ntiles) issue_cols<256, false, true>(buf, a.in, blockIdx.x, a.in_bs, 1 << 16);
+    cp_commit();
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const long long b = tile >> 3;
+        const int col = ((int)(tile & 7) << 5) + c;
+        uint32_t* s = buf + (it & 1) * 256 * 32;
+        cp_wait_all();
+        __syncthreads();
+        if (tile + gridDim.x < ntiles)
+            issue_cols<256, false, true>(buf + ((it + 1) & 1) * 256 * 32, a.in, tile + gridDim.x, a.in_bs, 1 << 16);
+        cp_commit();
+        uint32_t v[2][16];
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int r0 = 16 * (w + 8 * u);
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[u][t] = s[(r0 + t) * 32 + c];
+            dit_const(v[u], a.tc, f);
+#pragma unroll
+            for (int t = 0; t < 16; t++) s[(r0 + t) * 32 + c] = v[u][t];
+        }
+        __syncthreads();
+        uint32_t* dst = a.out + b * a.out_bs + col;
+        const int lim = (int)(a.out_len - col);
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int lo = w + 8 * u;
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[u][t] = s[(lo + 16 * t) * 32 + c];
+            dit_tab(v[u], lo, tws, f);
+#pragma unroll
+            for (int t = 0; t < 16; t++) {
+                const int row = lo + 16 * t;
+                if (!MASK || row * 256 < lim) dst[row * 256] = canon4(v[u][t], f);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- fused product rows
+// Tile = 16 rows of 256; thread (r, lo) = (tid >> 4, tid & 15).  Shared rows
+// are padded by one 16-byte chunk per 8 (chunk q at q + (q >> 3)) with a row
+// pitch of 76 chunks (= 4 mod 8): the strided 4-byte accesses of the table
+// groups (16 lanes x 4 chunks per row, two rows per warp) and the 16-byte
+// accesses of the constant group (8 lanes per phase) are both conflict-free,
+// and every address is a per-thread base plus an immediate.
+constexpr int ROWP = 76 * 4;   // words per padded row
+__device__ __forceinline__ int pad_word(int j) { return j + 4 * (j >> 5); }   // 4 * ((j >> 2) + (j >> 5)) + (j & 3)
+
+__global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
+    __shared__ uint2 twf[256], twi[256];
+    __shared__ __align__(16) uint32_t sa[16 * ROWP];
+    __shared__ __align__(16) uint32_t sb[16 * ROWP];
+    for (int i = threadIdx.x; i < 256; i += NT) {
+        twf[i] = a.lvl_f[i];
+        twi[i] = a.lvl_i[i];
+    }
+    const int r = threadIdx.x >> 4, lo = threadIdx.x & 15;
+    const long long ntiles = a.nrows >> 4;
+    const Fld f = a.f;
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row = tile * 16 + r;
+        uint32_t v[2][16];
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            v[0][t] = __ldg(a.A + row * 256 + lo + 16 * t);
+            v[1][t] = __ldg(a.B + row * 256 + lo + 16 * t);
+        }
+        dif_tab<2>(v, lo, twf, f, false);
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            const int ix = r * ROWP + pad_word(lo + 16 * t);
+            sa[ix] = v[0][t];
+            sb[ix] = v[1][t];
+        }
+        __syncthreads();
+        // constant group: 16 consecutive spectrum values of both operands
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int ix = r * ROWP + pad_word(16 * lo + 4 * i);
+            const uint4 x = *(const uint4*)(sa + ix);
+            const uint4 y = *(const uint4*)(sb + ix);
+            v[0][4 * i] = x.x; v[0][4 * i + 1] = x.y; v[0][4 * i + 2] = x.z; v[0][4 * i + 3] = x.w;
+            v[1][4 * i] = y.x; v[1][4 * i + 1] = y.y; v[1][4 * i + 2] = y.z; v[1][4 * i + 3] = y.w;
+        }
+        dif_const(v[0], a.tf, f);
+        dif_const(v[1], a.tf, f);
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[0][t] = redc(v[0][t], v[1][t], f);   // P:952 entry-wise product
+        dit_const(v[0], a.ti, f);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int ix = r * ROWP + pad_word(16 * lo + 4 * i);
+            *(uint4*)(sa + ix) = make_uint4(v[0][4 * i], v[0][4 * i + 1], v[0][4 * i + 2], v[0][4 * i + 3]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[0][t] = sa[r * ROWP + pad_word(lo + 16 * t)];
+        dit_tab(v[0], lo, twi, f);
+        // inverse step 2 (w^-(j1 [i2]_8)) with n^-1 2^32 folded in
+        const uint2* fsr = a.fsi + (row & 255) * 256 + lo;
+        uint32_t* dst = a.C + row * 256 + lo;
+#pragma unroll
+        for (int t = 0; t < 16; t++) dst[16 * t] = mulw(v[0][t], __ldg(fsr + 16 * t), f);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- launchers
+template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    long long cap = (long long)num_sms() * per_sm;
+    return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+}
+
+template <bool HALF, bool MASK, bool VEC>
+static mm_status col_fwd_k(const ColFwdArgs& a, cudaStream_t st) {
+    auto kern = k_col_fwd<HALF, MASK, VEC>;
+    const size_t smem = ColFwdSmem<HALF>::bytes;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {
+        LaunchScope ls("ntt_cols_fwd", st);
+        kern<<<grid_of(kern, a.nbatch * 8, smem), NT, smem, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_col_fwd(const ColFwdArgs& a, cudaStream_t st) {
+    const bool half = a.in_len <= (1 << 15);
+    const bool mask = a.in_len != (half ? (1 << 15) : (1 << 16));
+    const bool vec = a.in_bs % 4 == 0 && ((uintptr_t)a.in & 15) == 0;
+    if (half) {
+        if (!mask) return vec ? col_fwd_k<true, false, true>(a, st) : col_fwd_k<true, false, false>(a, st);
+        return vec ? col_fwd_k<true, true, true>(a, st) : col_fwd_k<true, true, false>(a, st);
+    }
+    if (!mask) return vec ? col_fwd_k<false, false, true>(a, st) : col_fwd_k<false, false, false>(a, st);
+    return vec ? col_fwd_k<false, true, true>(a, st) : col_fwd_k<false, true, false>(a, st);
+}
+mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st) {
+    if (a.nrows % 16) return set_err(MM_E_UNSUPPORTED_SIZE, "row count %lld is not a multiple of 16", a.nrows);
+    {
+        LaunchScope ls("pmul_rows_fourstep", st);
+        k_row_pmul<<<grid_of(k_row_pmul, a.nrows / 16, 0), NT, 0, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_col_inv(const ColInvArgs& a, cudaStream_t st) {
+    if (a.in_bs % 4 || ((uintptr_t)a.in & 15)) return set_err(MM_E_ARG, "inverse column pass needs 16-byte aligned rows");
+    auto kern = a.out_len == (1 << 16) ? k_col_inv<false> : k_col_inv<true>;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COL_INV_SMEM));
+    {
+        LaunchScope ls("ntt_cols_inv", st);
+        kern<<<grid_of(kern, a.nbatch * 8, COL_INV_SMEM), NT, COL_INV_SMEM, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+}  // namespace f32
+}  // namespace mm

@@ -245,6 +245,26 @@ def test_poly_mul_ragged(mm, O, bits, p, g):
             assert np.array_equal(c[r], ref), (la, lb, r)
 
 
+@pytest.mark.parametrize("p,g", [(P30, 3), (469762049, 3)])
+def test_poly_mul_fast16_shapes(mm, O, p, g):
+    # every product length in (2^15, 2^16] runs the specialised 256 x 256
+    # passes: half-zero / full / ragged inputs, exact and truncated outputs
+    cases = [(1 << 15, 1 << 15, 3), (30001, 20000, 2), (40000, 20000, 2), (1 << 16, 1, 1), (1, 1 << 16, 1),
+             (32769, 32768, 1), (16385, 16384, 2)]
+    rng = random.Random(p)
+    for la, lb, batch in cases:
+        a = residues(rng.randrange(1 << 30), 1, la * batch, p).reshape(batch, la)
+        b = residues(rng.randrange(1 << 30), 2, lb * batch, p).reshape(batch, lb)
+        c = u64(host(mm.poly_mul(dev(a), dev(b), p, g)))
+        for r in range(batch):
+            assert np.array_equal(c[r], O.poly_mul_ntt(a[r], b[r], p, g)), (la, lb, r)
+    # extreme residues: all p-1 (every lazy range at its maximum)
+    a = np.full((2, 1 << 15), p - 1, dtype=np.uint32)
+    c = u64(host(mm.poly_mul(dev(a), dev(a), p, g)))
+    for r in range(2):
+        assert np.array_equal(c[r], O.poly_mul_ntt(a[r], a[r], p, g))
+
+
 def test_poly_mul_c3_small_batch(mm, O):
     p, g = P30, 3
     B, d = 8, 1 << 15

@@ -37,6 +37,9 @@ def family(name: str) -> str:
 
 def scope_name(fam: str) -> str:
     """ncu family -> the LaunchScope name bench.py reports."""
+    fast = {"k_col_fwd": "ntt_cols_fwd", "k_col_inv": "ntt_cols_inv", "k_row_pmul": "pmul_rows_fourstep"}
+    if fam in fast:   # the specialised 2^16 = 256 x 256 kernels (ntt_fast32.cu)
+        return fast[fam]
     if fam.startswith("k_cols_fwd"):
         return "ntt_cols_fwd"
     if fam.startswith("k_cols_inv"):
