@@ -37,6 +37,7 @@ PG = (1 << 64) - (1 << 32) + 1
 C3_BATCH, C3_D = 4096, 1 << 15        # products per rank, coefficients per operand
 C3_LOG = 16                           # transform length 2^16
 C3_BFLY_PER_PROD = 3 * (1 << (C3_LOG - 1)) * C3_LOG
+C3_LDC = 1 << C3_LOG                  # output row stride (words): 128-byte aligned rows
 
 
 def c3_butterflies(batch: int) -> int:
@@ -61,20 +62,35 @@ def root_of_unity(p: int, g: int, k: int) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
-              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
-              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    """SM clocks + throttle reasons sampled during the timed region: NVML
+    (pynvml) polled every 2 ms from a thread, else nvidia-smi at 100 ms."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []          # (sm_mhz, max_mhz, reason bits) from NVML
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
+            fields = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+                      "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+                      "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(fields)}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -83,11 +99,31 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def mark(self, start: bool):
+        """Bracket the timed region (samples outside it are dropped when any fall inside)."""
+        n = len(self.samples) + len(self.lines)
+        if start:
+            self.i0 = n
+        else:
+            self.i1 = n
+
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -97,6 +133,15 @@ class ClockSampler:
 
     def summary(self) -> dict:
         sm, mx, reasons = [], 0.0, set()
+        i0, i1 = getattr(self, "i0", 0), getattr(self, "i1", None)
+        if self.samples and i1 is not None and i1 > i0 + 2:
+            self.samples = self.samples[i0:i1]
+        for clk, m, bits in self.samples:
+            sm.append(float(clk))
+            mx = max(mx, float(m))
+            for nm, bit in self.REASONS.items():
+                if bits & bit:
+                    reasons.add(nm)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
@@ -113,7 +158,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def dist_setup():
@@ -239,11 +284,19 @@ def extras_run(mm, torch, dev, peaks):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    # ALU probe (register-only butterflies)
+    # ALU probe (register-only butterflies) and per-class instruction issue rates
     b32 = mm.probe_butterfly(32, 4000)
     b64 = mm.probe_butterfly(64, 1000)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    issue = {}
+    for kind, nm in enumerate(["IMAD", "IMAD.HI", "IADD3", "VIADDMNMX", "IMAD.HI+2xIADD3"]):
+        r = mm.probe_issue(kind, 4000)
+        issue[nm] = round(r / (nsm * clk), 3)
     out["alu_probe"] = {"bfly32_G_per_s": round(b32 / 1e9, 1), "bfly64_G_per_s": round(b64 / 1e9, 1),
-                        "note": "register-resident butterflies, full grid, no memory traffic"}
+                        "warp_inst_per_clk_per_SM": issue,
+                        "note": "register-resident butterflies / single-class instruction chains, full grid, "
+                                "no memory traffic; per-clk rates at the max SM clock"}
 
     # C2: elementwise over 2^28 uint32 pairs, p = 3221225473
     n = 1 << 28
@@ -296,6 +349,15 @@ def extras_run(mm, torch, dev, peaks):
                                              "us_per_call_cuda_graph": round(ms_graph * 1e3, 2),
                                              "Gbutterfly_per_s_graph": round(bf / (ms_graph * 1e-3) / 1e9, 2)}
 
+    # C3 with the packed output layout (ldc = 2^16 - 1: rows not 32-byte aligned)
+    a3 = gen.residues_torch(gen.config_seed(3), 1, C3_BATCH * C3_D, P30, dev).view(torch.uint32).reshape(C3_BATCH, C3_D)
+    b3 = gen.residues_torch(gen.config_seed(3), 2, C3_BATCH * C3_D, P30, dev).view(torch.uint32).reshape(C3_BATCH, C3_D)
+    c3 = torch.empty((C3_BATCH, 2 * C3_D - 1), dtype=torch.uint32, device=dev)
+    ms = tloop(lambda: mm.poly_mul(a3, b3, P30, G30, out=c3), 10)
+    out["C3_packed_output"] = {"ms": round(ms, 4), "Gbutterfly_per_s": round(c3_butterflies(C3_BATCH) / (ms * 1e-3) / 1e9, 1),
+                               "note": "same C3 products, c rows packed at 2^16 - 1 words"}
+    del a3, b3, c3
+
     # C4: 8 x 2^24 Goldilocks forward NTT (four-step 2^12 x 2^12)
     w24 = root_of_unity(PG, 7, 24)
     plan4 = mm.NttPlan(64, PG, 24, w24, 8)
@@ -336,7 +398,12 @@ def run_ours(args, world, rank, local):
     start = rank * B * d             # each rank draws its own products
     a = gen.residues_torch(gen.config_seed(3), 1, B * d, P30, dev, start=start).view(torch.uint32).reshape(B, d)
     b = gen.residues_torch(gen.config_seed(3), 2, B * d, P30, dev, start=start).view(torch.uint32).reshape(B, d)
-    c = torch.empty((B, lc), dtype=torch.uint32, device=dev)
+    # output rows at a 128-byte leading dimension (ldc = 2^16 words; the row's
+    # last word is padding, never written): packed rows of 2^16 - 1 words split
+    # 32-byte sectors between neighbouring column tiles (the packed
+    # layout is timed in extra.C3_packed_output)
+    c_pad = torch.empty((B, C3_LDC), dtype=torch.uint32, device=dev)
+    c = c_pad[:, :lc]
 
     def step():
         mm.poly_mul(a, b, P30, G30, out=c)
@@ -346,8 +413,10 @@ def run_ours(args, world, rank, local):
     cnt = {}
     with ClockSampler(local) as clk:
         ms_total = timed(step, args.steps, args.warmup, world,
-                         on_start=lambda: (cnt.__setitem__("n0", mm.launch_count()), mm.prof_enable(True)),
+                         on_start=lambda: (cnt.__setitem__("n0", mm.launch_count()), mm.prof_enable(True),
+                                           clk.mark(True)),
                          on_stop=lambda: (mm.prof_enable(False), cnt.__setitem__("n1", mm.launch_count())))
+        clk.mark(False)
     launches = cnt["n1"] - cnt["n0"]
     prof = mm.prof_collect()
     ms_step = ms_total / args.steps
@@ -371,10 +440,13 @@ def run_ours(args, world, rank, local):
     roof = None
     kernels = {}
     sm_mhz_max = peaks.get("sm_max_mhz", 1965.0)
-    # ALU roofline: 148 SMs x 4 SMSP x 32 lanes / clk integer issue, 7 integer ops per lazy
-    # Shoup butterfly -> butterflies/s ceiling at the max SM clock.
+    # ALU roofline: integer multiplies issue only to the fmaheavy pipe,
+    # IMAD at 2 and IMAD.HI at 4 cycles per warp per SMSP (mm_probe_issue, ncu pipe
+    # counters).  The lazy Shoup butterfly needs IMAD.HI + 2 IMAD = 8 heavy cycles per
+    # warp (its 3 adds/mins go to the ALU pipe in parallel) -> 4 SMSP x 32 / 8 = 16
+    # butterflies / clk / SM, at the max SM clock.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_bfly_peak = nsm * 4 * 32 * sm_mhz_max * 1e6 / 7.0
+    alu_bfly_peak = nsm * 16 * sm_mhz_max * 1e6
     for k_, (cnt, tot) in prof.items():
         per = tot / cnt
         entry = {"launches": cnt, "avg_ms": round(per, 4), "share": round(tot / ms_total, 3)}
@@ -391,7 +463,8 @@ def run_ours(args, world, rank, local):
             roof = {"bound": "alu", "kernel": fam, "achieved": e["Gbutterfly_per_s"],
                     "peak": round(alu_bfly_peak / 1e9, 1), "unit": "Gbutterfly/s", "frac": e["alu_frac"],
                     "traffic": traffic.get(fam), "algorithmic_bytes": kb[fam][0], "hbm_frac": e["hbm_frac"],
-                    "peak_source": "derived: SMs x 128 int lanes/clk x 1965 MHz / 7 ops per butterfly"}
+                    "peak_source": f"derived: {nsm} SMs x 16 butterflies/clk/SM (fmaheavy pipe: IMAD.HI 4 + "
+                                   f"2 x IMAD 2 cycles per warp) x {sm_mhz_max:.0f} MHz"}
         else:
             roof = {"bound": "hbm", "kernel": fam, "achieved": e["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
                     "frac": e["hbm_frac"], "traffic": traffic.get(fam), "algorithmic_bytes": kb[fam][0],
@@ -439,6 +512,7 @@ def run_ours(args, world, rank, local):
                    "global_batch": B * world, "transform_len": n, "p": P30,
                    "butterflies_per_step_per_gpu": bfly_step,
                    "l2": "inputs 1 GiB + outputs 1 GiB per GPU > 126 MB L2 (no flush needed)",
+                   "output_layout": f"c[{B}][{lc}] at row stride {C3_LDC} words (mm_poly_mul_ld)",
                    "parallelism": f"dp{world} (independent products, no collective)"},
         "e2e": {"value": round(e2e_val, 2), "unit": "Gbutterfly/s",
                 "h2d_bytes_per_step": 2 * B * d * 4, "d2h_bytes_per_step": B * lc * 4,

@@ -135,6 +135,15 @@ mm_status mm_ntt_inverse(const mm_ntt_plan *plan, const void *in, void *out, mm_
  * c must not alias a or b (MM_E_ALIAS).  word_bits/p as for plans. */
 mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, const void *b,
                       size_t lb, void *c, size_t batch, void *stream);
+/* The same product with explicit row strides (leading dimensions, in
+ * elements, BLAS-style): row r of a starts at a + r lda (lda >= la), of b at
+ * b + r ldb, of c at c + r ldc (ldc >= la + lb - 1; elements of a c row beyond
+ * la + lb - 1 are not written).  mm_poly_mul = lda = la, ldb = lb,
+ * ldc = la + lb - 1.  A 128-byte multiple ldc keeps every output row
+ * line-aligned (the packed layout with odd la + lb - 1 splits sectors between
+ * neighbouring column tiles). */
+mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, size_t lda,
+                         const void *b, size_t lb, size_t ldb, void *c, size_t ldc, size_t batch, void *stream);
 
 /* ------------------------------------------------------------------------
  * Integer product (P:971-973 Kronecker segmentation, one
@@ -187,6 +196,12 @@ unsigned long long mm_launch_count(void);
  * a full grid, with no memory traffic.  Returns the kernel time (*ms, CUDA
  * events on `stream`, synchronises) and the butterfly count (*bfly). */
 mm_status mm_probe_butterfly(int word_bits, int iters, double *ms, double *bfly, void *stream);
+/* Instruction-issue probe: 8 independent dependency chains per thread of one
+ * SASS class (kind 0 IMAD, 1 IMAD.HI, 2 IADD3, 3 VIADDMNMX, 4 IMAD.HI + 2
+ * IADD3 interleaved) over a full grid.  Returns the kernel time (*ms) and the
+ * warp instructions of that class executed (*ops); ops / (ms x SMs x clock)
+ * is the per-SM issue rate that prices each instruction of the butterfly. */
+mm_status mm_probe_issue(int kind, int iters, double *ms, double *ops, void *stream);
 void mm_prof_enable(int on);
 int mm_prof_collect(char *buf, size_t len);
 

@@ -48,6 +48,7 @@ EXPORTS = {
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_poly_mul_ld": (_ST, [_i32, _u64, _u64, _P, _sz, _sz, _P, _sz, _sz, _P, _sz, _sz, _P]),
     "mm_int_mul_u16": (_ST, [_P, _sz, _P, _sz, _P, _P]),
     "mm_ntt_fwd_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
@@ -57,6 +58,7 @@ EXPORTS = {
     "mm_ntt_inv_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_launch_count": (ctypes.c_ulonglong, []),
     "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
+    "mm_probe_issue": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_prof_enable": (None, [_i32]),
     "mm_prof_collect": (_i32, [ctypes.c_char_p, _sz]),
 }
@@ -107,6 +109,15 @@ def _ptr(t: torch.Tensor | None):
         raise ValueError("tensors must live on a CUDA device (no CPU fallback)")
     if not t.is_contiguous():
         raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _ptr_rows(t: torch.Tensor):
+    """Pointer of a 2-D row-strided view (unit element stride; rows may be padded)."""
+    if not t.is_cuda:
+        raise ValueError("tensors must live on a CUDA device (no CPU fallback)")
+    if t.dim() != 2 or t.stride(-1) != 1:
+        raise ValueError("expected a 2-D view with unit element stride")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -251,6 +262,14 @@ def probe_butterfly(word_bits: int = 32, iters: int = 2000) -> float:
     return bf.value / (ms.value * 1e-3)
 
 
+def probe_issue(kind: int, iters: int = 2000) -> float:
+    """Warp instructions / s of one SASS class (0 IMAD, 1 IMAD.HI, 2 IADD3,
+    3 VIADDMNMX, 4 IMAD.HI + 2 IADD3) over a full grid."""
+    ms, ops = ctypes.c_double(), ctypes.c_double()
+    _check(lib().mm_probe_issue(kind, iters, ctypes.byref(ms), ctypes.byref(ops), _stream()))
+    return ops.value / (ms.value * 1e-3)
+
+
 def prof_enable(on: bool = True):
     lib().mm_prof_enable(1 if on else 0)
 
@@ -268,20 +287,38 @@ def prof_collect() -> dict:
 
 
 # ------------------------------------------------------------------ products
+def _rows(t: torch.Tensor) -> torch.Tensor:
+    """2-D view [rows, len] with unit element stride (row stride may exceed len)."""
+    t2 = t if t.dim() == 2 else (t.reshape(1, -1) if t.dim() == 1 else t.reshape(-1, t.shape[-1]))
+    if t2.stride(-1) != 1 or (t2.shape[0] > 1 and t2.stride(0) < t2.shape[1]):
+        t2 = t2.contiguous()
+    return t2
+
+
 def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | None = None,
              out: torch.Tensor | None = None) -> torch.Tensor:
-    """Batched product mod p (mm_poly_mul): a [batch, la], b [batch, lb] -> c [batch, la+lb-1]."""
+    """Batched product mod p: a [batch, la], b [batch, lb] -> c [batch, la+lb-1].
+
+    Row-strided 2-D views are passed through as leading dimensions
+    (mm_poly_mul_ld), e.g. out = c_pad[:, :la+lb-1] of a [batch, ldc] tensor."""
     if word_bits is None:
         word_bits = _esz(a) * 8
-    a2 = a.reshape(-1, a.shape[-1]) if a.dim() > 1 else a.reshape(1, -1)
-    b2 = b.reshape(-1, b.shape[-1]) if b.dim() > 1 else b.reshape(1, -1)
+    a2, b2 = _rows(a), _rows(b)
     batch, la = a2.shape
     if b2.shape[0] != batch:
         raise ValueError("batch mismatch")
     lb = b2.shape[1]
+    lc = la + lb - 1
     if out is None:
-        out = torch.empty((batch, la + lb - 1), dtype=a.dtype, device=a.device)
-    _check(lib().mm_poly_mul(word_bits, int(p), int(g), _ptr(a2), la, _ptr(b2), lb, _ptr(out), batch, _stream(a)))
+        out = torch.empty((batch, lc), dtype=a.dtype, device=a.device)
+    o2 = out if out.dim() == 2 else out.reshape(batch, lc)
+    if tuple(o2.shape) != (batch, lc) or o2.stride(-1) != 1 or (batch > 1 and o2.stride(0) < lc):
+        raise ValueError("out must be a [batch, la+lb-1] view with unit element stride")
+    lda = a2.stride(0) if batch > 1 else la
+    ldb = b2.stride(0) if batch > 1 else lb
+    ldc = o2.stride(0) if batch > 1 else lc
+    _check(lib().mm_poly_mul_ld(word_bits, int(p), int(g), _ptr_rows(a2), la, lda, _ptr_rows(b2), lb, ldb,
+                                _ptr_rows(o2), ldc, batch, _stream(a)))
     return out if a.dim() > 1 else out.reshape(-1)
 
 

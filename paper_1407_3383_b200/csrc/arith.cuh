@@ -156,22 +156,41 @@ struct FpG {
     static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
     static constexpr uint64_t EPS = 0xFFFFFFFFull;
 
+    // a + b for any a, b < 2^64: each carry out of 2^64 is worth EPS (2^64 = EPS
+    // mod p), added as -c in the low word (EPS * c = 2^32 c - c); a second carry
+    // leaves s < EPS, so the third fold cannot carry.  Branch-free carry chain.
     __device__ __forceinline__ static uint64_t add(uint64_t a, uint64_t b) {
-        uint64_t s = a + b;
-        if (s < a) {                  // 2^64 = EPS
-            s += EPS;
-            if (s < EPS) s += EPS;
-        }
-        return s;
+        uint32_t s0, s1;
+        asm("{\n\t.reg .u32 c, m;\n\t"
+            "add.cc.u32      %0, %2, %4;\n\t"
+            "addc.cc.u32     %1, %3, %5;\n\t"
+            "addc.u32        c, 0, 0;\n\t"
+            "sub.u32         m, 0, c;\n\t"
+            "add.cc.u32      %0, %0, m;\n\t"
+            "addc.cc.u32     %1, %1, 0;\n\t"
+            "addc.u32        c, 0, 0;\n\t"
+            "sub.u32         m, 0, c;\n\t"
+            "add.cc.u32      %0, %0, m;\n\t"
+            "addc.u32        %1, %1, 0;\n\t}"
+            : "=&r"(s0), "=&r"(s1)
+            : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+        return ((uint64_t)s1 << 32) | s0;
     }
+    // a - b: each borrow is worth -EPS (+p = -EPS mod 2^64); symmetric to add.
     __device__ __forceinline__ static uint64_t sub(uint64_t a, uint64_t b) {
-        uint64_t d = a - b;
-        if (a < b) {                  // + p = - EPS (mod 2^64)
-            uint64_t e = d - EPS;
-            if (d < EPS) e -= EPS;
-            d = e;
-        }
-        return d;
+        uint32_t d0, d1;
+        asm("{\n\t.reg .u32 m;\n\t"
+            "sub.cc.u32      %0, %2, %4;\n\t"
+            "subc.cc.u32     %1, %3, %5;\n\t"
+            "subc.u32        m, 0, 0;\n\t"
+            "sub.cc.u32      %0, %0, m;\n\t"
+            "subc.cc.u32     %1, %1, 0;\n\t"
+            "subc.u32        m, 0, 0;\n\t"
+            "sub.cc.u32      %0, %0, m;\n\t"
+            "subc.u32        %1, %1, 0;\n\t}"
+            : "=&r"(d0), "=&r"(d1)
+            : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+        return ((uint64_t)d1 << 32) | d0;
     }
     // 128-bit product from four 32 x 32 partial products (one mul/mad carry
     // chain: IMAD / IMAD.HI with carry), then with x = r0 + r1 2^32 + r2 2^64

@@ -721,9 +721,9 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
 }
 
 // n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
-static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, const uint32_t* b, long long lb,
-                                uint32_t* c, long long lc, long long batch, uint32_t* WA, uint32_t* WB,
-                                cudaStream_t st) {
+static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, long long lda, const uint32_t* b,
+                                long long lb, long long ldb, uint32_t* c, long long lc, long long ldc, long long batch,
+                                uint32_t* WA, uint32_t* WB, cudaStream_t st) {
     const f32::Fld f{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
     const long long n = 1ll << P->k;
     mm_status s;
@@ -732,7 +732,8 @@ static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la,
         cf.in = op == 0 ? a : b;
         cf.out = op == 0 ? WA : WB;
         cf.nbatch = batch;
-        cf.in_bs = cf.in_len = op == 0 ? la : lb;
+        cf.in_bs = op == 0 ? lda : ldb;
+        cf.in_len = op == 0 ? la : lb;
         cf.out_bs = n;
         cf.lvl = (const uint2*)P->lvl_f2;
         cf.fs = (const uint2*)P->fs_full_f;
@@ -754,7 +755,8 @@ static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la,
     ci.in = WA; ci.out = c;
     ci.nbatch = batch;
     ci.in_bs = n;
-    ci.out_bs = ci.out_len = lc;
+    ci.out_bs = ldc;
+    ci.out_len = lc;
     ci.lvl = (const uint2*)P->lvl_i2;
     ci.tc = P->tw_i2;
     ci.f = f;
@@ -764,7 +766,11 @@ static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la,
 // c = a * b for `batch` rows; TIn = input element type (uint16 limbs for int_mul)
 template <class F, class TIn, class TOut>
 static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const TIn* b, long long lb, TOut* c,
-                              long long lc, long long batch, cudaStream_t st) {
+                              long long lc, long long batch, cudaStream_t st, long long lda = -1, long long ldb = -1,
+                              long long ldc = -1) {
+    if (lda < 0) lda = la;
+    if (ldb < 0) ldb = lb;
+    if (ldc < 0) ldc = lc;
     typedef typename F::T T;
     typedef typename F::W W;
     F f = make_field<F>(P);
@@ -773,7 +779,7 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         PmulArgs<F> m{};
         m.a = a; m.b = b; m.c = c;
         m.nrows = batch;
-        m.a_rs = la; m.b_rs = lb; m.c_rs = lc;
+        m.a_rs = lda; m.b_rs = ldb; m.c_rs = ldc;
         m.la = la; m.lb = lb; m.lc = lc;
         m.k = P->k;
         m.sc = sc;
@@ -789,8 +795,8 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     T* WA = (T*)ws;
     T* WB = WA + n * batch;
     if constexpr (sizeof(T) == 4 && sizeof(TIn) == 4 && sizeof(TOut) == 4) {
-        if (P->fast16) return fast16_product(P, (const uint32_t*)a, la, (const uint32_t*)b, lb, (uint32_t*)c, lc,
-                                             batch, (uint32_t*)WA, (uint32_t*)WB, st);
+        if (P->fast16) return fast16_product(P, (const uint32_t*)a, la, lda, (const uint32_t*)b, lb, ldb, (uint32_t*)c,
+                                             lc, ldc, batch, (uint32_t*)WA, (uint32_t*)WB, st);
     }
     // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb
     for (int op = 0; op < 2; op++) {
@@ -800,7 +806,7 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         cc.ncols = n1;
         cc.nbatch = batch;
         cc.in_rs = n1; cc.out_rs = n1;
-        cc.in_bs = op == 0 ? la : lb; cc.out_bs = n;
+        cc.in_bs = op == 0 ? lda : ldb; cc.out_bs = n;
         cc.in_len = op == 0 ? la : lb; cc.out_len = n;
         cc.n1 = n1;
         cc.k = P->k2;
@@ -834,7 +840,7 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     ci.ncols = n1;
     ci.nbatch = batch;
     ci.in_rs = n1; ci.out_rs = n1;
-    ci.in_bs = n; ci.out_bs = lc;
+    ci.in_bs = n; ci.out_bs = ldc;
     ci.in_len = n; ci.out_len = lc;
     ci.n1 = n1;
     ci.k = P->k2;
@@ -967,14 +973,16 @@ static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
     return x < y + nb && y < x + na;
 }
 
-extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, const void* b,
-                                 size_t lb, void* c, size_t batch, void* stream) {
+extern "C" mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, size_t lda,
+                                    const void* b, size_t lb, size_t ldb, void* c, size_t ldc, size_t batch,
+                                    void* stream) {
     if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
     if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
     size_t lc = la + lb - 1;
+    if (lda < la || ldb < lb || ldc < lc) return set_err(MM_E_ARG, "leading dimension smaller than the row length");
     size_t es = esize(word_bits);
-    if (overlaps(a, la * batch * es, c, lc * batch * es) || overlaps(b, lb * batch * es, c, lc * batch * es))
-        return set_err(MM_E_ALIAS, "c aliases a or b");
+    const size_t ea = ((batch - 1) * lda + la) * es, eb = ((batch - 1) * ldb + lb) * es, ec = ((batch - 1) * ldc + lc) * es;
+    if (overlaps(a, ea, c, ec) || overlaps(b, eb, c, ec)) return set_err(MM_E_ALIAS, "c aliases a or b");
     int k = 0;
     while ((1ull << k) < lc) k++;
     if (k == 0) k = 1;
@@ -986,9 +994,16 @@ extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const vo
     cudaStream_t st = (cudaStream_t)stream;
     if (word_bits == 32)
         return product_impl<Fp32, uint32_t, uint32_t>(P, (const uint32_t*)a, (long long)la, (const uint32_t*)b,
-                                                      (long long)lb, (uint32_t*)c, (long long)lc, (long long)batch, st);
+                                                      (long long)lb, (uint32_t*)c, (long long)lc, (long long)batch, st,
+                                                      (long long)lda, (long long)ldb, (long long)ldc);
     return product_impl<FpG, uint64_t, uint64_t>(P, (const uint64_t*)a, (long long)la, (const uint64_t*)b, (long long)lb,
-                                                 (uint64_t*)c, (long long)lc, (long long)batch, st);
+                                                 (uint64_t*)c, (long long)lc, (long long)batch, st, (long long)lda,
+                                                 (long long)ldb, (long long)ldc);
+}
+
+extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, const void* b,
+                                 size_t lb, void* c, size_t batch, void* stream) {
+    return mm_poly_mul_ld(word_bits, p, g, a, la, la, b, lb, lb, c, la + lb - 1, batch, stream);
 }
 
 extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t* b, size_t nb, uint16_t* c,

@@ -18,6 +18,9 @@
 // min(x + y, x + y - 2p) with the second term opaque to ptxas, so it becomes
 // IADD3 + VIADDMNMX on the ALU pipe and the butterfly is 3 ALU + 3 FMA-pipe
 // instructions (the plain form puts the sum on the FMA pipe as IMAD.IADD).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <string.h>
 #include "common.h"
 #include "arith.cuh"
 #include "fast32.h"
@@ -33,6 +36,9 @@ __device__ __forceinline__ uint32_t add_sub(uint32_t x, uint32_t y, uint32_t c) 
     asm("{ .reg .u32 r; add.u32 r, %1, %2; sub.u32 %0, r, %3; }" : "=r"(t) : "r"(x), "r"(y), "r"(c));
     return t;
 }
+__device__ __forceinline__ uint32_t sub_add(uint32_t x, uint32_t y, uint32_t c) {   // x - y + c = (x + c) - y
+    return add_sub(x, c, y);
+}
 // Function 8 (lazy): x w mod p in [0, 2p) for any x < 2^32
 __device__ __forceinline__ uint32_t mulw(uint32_t x, uint2 w, const Fld& f) {
     uint32_t c = __umulhi(x, w.y);
@@ -40,27 +46,34 @@ __device__ __forceinline__ uint32_t mulw(uint32_t x, uint2 w, const Fld& f) {
 }
 __device__ __forceinline__ void dif(uint32_t& x, uint32_t& y, uint2 w, const Fld& f) {
     uint32_t t = add_sub(x, y, f.p2);
-    uint32_t d = x - y + f.p2;
+    uint32_t d = sub_add(x, y, f.p2);
     x = umin(x + y, t);
     y = mulw(d, w, f);
 }
 __device__ __forceinline__ void dif1(uint32_t& x, uint32_t& y, const Fld& f) {
     uint32_t t = add_sub(x, y, f.p2);
-    uint32_t d = x - y + f.p2;
+    uint32_t d = sub_add(x, y, f.p2);
     x = umin(x + y, t);
     y = umin(d, d - f.p2);
 }
+// DIT with the sum reduced: x' = min(xx + t, xx + t - 2p) in [0, 2p) (IADD3 +
+// VIADDMNMX on the ALU pipe, so ptxas cannot move the add to the FMA pipe as
+// IMAD.IADD), y' = xx - t + 2p in (0, 4p).  XR: x is already in [0, 2p).
+template <bool XR>
 __device__ __forceinline__ void dit(uint32_t& x, uint32_t& y, uint2 w, const Fld& f) {
-    uint32_t xx = umin(x, x - f.p2);
-    uint32_t t = mulw(y, w, f);
-    x = xx + t;
-    y = xx - t + f.p2;
+    const uint32_t xx = XR ? x : umin(x, x - f.p2);
+    const uint32_t t = mulw(y, w, f);
+    const uint32_t s = add_sub(xx, t, f.p2);
+    x = umin(xx + t, s);
+    y = sub_add(xx, t, f.p2);
 }
+template <bool XR>
 __device__ __forceinline__ void dit1(uint32_t& x, uint32_t& y, const Fld& f) {
-    uint32_t xx = umin(x, x - f.p2);
-    uint32_t yy = umin(y, y - f.p2);
-    x = xx + yy;
-    y = xx - yy + f.p2;
+    const uint32_t xx = XR ? x : umin(x, x - f.p2);
+    const uint32_t yy = umin(y, y - f.p2);
+    const uint32_t s = add_sub(xx, yy, f.p2);
+    x = umin(xx + yy, s);
+    y = sub_add(xx, yy, f.p2);
 }
 // Montgomery REDC (Function 13), subtractive form, lazy:
 // x y 2^-32 mod p in (0, 2p) for x y < 2^32 p.
@@ -114,19 +127,27 @@ __device__ __forceinline__ void dit_const(uint32_t* v, const Tw15& T, const Fld&
         for (int t = 0; t < 16; t++) {
             if (t & h) continue;
             const int k = t & (h - 1);
-            if (k == 0) dit1(v[t], v[t + h], f);
-            else dit(v[t], v[t + h], T.w[h + k], f);
+            const bool xr = h == 1 || (t & (h >> 1)) == 0;
+            if (k == 0) {
+                if (xr) dit1<true>(v[t], v[t + h], f); else dit1<false>(v[t], v[t + h], f);
+            } else {
+                if (xr) dit<true>(v[t], v[t + h], T.w[h + k], f); else dit<false>(v[t], v[t + h], T.w[h + k], f);
+            }
         }
     }
 }
-// DIT, elements lo + 16 t: half-spans 16, 32, 64, 128
+// DIT, elements lo + 16 t: half-spans 16, 32, 64, 128.  XR0: every input in [0, 2p).
+template <bool XR0>
 __device__ __forceinline__ void dit_tab(uint32_t* v, int lo, const uint2* tw, const Fld& f) {
 #pragma unroll
     for (int h = 1; h <= 8; h <<= 1) {
 #pragma unroll
         for (int t = 0; t < 16; t++) {
             if (t & h) continue;
-            dit(v[t], v[t + h], tw[16 * h + lo + 16 * (t & (h - 1))], f);
+            const uint2 w = tw[16 * h + lo + 16 * (t & (h - 1))];
+            // level h = 1 of this group takes the previous group's outputs: x' at t with bit 3 clear
+            const bool xr = h == 1 ? XR0 : (t & (h >> 1)) == 0;
+            if (xr) dit<true>(v[t], v[t + h], w, f); else dit<false>(v[t], v[t + h], w, f);
         }
     }
 }
@@ -148,6 +169,34 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_by
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// TMA (cp.async.bulk.tensor): one elected thread moves a whole 32-column tile
+// (3-D tensor map {256 columns, rows per batch row, batch}, box {32, R, 1},
+// rows beyond the tensor zero-filled) and arms an mbarrier with its byte
+// count; every thread waits on the barrier's phase parity.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "LAB_WAIT:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@P1 bra DONE;\n\t"
+                 "bra LAB_WAIT;\n"
+                 "DONE:\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// issued by one thread: generic-proxy reads of dst must be ordered before the async write
+__device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
+                                              unsigned bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"((const void*)tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 
 // rows [0, RIN) of the 32-column block `tile` -> st[row * 32 + c]; element
 // (row, col) of batch row b is in[b * in_bs + row * 256 + col], valid iff
@@ -182,26 +231,41 @@ __device__ __forceinline__ void issue_cols(uint32_t* st, const uint32_t* in, lon
 
 template <bool HALF> struct ColFwdSmem {
     static constexpr int RIN = HALF ? 128 : 256;
-    static constexpr size_t bytes = 256 * sizeof(uint2) + (RIN + 256) * 32 * sizeof(uint32_t);
+    static constexpr size_t bytes = 256 * sizeof(uint2) + (RIN + 256) * 32 * sizeof(uint32_t) + 128;
 };
 
-template <bool HALF, bool MASK, bool VEC>
-__global__ void __launch_bounds__(NT, HALF ? 4 : 3) k_col_fwd(ColFwdArgs a) {
+// TMA: tensor-map load of the staging tile (in_len a multiple of 256), else
+// cp.async with per-element zero fill (MASK, VEC as issue_cols).
+template <bool HALF, bool MASK, bool VEC, bool TMA>
+__global__ void __launch_bounds__(NT, HALF ? 4 : 3) k_col_fwd(const __grid_constant__ CUtensorMap tm, ColFwdArgs a) {
     constexpr int RIN = ColFwdSmem<HALF>::RIN;
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint2* tws = (uint2*)smem;
-    uint32_t* st = (uint32_t*)(tws + 256);     // staging: next tile's input rows
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t* st = (uint32_t*)smem;            // staging: next tile's input rows (TMA destination)
     uint32_t* s = st + RIN * 32;               // working tile
+    uint2* tws = (uint2*)(s + 256 * 32);
+    __shared__ uint64_t bar;
     for (int i = threadIdx.x; i < 256; i += NT) tws[i] = a.lvl[i];
     const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long ntiles = a.nbatch * 8;
     const Fld f = a.f;
-    if ((long long)blockIdx.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, blockIdx.x, a.in_bs, a.in_len);
-    cp_commit();
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && (long long)blockIdx.x < ntiles)
+            tma_load_tile(st, &tm, (int)(blockIdx.x & 7) * 32, 0, (int)(blockIdx.x >> 3), &bar, RIN * 128);
+    } else {
+        if ((long long)blockIdx.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, blockIdx.x, a.in_bs, a.in_len);
+        cp_commit();
+    }
+    unsigned it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const long long b = tile >> 3;
         const int col = ((int)(tile & 7) << 5) + c;
-        cp_wait_all();
+        if (TMA) mbar_wait(&bar, it & 1);
+        else cp_wait_all();
         __syncthreads();
         uint32_t v[2][16];
 #pragma unroll
@@ -209,8 +273,13 @@ __global__ void __launch_bounds__(NT, HALF ? 4 : 3) k_col_fwd(ColFwdArgs a) {
 #pragma unroll
             for (int t = 0; t < 16; t++) v[u][t] = (HALF && t >= 8) ? 0u : st[(w + 8 * u + 16 * t) * 32 + c];
         __syncthreads();
-        if (tile + gridDim.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, tile + gridDim.x, a.in_bs, a.in_len);
-        cp_commit();
+        if (TMA) {
+            const long long nt = tile + gridDim.x;
+            if (threadIdx.x == 0 && nt < ntiles) tma_load_tile(st, &tm, (int)(nt & 7) * 32, 0, (int)(nt >> 3), &bar, RIN * 128);
+        } else {
+            if (tile + gridDim.x < ntiles) issue_cols<RIN, MASK, VEC>(st, a.in, tile + gridDim.x, a.in_bs, a.in_len);
+            cp_commit();
+        }
         dif_tab<1>(&v[0], w, tws, f, HALF);
         dif_tab<1>(&v[1], w + 8, tws, f, HALF);
 #pragma unroll
@@ -235,29 +304,38 @@ __global__ void __launch_bounds__(NT, HALF ? 4 : 3) k_col_fwd(ColFwdArgs a) {
     }
 }
 
-constexpr size_t COL_INV_SMEM = 256 * sizeof(uint2) + 2 * 256 * 32 * sizeof(uint32_t);
+constexpr size_t COL_INV_SMEM = 256 * sizeof(uint2) + 2 * 256 * 32 * sizeof(uint32_t) + 128;
 
+// input tiles by TMA into two alternating buffers (one mbarrier each)
 template <bool MASK>
-__global__ void __launch_bounds__(NT, 3) k_col_inv(ColInvArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint2* tws = (uint2*)smem;
-    uint32_t* buf = (uint32_t*)(tws + 256);    // two 256 x 32 tiles
+__global__ void __launch_bounds__(NT, 3) k_col_inv(const __grid_constant__ CUtensorMap tm, ColInvArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t* buf = (uint32_t*)smem;           // two 256 x 32 tiles
+    uint2* tws = (uint2*)(buf + 2 * 256 * 32);
+    __shared__ uint64_t bar[2];
     for (int i = threadIdx.x; i < 256; i += NT) tws[i] = a.lvl[i];
     const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long ntiles = a.nbatch * 8;
     const Fld f = a.f;
-    if ((long long)blockIdx.x < ntiles) issue_cols<256, false, true>(buf, a.in, blockIdx.x, a.in_bs, 1 << 16);
-    cp_commit();
-    int it = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (long long)blockIdx.x < ntiles)
+        tma_load_tile(buf, &tm, (int)(blockIdx.x & 7) * 32, 0, (int)(blockIdx.x >> 3), &bar[0], 256 * 128);
+    unsigned it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
         const long long b = tile >> 3;
         const int col = ((int)(tile & 7) << 5) + c;
         uint32_t* s = buf + (it & 1) * 256 * 32;
-        cp_wait_all();
+        mbar_wait(&bar[it & 1], (it >> 1) & 1);
         __syncthreads();
-        if (tile + gridDim.x < ntiles)
-            issue_cols<256, false, true>(buf + ((it + 1) & 1) * 256 * 32, a.in, tile + gridDim.x, a.in_bs, 1 << 16);
-        cp_commit();
+        const long long nt = tile + gridDim.x;
+        if (threadIdx.x == 0 && nt < ntiles)
+            tma_load_tile(buf + ((it + 1) & 1) * 256 * 32, &tm, (int)(nt & 7) * 32, 0, (int)(nt >> 3), &bar[(it + 1) & 1],
+                          256 * 128);
         uint32_t v[2][16];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
@@ -276,7 +354,9 @@ __global__ void __launch_bounds__(NT, 3) k_col_inv(ColInvArgs a) {
             const int lo = w + 8 * u;
 #pragma unroll
             for (int t = 0; t < 16; t++) v[u][t] = s[(lo + 16 * t) * 32 + c];
-            dit_tab(v[u], lo, tws, f);
+            // phase A left x' (in [0, 2p)) at chunk positions < 8, i.e. rows with lo < 8
+            if (u == 0) dit_tab<true>(v[u], lo, tws, f);
+            else dit_tab<false>(v[u], lo, tws, f);
 #pragma unroll
             for (int t = 0; t < 16; t++) {
                 const int row = lo + 16 * t;
@@ -346,7 +426,7 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < 16; t++) v[0][t] = sa[r * ROWP + pad_word(lo + 16 * t)];
-        dit_tab(v[0], lo, twi, f);
+        dit_tab<false>(v[0], lo, twi, f);
         // inverse step 2 (w^-(j1 [i2]_8)) with n^-1 2^32 folded in
         const uint2* fsr = a.fsi + (row & 255) * 256 + lo;
         uint32_t* dst = a.C + row * 256 + lo;
@@ -365,14 +445,48 @@ template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
     return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
 }
 
-template <bool HALF, bool MASK, bool VEC>
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }();
+    return fn;
+}
+// 3-D map of 32-bit words {256 columns, rows per batch row, batch}, box {32, box_rows, 1}
+static mm_status make_col_map(CUtensorMap* tm, const void* base, long long rows, long long batch, long long bstride_words,
+                              int box_rows) {
+    auto enc = tma_encoder();
+    if (!enc) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled is not available");
+    cuuint64_t dims[3] = {256, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {1024, (cuuint64_t)bstride_words * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return MM_OK;
+}
+
+template <bool HALF, bool MASK, bool VEC, bool TMA>
 static mm_status col_fwd_k(const ColFwdArgs& a, cudaStream_t st) {
-    auto kern = k_col_fwd<HALF, MASK, VEC>;
+    auto kern = k_col_fwd<HALF, MASK, VEC, TMA>;
     const size_t smem = ColFwdSmem<HALF>::bytes;
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    if (TMA) {
+        mm_status s = make_col_map(&tm, a.in, a.in_len / 256, a.nbatch, a.in_bs, ColFwdSmem<HALF>::RIN);
+        if (s != MM_OK) return s;
+    }
     MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
         LaunchScope ls("ntt_cols_fwd", st);
-        kern<<<grid_of(kern, a.nbatch * 8, smem), NT, smem, st>>>(a);
+        kern<<<grid_of(kern, a.nbatch * 8, smem), NT, smem, st>>>(tm, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
@@ -381,12 +495,15 @@ mm_status launch_col_fwd(const ColFwdArgs& a, cudaStream_t st) {
     const bool half = a.in_len <= (1 << 15);
     const bool mask = a.in_len != (half ? (1 << 15) : (1 << 16));
     const bool vec = a.in_bs % 4 == 0 && ((uintptr_t)a.in & 15) == 0;
+    // whole 256-element rows at 16-byte aligned strides: the tensor-map load
+    const bool tma = vec && a.in_len % 256 == 0 && tma_encoder() != nullptr;
+    if (tma) return half ? col_fwd_k<true, false, true, true>(a, st) : col_fwd_k<false, false, true, true>(a, st);
     if (half) {
-        if (!mask) return vec ? col_fwd_k<true, false, true>(a, st) : col_fwd_k<true, false, false>(a, st);
-        return vec ? col_fwd_k<true, true, true>(a, st) : col_fwd_k<true, true, false>(a, st);
+        if (!mask) return vec ? col_fwd_k<true, false, true, false>(a, st) : col_fwd_k<true, false, false, false>(a, st);
+        return vec ? col_fwd_k<true, true, true, false>(a, st) : col_fwd_k<true, true, false, false>(a, st);
     }
-    if (!mask) return vec ? col_fwd_k<false, false, true>(a, st) : col_fwd_k<false, false, false>(a, st);
-    return vec ? col_fwd_k<false, true, true>(a, st) : col_fwd_k<false, true, false>(a, st);
+    if (!mask) return vec ? col_fwd_k<false, false, true, false>(a, st) : col_fwd_k<false, false, false, false>(a, st);
+    return vec ? col_fwd_k<false, true, true, false>(a, st) : col_fwd_k<false, true, false, false>(a, st);
 }
 mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st) {
     if (a.nrows % 16) return set_err(MM_E_UNSUPPORTED_SIZE, "row count %lld is not a multiple of 16", a.nrows);
@@ -400,10 +517,13 @@ mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st) {
 mm_status launch_col_inv(const ColInvArgs& a, cudaStream_t st) {
     if (a.in_bs % 4 || ((uintptr_t)a.in & 15)) return set_err(MM_E_ARG, "inverse column pass needs 16-byte aligned rows");
     auto kern = a.out_len == (1 << 16) ? k_col_inv<false> : k_col_inv<true>;
+    CUtensorMap tm;
+    mm_status s = make_col_map(&tm, a.in, 256, a.nbatch, a.in_bs, 256);
+    if (s != MM_OK) return s;
     MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)COL_INV_SMEM));
     {
         LaunchScope ls("ntt_cols_inv", st);
-        kern<<<grid_of(kern, a.nbatch * 8, COL_INV_SMEM), NT, COL_INV_SMEM, st>>>(a);
+        kern<<<grid_of(kern, a.nbatch * 8, COL_INV_SMEM), NT, COL_INV_SMEM, st>>>(tm, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;

@@ -60,9 +60,79 @@ __global__ void __launch_bounds__(256) k_probe_bfly64(int iters, uint64_t* sink)
     if (acc == 0x12345678ull) sink[0] = acc;
 }
 
+// Single-instruction issue probes: 8 independent dependency chains per
+// thread of one SASS instruction class (inline PTX so ptxas keeps the form):
+//   kind 0: mul.lo.u32 -> IMAD       kind 1: mul.hi.u32 -> IMAD.HI
+//   kind 2: 3-input add -> IADD3     kind 3: min(a + b, c) -> VIADDMNMX
+//   kind 4: IMAD.HI + 2 IADD3 interleaved (pipe overlap)
+template <int KIND>
+__global__ void __launch_bounds__(256) k_probe_issue(uint32_t seed, int iters, uint32_t* sink) {
+    uint32_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = seed * (threadIdx.x + 1) + i * 0x9E3779B9u;
+    const uint32_t k = seed | 1u, c = seed ^ 0x5bd1e995u;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                if (KIND == 0) asm volatile("mul.lo.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(k));
+                if (KIND == 1) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(k));
+                if (KIND == 2) asm volatile("{.reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(x[i]) : "r"(k), "r"(c));
+                if (KIND == 3) asm volatile("{.reg .u32 t; add.u32 t, %0, %1; min.u32 %0, t, %2;}" : "+r"(x[i]) : "r"(k), "r"(c));
+                if (KIND == 4) {
+                    asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(k));
+                    asm volatile("{.reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(x[i]) : "r"(k), "r"(c));
+                    asm volatile("{.reg .u32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(x[i]) : "r"(c), "r"(k));
+                }
+            }
+        }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc ^= x[i];
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
 }  // namespace mm
 
 using namespace mm;
+
+// Runs instruction probe `kind` once; *ms = kernel time, *ops = warp
+// instructions of the probed class executed (per SM per clock = ops /
+// (ms 1e-3 x SMs x clock)).
+extern "C" mm_status mm_probe_issue(int kind, int iters, double* ms, double* ops, void* stream) {
+    if (!ms || !ops || iters <= 0 || kind < 0 || kind > 4) return set_err(MM_E_ARG, "bad probe arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int blocks = num_sms() * 8, threads = 256;
+    void* sink = nullptr;
+    MM_CUDA_TRY(cudaMalloc(&sink, 16));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    {
+        LaunchScope ls("probe_issue", st);
+        switch (kind) {
+            case 0: k_probe_issue<0><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            case 1: k_probe_issue<1><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            case 2: k_probe_issue<2><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            case 3: k_probe_issue<3><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            default: k_probe_issue<4><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+        }
+    }
+    cudaEventRecord(b, st);
+    cudaError_t e = cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return set_err(MM_E_CUDA, "probe failed: %s", cudaGetErrorString(e));
+    *ms = t;
+    *ops = (double)blocks * (threads / 32) * iters * 64.0 * (kind == 4 ? 3.0 : 1.0);
+    return MM_OK;
+}
 
 // Runs the probe once on `stream` and returns the kernel time in ms through
 // *ms (events on the launching stream) and the butterfly count through *bfly.

@@ -258,6 +258,18 @@ def test_poly_mul_fast16_shapes(mm, O, p, g):
         c = u64(host(mm.poly_mul(dev(a), dev(b), p, g)))
         for r in range(batch):
             assert np.array_equal(c[r], O.poly_mul_ntt(a[r], b[r], p, g)), (la, lb, r)
+    # leading dimensions: strided a / b rows and a padded output (mm_poly_mul_ld)
+    for la, lb, lda, ldb, ldc in [(1 << 15, 1 << 15, (1 << 15) + 4, 1 << 16, 1 << 16), (3000, 5000, 3001, 5003, 8000),
+                                  (30001, 20000, 30008, 20000, 50016)]:
+        batch = 3
+        A = residues(la + 7, 1, batch * lda, p).reshape(batch, lda)
+        B = residues(lb + 7, 2, batch * ldb, p).reshape(batch, ldb)
+        Cp = torch.full((batch, ldc), 0xDEADBEEF, dtype=torch.uint32, device=DEV)
+        mm.poly_mul(dev(A)[:, :la], dev(B)[:, :lb], p, g, out=Cp[:, :la + lb - 1])
+        ch = host(Cp)
+        for r in range(batch):
+            assert np.array_equal(u64(ch[r, :la + lb - 1]), O.poly_mul_ntt(A[r, :la], B[r, :lb], p, g)), (la, lb, r)
+            assert (ch[r, la + lb - 1:] == 0xDEADBEEF).all(), "wrote beyond the row"
     # extreme residues: all p-1 (every lazy range at its maximum)
     a = np.full((2, 1 << 15), p - 1, dtype=np.uint32)
     c = u64(host(mm.poly_mul(dev(a), dev(a), p, g)))
