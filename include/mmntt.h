@@ -142,6 +142,16 @@ mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const void *a, size
  * ldc = la + lb - 1.  A 128-byte multiple ldc keeps every output row
  * line-aligned (the packed layout with odd la + lb - 1 splits sectors between
  * neighbouring column tiles). */
+/* The same product with HOST operands and result (a: [batch][la], b:
+ * [batch][lb], c: [batch][la+lb-1], packed, page-locked memory for overlap):
+ * the batch is cut into chunks that upload (own stream), multiply (the
+ * caller's `stream`) and download (own stream) as a three-slot pipeline, so
+ * the PCIe copies in both directions overlap the kernels.  Asynchronous with
+ * respect to the host: `stream` is ordered after the last download (callers
+ * synchronise it before reading c).  Device memory (3 chunk slots) is owned by
+ * the library and reused. */
+mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, const void *b,
+                           size_t lb, void *c, size_t batch, void *stream);
 mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, size_t lda,
                          const void *b, size_t lb, size_t ldb, void *c, size_t ldc, size_t batch, void *stream);
 

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "int_mul_u16", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_mul_host", "int_mul_u16", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -48,6 +48,7 @@ EXPORTS = {
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_poly_mul_host": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_mul_ld": (_ST, [_i32, _u64, _u64, _P, _sz, _sz, _P, _sz, _sz, _P, _sz, _sz, _P]),
     "mm_int_mul_u16": (_ST, [_P, _sz, _P, _sz, _P, _P]),
     "mm_ntt_fwd_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
@@ -320,6 +321,31 @@ def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | 
     _check(lib().mm_poly_mul_ld(word_bits, int(p), int(g), _ptr_rows(a2), la, lda, _ptr_rows(b2), lb, ldb,
                                 _ptr_rows(o2), ldc, batch, _stream(a)))
     return out if a.dim() > 1 else out.reshape(-1)
+
+
+def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.Tensor | None = None,
+                  word_bits: int | None = None) -> torch.Tensor:
+    """poly_mul on HOST tensors (pinned for overlap): mm_poly_mul_host pipelines
+    chunked uploads, kernels and downloads; returns after the result is in
+    `out` (synchronises the current stream)."""
+    if a.is_cuda or b.is_cuda:
+        raise ValueError("poly_mul_host takes host tensors")
+    if word_bits is None:
+        word_bits = _esz(a) * 8
+    a2 = a.reshape(-1, a.shape[-1]).contiguous()
+    b2 = b.reshape(-1, b.shape[-1]).contiguous()
+    batch, la = a2.shape
+    lb = b2.shape[1]
+    if out is None:
+        out = torch.empty((batch, la + lb - 1), dtype=a.dtype, pin_memory=True)
+    if out.is_cuda or not out.is_contiguous() or out.numel() != batch * (la + lb - 1):
+        raise ValueError("out must be a contiguous host tensor of batch x (la + lb - 1)")
+    st = torch.cuda.current_stream()
+    _check(lib().mm_poly_mul_host(word_bits, int(p), int(g), ctypes.c_void_p(a2.data_ptr()), la,
+                                  ctypes.c_void_p(b2.data_ptr()), lb, ctypes.c_void_p(out.data_ptr()), batch,
+                                  ctypes.c_void_p(st.cuda_stream)))
+    st.synchronize()
+    return out
 
 
 def int_mul_u16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -1006,6 +1006,97 @@ extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const vo
     return mm_poly_mul_ld(word_bits, p, g, a, la, la, b, lb, lb, c, la + lb - 1, batch, stream);
 }
 
+// ---- host-buffer product: chunked H2D / compute / D2H pipeline -------------------
+// Three device slots; H2D and D2H on their own streams, the products on the
+// caller's stream, events between them, so chunk i+1 uploads and chunk i-1
+// downloads while chunk i computes.  Device output rows use a 128-byte
+// leading dimension; the D2H copy packs them (cudaMemcpy2DAsync).
+struct HostPipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t in[3], done[3], freed[3];
+    bool used[3] = {false, false, false};
+    void* buf = nullptr;
+    size_t bytes = 0;
+    std::mutex mu;
+};
+static std::mutex g_pipe_mu;
+static std::map<int, HostPipe*> g_pipes;
+
+static mm_status host_pipe(HostPipe** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_pipe_mu);
+    HostPipe*& P = g_pipes[dev];
+    if (!P) {
+        HostPipe* h = new (std::nothrow) HostPipe;
+        if (!h) return set_err(MM_E_ARG, "out of host memory");
+        MM_CUDA_TRY(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+        MM_CUDA_TRY(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 3; i++) {
+            MM_CUDA_TRY(cudaEventCreateWithFlags(&h->in[i], cudaEventDisableTiming));
+            MM_CUDA_TRY(cudaEventCreateWithFlags(&h->done[i], cudaEventDisableTiming));
+            MM_CUDA_TRY(cudaEventCreateWithFlags(&h->freed[i], cudaEventDisableTiming));
+        }
+        P = h;
+    }
+    *out = P;
+    return MM_OK;
+}
+
+extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, const void* b,
+                                      size_t lb, void* c, size_t batch, void* stream) {
+    if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
+    if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
+    if (word_bits != 32 && word_bits != 64) return set_err(MM_E_ARG, "word_bits must be 32 or 64");
+    const size_t es = esize(word_bits), lc = la + lb - 1;
+    const size_t q = 128 / es, ldc = (lc + q - 1) / q * q;
+    const size_t per = (la + lb + ldc) * es;
+    size_t ch = ((size_t)96 << 20) / per;               // ~96 MiB of device traffic per chunk
+    if (ch < 1) ch = 1;
+    if (ch > batch) ch = batch;
+    HostPipe* H = nullptr;
+    mm_status s = host_pipe(&H);
+    if (s != MM_OK) return s;
+    std::lock_guard<std::mutex> lk(H->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t slot_bytes = ch * per;
+    if (H->bytes < 3 * slot_bytes) {
+        MM_CUDA_TRY(cudaDeviceSynchronize());
+        if (H->buf) cudaFree(H->buf);
+        H->buf = nullptr;
+        H->bytes = 0;
+        MM_CUDA_TRY(cudaMalloc(&H->buf, 3 * slot_bytes));
+        H->bytes = 3 * slot_bytes;
+        for (int i = 0; i < 3; i++) H->used[i] = false;
+    }
+    const size_t nch = (batch + ch - 1) / ch;
+    int last = 0;
+    for (size_t i = 0; i < nch; i++) {
+        const int k = (int)(i % 3);
+        const size_t r0 = i * ch, rows = batch - r0 < ch ? batch - r0 : ch;
+        char* base = (char*)H->buf + k * slot_bytes;
+        char* da = base;
+        char* db = da + ch * la * es;
+        char* dc = db + ch * lb * es;
+        if (H->used[k]) MM_CUDA_TRY(cudaStreamWaitEvent(H->h2d, H->freed[k], 0));
+        MM_CUDA_TRY(cudaMemcpyAsync(da, (const char*)a + r0 * la * es, rows * la * es, cudaMemcpyHostToDevice, H->h2d));
+        MM_CUDA_TRY(cudaMemcpyAsync(db, (const char*)b + r0 * lb * es, rows * lb * es, cudaMemcpyHostToDevice, H->h2d));
+        MM_CUDA_TRY(cudaEventRecord(H->in[k], H->h2d));
+        MM_CUDA_TRY(cudaStreamWaitEvent(st, H->in[k], 0));
+        if ((s = mm_poly_mul_ld(word_bits, p, g, da, la, la, db, lb, lb, dc, ldc, rows, stream)) != MM_OK) return s;
+        MM_CUDA_TRY(cudaEventRecord(H->done[k], st));
+        MM_CUDA_TRY(cudaStreamWaitEvent(H->d2h, H->done[k], 0));
+        MM_CUDA_TRY(cudaMemcpy2DAsync((char*)c + r0 * lc * es, lc * es, dc, ldc * es, lc * es, rows,
+                                      cudaMemcpyDeviceToHost, H->d2h));
+        MM_CUDA_TRY(cudaEventRecord(H->freed[k], H->d2h));
+        H->used[k] = true;
+        last = k;
+    }
+    // the caller's stream is ordered after the last download
+    MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
+    return MM_OK;
+}
+
 extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t* b, size_t nb, uint16_t* c,
                                     void* stream) {
     if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");

@@ -277,6 +277,24 @@ def test_poly_mul_fast16_shapes(mm, O, p, g):
         assert np.array_equal(c[r], O.poly_mul_ntt(a[r], a[r], p, g))
 
 
+def test_poly_mul_host_pipeline(mm, O):
+    # host operands, several pipeline chunks (~192 products each) + a ragged last chunk
+    p, g, B, d = P30, 3, 500, 1 << 15
+    a = torch.from_numpy(residues(11, 1, B * d, p).reshape(B, d)).pin_memory()
+    b = torch.from_numpy(residues(11, 2, B * d, p).reshape(B, d)).pin_memory()
+    c = mm.poly_mul_host(a, b, p, g)
+    cd = mm.poly_mul(a.to(DEV), b.to(DEV), p, g).cpu()
+    assert torch.equal(c, cd)
+    for r in (0, 191, 192, 499):
+        assert np.array_equal(u64(c[r].numpy()), O.poly_mul_ntt(a[r].numpy(), b[r].numpy(), p, g)), r
+    # small and 64-bit: a single chunk
+    a = residues(12, 1, 3 * 700, PG).reshape(3, 700)
+    b = residues(12, 2, 3 * 300, PG).reshape(3, 300)
+    c = mm.poly_mul_host(torch.from_numpy(a), torch.from_numpy(b), PG, 7)
+    for r in range(3):
+        assert np.array_equal(u64(c[r].numpy()), O.poly_mul_schoolbook(a[r], b[r], PG)), r
+
+
 def test_poly_mul_c3_small_batch(mm, O):
     p, g = P30, 3
     B, d = 8, 1 << 15
