@@ -383,6 +383,19 @@ def extras_run(mm, torch, dev, peaks):
     ms = tloop(lambda: mm.int_mul_u16(ia, ib, out=ic), 10)
     out["C5_int_mul_2^28bit"] = {"ms": round(ms, 3), "Mbit_per_s": round(2 * (1 << 28) / (ms * 1e-3) / 1e6, 1),
                                  "Gbutterfly_per_s": round(3 * (1 << 24) * 25 / (ms * 1e-3) / 1e9, 1)}
+    # the paper's three-prime integer product at
+    # Table 16's largest size, 32 x 2^20-bit operands, beside the Goldilocks path
+    n32 = 1 << 20
+    ja = gen.limbs16_torch(gen.config_seed(5), 3, 2 * n32, dev).view(torch.uint32)
+    jb = gen.limbs16_torch(gen.config_seed(5), 4, 2 * n32, dev).view(torch.uint32)
+    jc = torch.empty(2 * n32, dtype=torch.uint32, device=dev)
+    ms3 = tloop(lambda: mm.int_mul_u32(ja, jb, out=jc), 10)
+    jc16 = torch.empty(4 * n32, dtype=torch.uint16, device=dev)
+    ms1 = tloop(lambda: mm.int_mul_u16(ja.view(torch.uint16), jb.view(torch.uint16), out=jc16), 10)
+    out["int_mul_32x2^20bit"] = {
+        "three_prime_ms": round(ms3, 4), "three_prime_Mbit_per_s": round(2 * 32 * n32 / (ms3 * 1e-3) / 1e6, 1),
+        "goldilocks_ms": round(ms1, 4), "goldilocks_Mbit_per_s": round(2 * 32 * n32 / (ms1 * 1e-3) / 1e6, 1),
+        "note": "Table 16 size (paper: 200 ms MATHEMAGIX / 240 ms GMP on one i7-4770 core, context only)"}
     return out
 
 

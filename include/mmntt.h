@@ -165,6 +165,18 @@ mm_status mm_int_mul_u16(const uint16_t *a, size_t na, const uint16_t *b, size_t
                          void *stream);
 
 /* ------------------------------------------------------------------------
+ * Integer product by the paper's three-prime FFT (SURVEY §8(f)
+ * item 1): a (na limbs) and b (nb limbs) are little-endian 32-bit limbs,
+ * i.e. Kronecker segmentation with h = 32 (A(2^32) = a).  The three 32-bit
+ * NTT products run mod p1 = 998244353, p2 = 985661441, p3 = 943718401
+ * (generators 3, 3, 7), the coefficients (< min(na,nb) 2^64 < 2^85 <
+ * p1 p2 p3) are rebuilt by Garner's CRT as 96-bit words and carried into c,
+ * exactly na + nb limbs.  Transform length <= 2^22 (the 2-adicity of p2, p3),
+ * so na + nb - 1 <= 2^22 (MM_E_SIZE_OVERFLOW otherwise).  Device pointers,
+ * c must not alias a or b; the library owns its workspace (per stream). */
+mm_status mm_int_mul_u32(const uint32_t *a, size_t na, const uint32_t *b, size_t nb, uint32_t *c, void *stream);
+
+/* ------------------------------------------------------------------------
  * Four-step building blocks for the distributed transform (SURVEY a6/a7,
  * Algorithm 1 split across ranks).  The full transform of length n = n2 n1
  * (the plan's n) is viewed as n2 rows x n1 columns, a[j2 n1 + j1].

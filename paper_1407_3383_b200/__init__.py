@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_mul_host", "int_mul_u16", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -48,6 +48,7 @@ EXPORTS = {
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_int_mul_u32": (_ST, [_P, _sz, _P, _sz, _P, _P]),
     "mm_poly_mul_host": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_mul_ld": (_ST, [_i32, _u64, _u64, _P, _sz, _sz, _P, _sz, _sz, _P, _sz, _sz, _P]),
     "mm_int_mul_u16": (_ST, [_P, _sz, _P, _sz, _P, _P]),
@@ -345,6 +346,17 @@ def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.T
                                   ctypes.c_void_p(b2.data_ptr()), lb, ctypes.c_void_p(out.data_ptr()), batch,
                                   ctypes.c_void_p(st.cuda_stream)))
     st.synchronize()
+    return out
+
+
+def int_mul_u32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Exact product of little-endian 32-bit limb arrays by the paper's three-prime
+    FFT (mm_int_mul_u32); na + nb limbs."""
+    if a.element_size() != 4 or b.element_size() != 4:
+        raise ValueError("32-bit limbs expected")
+    if out is None:
+        out = torch.empty(a.numel() + b.numel(), dtype=a.dtype, device=a.device)
+    _check(lib().mm_int_mul_u32(_ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(out), _stream(a)))
     return out
 
 

@@ -104,24 +104,54 @@ __global__ void k_fs_table_scaled32(uint2* t, int k1, int k2, uint32_t w, uint32
 }
 
 // ---------------------------------------------------------------- carries (int_mul)
-// coefficient c_k < 2^56 (exact integer) -> 16-bit digits; s_j = sum_t digit_t(c_{j-t}) < 2^18.
-// u_j = (s_j mod 2^16) + (s_{j-1} >> 16)  < 2^16 + 4; w_j = u_j mod 2^16, g_j = u_j >> 16 in {0,1};
-// carry chain: C_{j+1} = g_j | (w_j == 0xFFFF & C_j); out_j = (w_j + C_j) mod 2^16.
-__device__ __forceinline__ uint32_t s_at(const uint64_t* __restrict__ c, long long j, long long nc) {
-    uint32_t s = 0;
+// The product coefficients c_k (exact integers) are evaluated at 2^W (P:973,
+// "A(2^h) = a") digit by digit: s_j = sum_t digit_t(c_{j-t}) (T digits of W
+// bits per coefficient); u_j = (s_j mod 2^W) + (s_{j-1} >> W) < 2^W + T;
+// w_j = u_j mod 2^W, g_j = u_j >> W in {0,1}; carry chain
+// C_{j+1} = g_j | (w_j == 2^W - 1 & C_j); out_j = (w_j + C_j) mod 2^W.
+// Dig16: Goldilocks path, c_k < 2^56 in a u64, 16-bit limbs (T = 4).
+// Dig32x3: three-prime path, c_k < 2^86 as three 32-bit words, 32-bit limbs (T = 3).
+struct Dig16 {
+    typedef uint16_t Out;
+    enum { W = 16 };
+    const uint64_t* c;
+    long long nc;
+    __device__ __forceinline__ uint64_t s_at(long long j) const {
+        uint64_t s = 0;
 #pragma unroll
-    for (int t = 0; t < 4; t++) {
-        long long k = j - t;
-        if (k >= 0 && k < nc) s += (uint32_t)((c[k] >> (16 * t)) & 0xFFFF);
+        for (int t = 0; t < 4; t++) {
+            long long k = j - t;
+            if (k >= 0 && k < nc) s += (c[k] >> (16 * t)) & 0xFFFF;
+        }
+        return s;
     }
-    return s;
+};
+struct Dig32x3 {
+    typedef uint32_t Out;
+    enum { W = 32 };
+    const uint32_t* w;   // coefficient k at w[3k], w[3k+1], w[3k+2] (little-endian words)
+    long long nc;
+    __device__ __forceinline__ uint64_t s_at(long long j) const {
+        uint64_t s = 0;
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            long long k = j - t;
+            if (k >= 0 && k < nc) s += w[3 * k + t];
+        }
+        return s;
+    }
+};
+template <class D>
+__device__ __forceinline__ void carry_gp(const D& d, long long j, uint32_t& w, uint32_t& g) {
+    constexpr uint64_t M = (D::W == 32) ? 0xFFFFFFFFull : ((1ull << D::W) - 1);
+    const uint64_t sj = d.s_at(j);
+    const uint64_t sp = j > 0 ? d.s_at(j - 1) : 0;
+    const uint64_t u = (sj & M) + (sp >> D::W);
+    w = (uint32_t)(u & M);
+    g = (uint32_t)(u >> D::W);
 }
-__device__ __forceinline__ void carry_gp(const uint64_t* c, long long j, long long nc, uint32_t& w, uint32_t& g) {
-    uint32_t sj = s_at(c, j, nc);
-    uint32_t sp = j > 0 ? s_at(c, j - 1, nc) : 0;
-    uint32_t u = (sj & 0xFFFF) + (sp >> 16);
-    w = u & 0xFFFF;
-    g = u >> 16;
+template <class D> __device__ __forceinline__ bool all_ones(uint32_t w) {
+    return D::W == 32 ? w == 0xFFFFFFFFu : w == ((1u << D::W) - 1);
 }
 // (G,P) composition: applying segment lo then hi: G = Ghi | (Phi & Glo), P = Phi & Plo
 constexpr int CARRY_T = 256, CARRY_E = 16, CARRY_B = CARRY_T * CARRY_E;
@@ -164,8 +194,8 @@ __device__ uint32_t block_carry_in(uint32_t mine, uint32_t cin, uint32_t* sh) {
     return res;
 }
 
-__global__ void __launch_bounds__(CARRY_T) k_carry_reduce(const uint64_t* __restrict__ c, long long nc, long long nout,
-                                                          uint32_t* __restrict__ agg) {
+template <class D>
+__global__ void __launch_bounds__(CARRY_T) k_carry_reduce(D d, long long nout, uint32_t* __restrict__ agg) {
     __shared__ uint32_t sh[64];
     long long j0 = (long long)blockIdx.x * CARRY_B + (long long)threadIdx.x * CARRY_E;
     uint32_t acc = 2u;   // identity
@@ -174,8 +204,8 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_reduce(const uint64_t* __rest
         uint32_t gp = 2u;
         if (j < nout) {
             uint32_t w, g;
-            carry_gp(c, j, nc, w, g);
-            gp = g | ((w == 0xFFFF ? 1u : 0u) << 1);
+            carry_gp(d, j, w, g);
+            gp = g | ((all_ones<D>(w) ? 1u : 0u) << 1);
         }
         acc = gp_comb(acc, gp);
     }
@@ -213,9 +243,9 @@ __global__ void k_carry_scan(uint32_t* agg, long long nblk) {
     }
 }
 
-__global__ void __launch_bounds__(CARRY_T) k_carry_apply(const uint64_t* __restrict__ c, long long nc, long long nout,
-                                                         const uint32_t* __restrict__ cin_blk,
-                                                         uint16_t* __restrict__ out) {
+template <class D>
+__global__ void __launch_bounds__(CARRY_T) k_carry_apply(D d, long long nout, const uint32_t* __restrict__ cin_blk,
+                                                         typename D::Out* __restrict__ out) {
     __shared__ uint32_t sh[64];
     long long j0 = (long long)blockIdx.x * CARRY_B + (long long)threadIdx.x * CARRY_E;
     uint32_t w[CARRY_E], g[CARRY_E];
@@ -226,8 +256,8 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_apply(const uint64_t* __restr
         w[e] = 0; g[e] = 0;
         uint32_t gp = 2u;
         if (j < nout) {
-            carry_gp(c, j, nc, w[e], g[e]);
-            gp = g[e] | ((w[e] == 0xFFFF ? 1u : 0u) << 1);
+            carry_gp(d, j, w[e], g[e]);
+            gp = g[e] | ((all_ones<D>(w[e]) ? 1u : 0u) << 1);
         }
         acc = gp_comb(acc, gp);
     }
@@ -235,8 +265,41 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_apply(const uint64_t* __restr
 #pragma unroll
     for (int e = 0; e < CARRY_E; e++) {
         long long j = j0 + e;
-        if (j < nout) out[j] = (uint16_t)((w[e] + C) & 0xFFFF);
-        C = g[e] | ((w[e] == 0xFFFF) & C);
+        if (j < nout) out[j] = (typename D::Out)(w[e] + C);    // mod 2^W by the cast
+        C = g[e] | ((all_ones<D>(w[e]) ? 1u : 0u) & C);
+    }
+}
+
+// ---------------------------------------------------------------- three-prime integer product
+// p1 = 998244353, p2 = 985661441, p3 = 943718401, 32-bit chunks (h = 32).
+struct Crt3 {
+    uint32_t p1, p2, p3;
+    uint32_t i12, i13, i23;   // p1^-1 mod p2, p1^-1 mod p3, p2^-1 mod p3
+    uint64_t p12;             // p1 p2
+};
+__global__ void k_residues3(const uint32_t* __restrict__ x, long long n, uint32_t* __restrict__ r, long long stride,
+                            Crt3 K) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const uint32_t v = x[i];
+        r[i] = v % K.p1;
+        r[stride + i] = v % K.p2;
+        r[2 * stride + i] = v % K.p3;
+    }
+}
+// Garner: c = x1 + p1 x2 + p1 p2 x3 < p1 p2 p3 < 2^90 from c mod p1, p2, p3 -> three 32-bit words
+__global__ void k_crt3(const uint32_t* __restrict__ c, long long stride, long long n, uint32_t* __restrict__ w, Crt3 K) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const uint32_t x1 = c[k], r2 = c[stride + k], r3 = c[2 * stride + k];
+        const uint32_t t2 = (uint32_t)(((uint64_t)(r2 + K.p2 - x1 % K.p2) % K.p2 * K.i12) % K.p2);
+        const uint32_t t3 = (uint32_t)(((uint64_t)(r3 + K.p3 - x1 % K.p3) % K.p3 * K.i13) % K.p3);
+        const uint32_t x3 = (uint32_t)(((uint64_t)(t3 + K.p3 - t2 % K.p3) % K.p3 * K.i23) % K.p3);
+        const uint64_t lo = (uint64_t)x1 + (uint64_t)K.p1 * t2;           // < 2^61
+        const uint64_t ml = K.p12 * x3, mh = __umul64hi(K.p12, (uint64_t)x3);
+        const uint64_t s = lo + ml;
+        const uint64_t hi = mh + (s < lo ? 1 : 0);
+        w[3 * k] = (uint32_t)s;
+        w[3 * k + 1] = (uint32_t)(s >> 32);
+        w[3 * k + 2] = (uint32_t)hi;
     }
 }
 
@@ -720,6 +783,27 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
     return MM_OK;
 }
 
+// a second per-stream workspace for drivers that call product_impl (which owns the first)
+static std::map<WsKey, std::pair<void*, size_t>> g_ws2;
+static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto& e = g_ws2[WsKey{dev, st}];
+    if (e.second < bytes) {
+        if (e.first) {
+            MM_CUDA_TRY(cudaStreamSynchronize(st));
+            cudaFree(e.first);
+            e.first = nullptr;
+            e.second = 0;
+        }
+        MM_CUDA_TRY(cudaMalloc(&e.first, bytes));
+        e.second = bytes;
+    }
+    *out = e.first;
+    return MM_OK;
+}
+
 // n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
 static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, long long lda, const uint32_t* b,
                                 long long lb, long long ldb, uint32_t* c, long long lc, long long ldc, long long batch,
@@ -1097,6 +1181,28 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     return MM_OK;
 }
 
+// reduce -> scan -> apply over nout output digits; agg: one word per CARRY_B digits
+template <class D>
+static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D::Out* out, cudaStream_t st) {
+    const long long nblk = (nout + CARRY_B - 1) / CARRY_B;
+    {
+        LaunchScope ls("carry_reduce", st);
+        k_carry_reduce<D><<<(int)nblk, CARRY_T, 0, st>>>(d, nout, agg);
+    }
+    MM_LAUNCH_CHECK();
+    {
+        LaunchScope ls("carry_scan", st);
+        k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
+    }
+    MM_LAUNCH_CHECK();
+    {
+        LaunchScope ls("carry_apply", st);
+        k_carry_apply<D><<<(int)nblk, CARRY_T, 0, st>>>(d, nout, agg, out);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
 extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t* b, size_t nb, uint16_t* c,
                                     void* stream) {
     if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
@@ -1125,23 +1231,62 @@ extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t
         MM_OK)
         return s;
     // carry propagation (evaluation at 2^16)
-    long long nblk = ((long long)nout + CARRY_B - 1) / CARRY_B;
-    uint32_t* agg = (uint32_t*)(coef + lc);
-    if (nblk > 16 * 1024 * 2) return set_err(MM_E_SIZE_OVERFLOW, "too many carry blocks");
+    if ((long long)(nout + CARRY_B - 1) / CARRY_B > 16 * 1024 * 2) return set_err(MM_E_SIZE_OVERFLOW, "too many carry blocks");
+    return carry_run(Dig16{coef, (long long)lc}, (long long)nout, (uint32_t*)(coef + lc), c, st);
+}
+
+// Three-prime integer product: 32-bit chunks (h = 32, A(2^32) = a),
+// three 32-bit NTT products mod p1, p2, p3, Garner CRT, carries.
+extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t* b, size_t nb, uint32_t* c,
+                                    void* stream) {
+    if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
+    if (na == 0 || nb == 0) return set_err(MM_E_ARG, "empty operands");
+    const size_t nout = na + nb, lc = na + nb - 1;
+    if (overlaps(a, na * 4, c, nout * 4) || overlaps(b, nb * 4, c, nout * 4))
+        return set_err(MM_E_ALIAS, "c aliases a or b");
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k == 0) k = 1;
+    // transform length <= 2^22 (2-adicity of p2, p3); then every coefficient
+    // <= min(na, nb) (2^32 - 1)^2 < 2^85 < p1 p2 p3 (2^89.6): H < log2(p1 p2 p3)
+    if (k > 22) return set_err(MM_E_SIZE_OVERFLOW, "na + nb - 1 > 2^22 (three-prime transform limit)");
+    static const uint32_t PR[3] = {998244353u, 985661441u, 943718401u}, GEN[3] = {3, 3, 7};
+    Crt3 K;
+    K.p1 = PR[0]; K.p2 = PR[1]; K.p3 = PR[2];
+    K.i12 = (uint32_t)hpowmod(PR[0] % PR[1], PR[1] - 2, PR[1]);
+    K.i13 = (uint32_t)hpowmod(PR[0] % PR[2], PR[2] - 2, PR[2]);
+    K.i23 = (uint32_t)hpowmod(PR[1] % PR[2], PR[2] - 2, PR[2]);
+    K.p12 = (uint64_t)PR[0] * PR[1];
+    cudaStream_t st = (cudaStream_t)stream;
+    // workspace: residues [3][na + nb], products [3][lc], CRT words [3 lc], carry aggregates
+    const size_t rs = na + nb;
+    const size_t nblk = (nout + CARRY_B - 1) / CARRY_B;
+    void* ws = nullptr;
+    mm_status s = stream_ws2(st, (3 * rs + 3 * lc + 3 * lc + nblk + 64) * 4, &ws);
+    if (s != MM_OK) return s;
+    uint32_t* R = (uint32_t*)ws;          // R[i * rs + j]: a_j mod p_i (j < na), b at offset na
+    uint32_t* Cp = R + 3 * rs;            // Cp[i * lc + k]: c_k mod p_i
+    uint32_t* Wd = Cp + 3 * lc;           // 96-bit coefficients
+    uint32_t* agg = Wd + 3 * lc;
+    const int grid = num_sms() * 8;
     {
-        LaunchScope ls("carry_reduce", st);
-        k_carry_reduce<<<(int)nblk, CARRY_T, 0, st>>>(coef, (long long)lc, (long long)nout, agg);
+        LaunchScope ls("crt_residues", st);
+        k_residues3<<<grid, 256, 0, st>>>(a, (long long)na, R, (long long)rs, K);
+        k_residues3<<<grid, 256, 0, st>>>(b, (long long)nb, R + na, (long long)rs, K);
     }
     MM_LAUNCH_CHECK();
+    for (int i = 0; i < 3; i++) {
+        uint64_t omega = hpowmod(GEN[i], (PR[i] - 1) >> k, PR[i]);
+        mm_ntt_plan* P = nullptr;
+        if ((s = cached_plan(32, PR[i], k, omega, &P)) != MM_OK) return s;
+        if ((s = product_impl<Fp32, uint32_t, uint32_t>(P, R + i * rs, (long long)na, R + i * rs + na, (long long)nb,
+                                                        Cp + i * lc, (long long)lc, 1, st)) != MM_OK)
+            return s;
+    }
     {
-        LaunchScope ls("carry_scan", st);
-        k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
+        LaunchScope ls("crt_garner", st);
+        k_crt3<<<grid, 256, 0, st>>>(Cp, (long long)lc, (long long)lc, Wd, K);
     }
     MM_LAUNCH_CHECK();
-    {
-        LaunchScope ls("carry_apply", st);
-        k_carry_apply<<<(int)nblk, CARRY_T, 0, st>>>(coef, (long long)lc, (long long)nout, agg, c);
-    }
-    MM_LAUNCH_CHECK();
-    return MM_OK;
+    return carry_run(Dig32x3{Wd, (long long)lc}, (long long)nout, agg, c, st);
 }

@@ -311,8 +311,12 @@ def test_poly_mul_c3_full_sampled(mm, O):
     p, g, B, d = P30, 3, 4096, 1 << 15
     a = gen.residues_torch(config_seed(3), 1, B * d, p, DEV).view(torch.uint32).reshape(B, d)
     b = gen.residues_torch(config_seed(3), 2, B * d, p, DEV).view(torch.uint32).reshape(B, d)
-    c = mm.poly_mul(a, b, p, g)
+    # bench.py's launch: output rows at leading dimension 2^16 (mm_poly_mul_ld)
+    c_pad = torch.empty((B, 1 << 16), dtype=torch.uint32, device=DEV)
+    c = mm.poly_mul(a, b, p, g, out=c_pad[:, :2 * d - 1])
     ah, bh, ch = host(a), host(b), host(c)
+    cp = mm.poly_mul(a[:64], b[:64], p, g)                # packed layout, same products
+    assert torch.equal(c[:64], cp)
     rng = random.Random(3)
     for r in range(0, B, 1):
         x = rng.randrange(1, p)
@@ -324,6 +328,54 @@ def test_poly_mul_c3_full_sampled(mm, O):
 # ------------------------------------------------------------------ int_mul
 def _to_int(limbs):
     return int.from_bytes(np.asarray(limbs, dtype="<u2").tobytes(), "little")
+
+
+def _to_int32(limbs):
+    return int.from_bytes(np.asarray(limbs, dtype="<u4").tobytes(), "little")
+
+
+def _limbs32(seed, n):
+    return (limbs16(seed, 1, 2 * n).view(np.uint32)).copy()
+
+
+@pytest.mark.parametrize("na,nb", [(1, 1), (2, 2), (3, 1), (300, 257), (2048, 2049), (4096, 4096), (5000, 3),
+                                   (10000, 12345), (1 << 15, 1 << 15), (40000, 70000)])
+def test_int_mul_u32_three_prime(mm, O, na, nb):
+    # P:971-979 three-prime FFT product vs Python big integers (library routine)
+    a, b = _limbs32(na, na), _limbs32(nb + 1, nb)
+    c = host(mm.int_mul_u32(dev(a), dev(b)))
+    assert c.dtype == np.uint32 and c.size == na + nb
+    assert _to_int32(c) == _to_int32(a) * _to_int32(b)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4097, 1 << 16])
+def test_int_mul_u32_all_ones(mm, O, N):
+    # (2^(32N) - 1)^2: every coefficient at its maximum N (2^32 - 1)^2 (closed form)
+    a = np.full(N, 0xFFFFFFFF, dtype=np.uint32)
+    c = host(mm.int_mul_u32(dev(a), dev(a)))
+    ref = np.zeros(2 * N, dtype=np.uint32)
+    ref[0] = 1
+    ref[N] = 0xFFFFFFFE
+    ref[N + 1:] = 0xFFFFFFFF
+    assert np.array_equal(c, ref)
+
+
+def test_int_mul_u32_paper_max(mm, O):
+    # Table 16's largest size: 32 x 2^20-bit operands (na = nb = 2^20, transform 2^21);
+    # checked by casting out random 61-bit primes and on the low 2^11 limbs exactly
+    n = 1 << 20
+    a, b = _limbs32(71, n), _limbs32(72, n)
+    c = host(mm.int_mul_u32(dev(a), dev(b)))
+    rng = random.Random(20)
+    for _ in range(3):
+        q = rng.randrange(1 << 60, 1 << 61) | 1
+        assert O.limbs_mod(c.view(np.uint16), q) == O.limbs_mod(a.view(np.uint16), q) * O.limbs_mod(b.view(np.uint16), q) % q
+    k = 1 << 11
+    lo = _to_int32(a[:k]) * _to_int32(b[:k]) % (1 << (32 * k))
+    assert _to_int32(c[:k]) == lo
+    # and the same product through the Goldilocks path (16-bit limbs)
+    c16 = host(mm.int_mul_u16(dev(a.view(np.uint16)), dev(b.view(np.uint16))))
+    assert np.array_equal(c16.view(np.uint32), c)
 
 
 @pytest.mark.parametrize("na,nb", [(1, 1), (2, 2), (3, 1), (300, 257), (2048, 2049), (4096, 4096),
