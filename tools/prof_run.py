@@ -16,7 +16,7 @@ if which == "c3":
     B, d = 4096, 1 << 15
     a = gen.residues_torch(gen.config_seed(3), 1, B * d, P30, dev).view(torch.uint32).reshape(B, d)
     b = gen.residues_torch(gen.config_seed(3), 2, B * d, P30, dev).view(torch.uint32).reshape(B, d)
-    c = torch.empty((B, 2 * d - 1), dtype=torch.uint32, device=dev)
+    c = torch.empty((B, 1 << 16), dtype=torch.uint32, device=dev)[:, :2 * d - 1]   # bench.py's ldc
     for _ in range(2):
         mm.poly_mul(a, b, P30, 3, out=c)
 elif which == "c4":
