@@ -399,6 +399,47 @@ def extras_run(mm, torch, dev, peaks):
     return out
 
 
+def sharded_run(mm, torch, dev, world, rank):
+    """N > 1: the partitioned configs -- C4's 2^24 Goldilocks
+    transforms and C5's integer product, each split across all ranks by
+    dist.py (column blocks, NCCL all-to-all, row blocks); strong scaling,
+    device time max over ranks."""
+    import gen
+    from paper_1407_3383_b200.dist import ShardedIntMul, ShardedNtt
+    out = {}
+    # C4: 8 forward transforms of 2^24, each sharded over all ranks
+    k = 24
+    plan = mm.NttPlan(64, PG, k, root_of_unity(PG, 7, k), 1)
+    sh = ShardedNtt(plan)
+    idx = sh.column_block_indices().reshape(-1).to(dev)
+    xs = []
+    for t in range(8):
+        full = gen.residues_torch(gen.config_seed(4), 1, 1 << k, PG, dev, start=t << k).view(torch.int64)
+        xs.append(full[idx].reshape(sh.n2, sh.c1).view(torch.uint64).contiguous())
+        del full
+
+    def c4():
+        for x in xs:
+            sh.forward(x)
+
+    ms = timed(c4, 3, 3, world)
+    ms /= 3
+    bfly = 8 * (1 << (k - 1)) * k
+    out["C4_sharded_8x2^24_fwd"] = {"ms": round(ms, 3), "Gbutterfly_per_s": round(bfly / (ms * 1e-3) / 1e9, 1),
+                                    "scaling": "strong", "ranks": world}
+    del xs
+    # C5: one 2^28-bit x 2^28-bit product sharded over all ranks
+    n = 1 << 24
+    a = gen.limbs16_torch(gen.config_seed(5), 1, n, dev).view(torch.uint16)
+    b = gen.limbs16_torch(gen.config_seed(5), 2, n, dev).view(torch.uint16)
+    plan5 = mm.NttPlan(64, PG, 25, root_of_unity(PG, 7, 25), 1)
+    im = ShardedIntMul(plan5, n, n)
+    ms = timed(lambda: im(a, b), 3, 3, world) / 3
+    out["C5_sharded_int_mul_2^28bit"] = {"ms": round(ms, 3), "Mbit_per_s": round(2 * (1 << 28) / (ms * 1e-3) / 1e6, 1),
+                                         "scaling": "strong", "ranks": world}
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
     import gen
@@ -516,6 +557,11 @@ def run_ours(args, world, rank, local):
     extra = {}
     if world == 1 and not args.no_extras:
         extra = extras_run(mm, torch, dev, peaks)
+    if world > 1 and not args.no_extras:
+        try:
+            extra = sharded_run(mm, torch, dev, world, rank)
+        except Exception as e:   # the headline line must survive a failing secondary measurement
+            extra = {"sharded_error": repr(e)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -241,6 +241,41 @@ mm_status mm_ntt_fwd_rows_seg(const mm_ntt_plan *plan, const void *in, void *out
 mm_status mm_ntt_inv_rows_seg(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
                               size_t out_seg_len, size_t out_seg_stride, void *stream);
 
+/* Sharded integer product blocks (paper_1407_3383_b200/dist.py
+ * ShardedIntMul; 64-bit Goldilocks plans):
+ *   mm_ntt_fwd_cols_u16 : Algorithm 1 steps 1-2 on columns
+ *       [col0, col0 + ncols) of the zero-padded 16-bit limb vector (nlimbs
+ *       valid limbs, read in place, widened) viewed as [n2][n1]; out
+ *       [n2][ncols] u64.
+ *   mm_ntt_pmul_rows_seg : for rows [row0, row0 + nrows) held in segmented
+ *       all-to-all buffers (element (r, j) at (j / seg_len) seg_stride +
+ *       r seg_len + j mod seg_len) of both operands: steps 3-4, pointwise
+ *       product, inverse steps 4-3 and the inverse step-2 twiddle,
+ *       into the segmented send buffer c.  No n^-1 (mm_ntt_inv_cols has it).
+ * Carries over column blocks (evaluation at 2^16): a rank holds
+ * coefficients c_j, j = r n1 + col0 + i for r < nrows, i < c1 (nc product
+ * coefficients in all, nout output limbs).  halo[r] = the 4 coefficients
+ * before chunk r (from the previous rank; shift = 1 on rank 0, whose row r
+ * follows row r - 1 of the last rank).
+ *   mm_carry_chunks_halo   : halo_out[r] = last 4 coefficients of chunk r.
+ *   mm_carry_chunks_reduce : agg[r] = (generate, propagate) of chunk r.
+ *   mm_carry_chunks_scan   : agg_all = all-gathered [G][nrows] aggregates;
+ *       replaced in place by the carry into each chunk, chunks taken in
+ *       natural order r G + g.
+ *   mm_carry_chunks_apply  : out[r][i] = 16-bit limb j of the product. */
+mm_status mm_ntt_fwd_cols_u16(const mm_ntt_plan *plan, const uint16_t *limbs, size_t nlimbs, void *out, size_t col0,
+                              size_t ncols, void *stream);
+mm_status mm_ntt_pmul_rows_seg(const mm_ntt_plan *plan, const void *a, const void *b, void *c, size_t row0,
+                               size_t nrows, size_t seg_len, size_t seg_stride, void *stream);
+mm_status mm_carry_chunks_halo(const uint64_t *coef, size_t nrows, size_t c1, uint64_t *halo_out, void *stream);
+mm_status mm_carry_chunks_reduce(const uint64_t *coef, const uint64_t *halo_in, size_t nrows, size_t c1, size_t n1,
+                                 size_t col0, size_t nc, size_t nout, int shift, uint32_t *agg, void *stream);
+mm_status mm_carry_chunks_scan(uint32_t *agg_all, size_t G, size_t nrows, void *stream);
+mm_status mm_carry_chunks_apply(const uint64_t *coef, const uint64_t *halo_in, size_t nrows, size_t c1, size_t n1,
+                                size_t col0, size_t nc, size_t nout, int shift, const uint32_t *cin, uint16_t *out,
+                                void *stream);
+
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,12 @@ EXPORTS = {
     "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ntt_fwd_cols_u16": (_ST, [_P, _P, _sz, _P, _sz, _sz, _P]),
+    "mm_ntt_pmul_rows_seg": (_ST, [_P, _P, _P, _P, _sz, _sz, _sz, _sz, _P]),
+    "mm_carry_chunks_halo": (_ST, [_P, _sz, _sz, _P, _P]),
+    "mm_carry_chunks_reduce": (_ST, [_P, _P, _sz, _sz, _sz, _sz, _sz, _sz, _i32, _P, _P]),
+    "mm_carry_chunks_scan": (_ST, [_P, _sz, _sz, _P]),
+    "mm_carry_chunks_apply": (_ST, [_P, _P, _sz, _sz, _sz, _sz, _sz, _sz, _i32, _P, _P, _P]),
     "mm_ntt_fwd_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_ntt_inv_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_launch_count": (ctypes.c_ulonglong, []),
@@ -246,6 +252,21 @@ class NttPlan:
         _check(lib().mm_ntt_inv_rows_seg(self._h, _ptr(x), _ptr(out), row0, nrows, seg_len, seg_stride, _stream(x)))
         return out
 
+    def fwd_cols_u16(self, limbs, out, col0, ncols):
+        """Steps 1-2 on columns [col0, col0 + ncols) of the zero-padded 16-bit limb
+        vector viewed as [n2][n1] (widened to the 64-bit field); out [n2][ncols]."""
+        _check(lib().mm_ntt_fwd_cols_u16(self._h, _ptr(limbs), limbs.numel(), _ptr(out), col0, ncols,
+                                         _stream(limbs)))
+        return out
+
+    def pmul_rows_seg(self, a, b, out, row0, nrows, seg_len, seg_stride):
+        """Rows of both operands (segmented receive buffers): steps 3-4, pointwise
+        product, inverse steps 4-3 and twiddle, into a segmented send buffer
+        (no n^-1: inv_cols applies it)."""
+        _check(lib().mm_ntt_pmul_rows_seg(self._h, _ptr(a), _ptr(b), _ptr(out), row0, nrows, seg_len, seg_stride,
+                                          _stream(a)))
+        return out
+
     def inv_cols(self, x, out, col0, ncols):
         _check(lib().mm_ntt_inv_cols(self._h, _ptr(x), _ptr(out), col0, ncols, _stream(x)))
         return out
@@ -346,6 +367,30 @@ def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.T
                                   ctypes.c_void_p(b2.data_ptr()), lb, ctypes.c_void_p(out.data_ptr()), batch,
                                   ctypes.c_void_p(st.cuda_stream)))
     st.synchronize()
+    return out
+
+
+# ------------------------------------------------------------------ chunked carries (sharded int_mul)
+def carry_chunks_halo(coef, halo_out):
+    """halo_out[r] = the last 4 coefficients of chunk r of a [nrows][c1] block."""
+    _check(lib().mm_carry_chunks_halo(_ptr(coef), coef.shape[0], coef.shape[1], _ptr(halo_out), _stream(coef)))
+    return halo_out
+
+
+def carry_chunks_reduce(coef, halo, n1, col0, nc, nout, shift, agg):
+    _check(lib().mm_carry_chunks_reduce(_ptr(coef), _ptr(halo), coef.shape[0], coef.shape[1], n1, col0, nc, nout,
+                                        int(shift), _ptr(agg), _stream(coef)))
+    return agg
+
+
+def carry_chunks_scan(agg_all, G, nrows):
+    _check(lib().mm_carry_chunks_scan(_ptr(agg_all), G, nrows, _stream(agg_all)))
+    return agg_all
+
+
+def carry_chunks_apply(coef, halo, n1, col0, nc, nout, shift, cin, out):
+    _check(lib().mm_carry_chunks_apply(_ptr(coef), _ptr(halo), coef.shape[0], coef.shape[1], n1, col0, nc, nout,
+                                       int(shift), _ptr(cin), _ptr(out), _stream(coef)))
     return out
 
 

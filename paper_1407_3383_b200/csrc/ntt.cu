@@ -270,6 +270,121 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_apply(D d, long long nout, co
     }
 }
 
+// ---------------------------------------------------------------- carries over column blocks (sharded int_mul)
+// A rank of the sharded product holds coefficients c_j, j = r n1 + col0 + i
+// (row r < nrows, i < c1): one chunk of c1 consecutive j per row.  The digit
+// sums at the start of a chunk need the 4 coefficients before it (halo):
+// halo[r] = the last 4 coefficients of the preceding chunk, i.e. of the same
+// row on the previous rank, or -- on rank 0 (shift) -- of row r - 1 on the last
+// rank.  Coefficients with global index outside [0, nc) are zero.
+struct ChunkRef {
+    const uint64_t* coef;
+    const uint64_t* halo;
+    long long c1, n1, col0, nc, nout;
+    int shift;
+    __device__ __forceinline__ uint64_t cf(long long r, long long i) const {
+        if (i >= 0) return coef[r * c1 + i];
+        const long long hr = shift ? r - 1 : r;
+        return hr >= 0 ? halo[hr * 4 + 4 + i] : 0;
+    }
+    __device__ __forceinline__ uint64_t s_at(long long r, long long i) const {
+        const long long jg = r * n1 + col0 + i;
+        uint64_t s = 0;
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+            if (jg - t >= 0 && jg - t < nc) s += (cf(r, i - t) >> (16 * t)) & 0xFFFF;
+        return s;
+    }
+    __device__ __forceinline__ void gp(long long r, long long i, uint32_t& w, uint32_t& g) const {
+        const uint64_t sj = s_at(r, i);
+        const uint64_t sp = (r * n1 + col0 + i > 0) ? s_at(r, i - 1) : 0;
+        const uint64_t u = (sj & 0xFFFF) + (sp >> 16);
+        w = (uint32_t)(u & 0xFFFF);
+        g = (uint32_t)(u >> 16);
+    }
+};
+__global__ void k_chunk_halo(const uint64_t* __restrict__ coef, long long nrows, long long c1, uint64_t* __restrict__ halo) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nrows * 4; i += (long long)gridDim.x * blockDim.x)
+        halo[i] = coef[(i >> 2) * c1 + c1 - 4 + (i & 3)];
+}
+// one CTA per chunk: (G, P) aggregate of its digits (identity beyond nout)
+__global__ void __launch_bounds__(256) k_chunk_reduce(ChunkRef R, uint32_t* __restrict__ agg) {
+    __shared__ uint32_t sh[64];
+    const long long r = blockIdx.x;
+    const int E = (int)((R.c1 + blockDim.x - 1) / blockDim.x);
+    uint32_t acc = 2u;
+    for (int e = 0; e < E; e++) {
+        const long long i = (long long)threadIdx.x * E + e;
+        uint32_t gpv = 2u;
+        if (i < R.c1 && r * R.n1 + R.col0 + i < R.nout) {
+            uint32_t w, g;
+            R.gp(r, i, w, g);
+            gpv = g | ((w == 0xFFFF ? 1u : 0u) << 1);
+        }
+        acc = gp_comb(acc, gpv);
+    }
+    // block reduction of the (G, P) pairs in thread order
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = gp_comb(y, x);
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t v = 2u;
+        for (int q = 0; q < (int)(blockDim.x >> 5); q++) v = gp_comb(v, sh[q]);
+        agg[r] = v;
+    }
+}
+// sequential scan of chunk aggregates in natural chunk order q = r G + g, stored at
+// agg[g nrows + r] (the all-gathered layout); replaced by the carry into each chunk
+__global__ void k_chunk_scan(uint32_t* agg, long long G, long long nrows) {
+    __shared__ uint32_t sh[64];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const long long nq = G * nrows;
+    for (long long base = 0; base < nq; base += blockDim.x) {
+        const long long q = base + threadIdx.x;
+        const long long at = q < nq ? (q % G) * nrows + q / G : 0;
+        const uint32_t mine = q < nq ? agg[at] : 2u;
+        const uint32_t cin = block_carry_in(mine, carry, sh);
+        __syncthreads();
+        if (q < nq) agg[at] = cin;
+        if (threadIdx.x == blockDim.x - 1) carry = (mine & 1) | ((mine >> 1) & cin);
+        __syncthreads();
+    }
+}
+__global__ void __launch_bounds__(256) k_chunk_apply(ChunkRef R, const uint32_t* __restrict__ cin_chunk,
+                                                     uint16_t* __restrict__ out) {
+    __shared__ uint32_t sh[64];
+    const long long r = blockIdx.x;
+    const int E = (int)((R.c1 + blockDim.x - 1) / blockDim.x);
+    uint32_t acc = 2u;
+    for (int e = 0; e < E; e++) {
+        const long long i = (long long)threadIdx.x * E + e;
+        uint32_t gpv = 2u;
+        if (i < R.c1 && r * R.n1 + R.col0 + i < R.nout) {
+            uint32_t w, g;
+            R.gp(r, i, w, g);
+            gpv = g | ((w == 0xFFFF ? 1u : 0u) << 1);
+        }
+        acc = gp_comb(acc, gpv);
+    }
+    uint32_t C = block_carry_in(acc, cin_chunk[r], sh);
+    for (int e = 0; e < E; e++) {
+        const long long i = (long long)threadIdx.x * E + e;
+        if (i >= R.c1) break;
+        uint32_t w = 0, g = 0;
+        const bool live = r * R.n1 + R.col0 + i < R.nout;
+        if (live) R.gp(r, i, w, g);
+        out[r * R.c1 + i] = live ? (uint16_t)(w + C) : (uint16_t)0;
+        C = g | ((w == 0xFFFF ? 1u : 0u) & C);
+    }
+}
+
 // ---------------------------------------------------------------- three-prime integer product
 // p1 = 998244353, p2 = 985661441, p3 = 943718401, 32-bit chunks (h = 32).
 struct Crt3 {
@@ -1289,4 +1404,132 @@ extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t
     }
     MM_LAUNCH_CHECK();
     return carry_run(Dig32x3{Wd, (long long)lc}, (long long)nout, agg, c, st);
+}
+
+// ---- sharded integer product building blocks (dist.py ShardedIntMul) ----------------
+extern "C" mm_status mm_ntt_fwd_cols_u16(const mm_ntt_plan* plan, const uint16_t* limbs, size_t nlimbs, void* out,
+                                         size_t col0, size_t ncols, void* stream) {
+    mm_status s = dist_check(plan, limbs, out, col0, ncols, true);
+    if (s != MM_OK) return s;
+    if (plan->word_bits != 64) return set_err(MM_E_ARG, "16-bit limb columns need a 64-bit (Goldilocks) plan");
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    FpG f;
+    ColArgs<FpG> c{};
+    c.in = limbs + col0;     // element (j2, j1) of the zero-padded limb vector at limbs[j2 n1 + j1]
+    c.out = out;
+    c.ncols = (long long)ncols;
+    c.nbatch = 1;
+    c.in_rs = 1ll << P->k1;
+    c.out_rs = (long long)ncols;
+    c.in_bs = c.out_bs = 0;
+    c.in_len = (long long)nlimbs;
+    c.out_len = 1ll << P->k;
+    c.col0 = (long long)col0;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.fs = 1;
+    c.lvl = (const uint64_t*)P->lvl_f2;
+    c.fs_lo = (const uint64_t*)P->fs_lo_f;
+    c.fs_hi = (const uint64_t*)P->fs_hi_f;
+    c.fs_full = (const uint64_t*)P->fs_full_f;
+    c.fs_h = P->fs_h;
+    return launch_cols<FpG, false, uint16_t, uint64_t>(f, c, (cudaStream_t)stream);
+}
+
+template <class F>
+static mm_status pmul_rows_seg_impl(mm_ntt_plan* P, const void* a, const void* b, void* c, size_t row0, size_t nrows,
+                                    int sl, long long seg_stride, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    PmulArgs<F> m{};
+    m.a = a; m.b = b; m.c = c;
+    m.nrows = (long long)nrows;
+    m.a_rs = m.b_rs = m.c_rs = 1ll << sl;
+    m.la = m.lb = m.lc = 1ll << P->k1;
+    m.k = P->k1;
+    m.fs = 1; m.k2 = P->k2; m.row0 = (long long)row0;
+    m.in_seg_log = m.out_seg_log = sl;
+    m.in_seg_stride = m.out_seg_stride = seg_stride;
+    // unscaled product (mm_ntt_inv_cols applies n^-1): 1, or 2^32 to undo the 32-bit REDC
+    m.sc = host_w<W>(sizeof(T) == 4 ? (uint64_t)(((u128)1 << 32) % P->p) : 1, P->p);
+    m.lvl_f = (const W*)P->lvl_f1;
+    m.lvl_i = (const W*)P->lvl_i1;
+    m.fs_lo = (const W*)P->fs_lo_i;
+    m.fs_hi = (const W*)P->fs_hi_i;
+    m.fs_full = (const W*)P->fs_full_i;
+    m.fs_h = P->fs_h;
+    return launch_pmul<F, T, T>(f, m, st);
+}
+extern "C" mm_status mm_ntt_pmul_rows_seg(const mm_ntt_plan* plan, const void* a, const void* b, void* c, size_t row0,
+                                          size_t nrows, size_t seg_len, size_t seg_stride, void* stream) {
+    mm_status s = dist_check(plan, a, c, row0, nrows, false);
+    if (s != MM_OK) return s;
+    if (!b) return set_err(MM_E_ARG, "null argument");
+    int sl = 0;
+    if ((s = seg_check(plan, seg_len, seg_stride, nrows, &sl)) != MM_OK) return s;
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    cudaStream_t st = (cudaStream_t)stream;
+    return P->word_bits == 32 ? pmul_rows_seg_impl<Fp32>(P, a, b, c, row0, nrows, sl, (long long)seg_stride, st)
+                              : pmul_rows_seg_impl<FpG>(P, a, b, c, row0, nrows, sl, (long long)seg_stride, st);
+}
+
+static mm_status chunk_args(const uint64_t* coef, const uint64_t* halo, size_t nrows, size_t c1, size_t n1, size_t col0,
+                            size_t nc, size_t nout, int shift, ChunkRef* R) {
+    if (!coef || (!halo && nrows > 0)) return set_err(MM_E_ARG, "null argument");
+    if (c1 < 4 || c1 > n1 || col0 + c1 > n1) return set_err(MM_E_ARG, "chunk [%zu, %zu) not inside a row of %zu", col0, col0 + c1, n1);
+    R->coef = coef; R->halo = halo;
+    R->c1 = (long long)c1; R->n1 = (long long)n1; R->col0 = (long long)col0;
+    R->nc = (long long)nc; R->nout = (long long)nout; R->shift = shift;
+    return MM_OK;
+}
+extern "C" mm_status mm_carry_chunks_halo(const uint64_t* coef, size_t nrows, size_t c1, uint64_t* halo_out, void* stream) {
+    if (!coef || !halo_out || c1 < 4) return set_err(MM_E_ARG, "bad halo arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        LaunchScope ls("carry_halo", st);
+        k_chunk_halo<<<(int)((nrows * 4 + 255) / 256), 256, 0, st>>>(coef, (long long)nrows, (long long)c1, halo_out);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+extern "C" mm_status mm_carry_chunks_reduce(const uint64_t* coef, const uint64_t* halo_in, size_t nrows, size_t c1,
+                                            size_t n1, size_t col0, size_t nc, size_t nout, int shift, uint32_t* agg,
+                                            void* stream) {
+    ChunkRef R;
+    mm_status s = chunk_args(coef, halo_in, nrows, c1, n1, col0, nc, nout, shift, &R);
+    if (s != MM_OK) return s;
+    if (!agg) return set_err(MM_E_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        LaunchScope ls("carry_reduce", st);
+        k_chunk_reduce<<<(int)nrows, 256, 0, st>>>(R, agg);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+extern "C" mm_status mm_carry_chunks_scan(uint32_t* agg_all, size_t G, size_t nrows, void* stream) {
+    if (!agg_all || G == 0) return set_err(MM_E_ARG, "bad scan arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        LaunchScope ls("carry_scan", st);
+        k_chunk_scan<<<1, 1024, 0, st>>>(agg_all, (long long)G, (long long)nrows);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+extern "C" mm_status mm_carry_chunks_apply(const uint64_t* coef, const uint64_t* halo_in, size_t nrows, size_t c1,
+                                           size_t n1, size_t col0, size_t nc, size_t nout, int shift,
+                                           const uint32_t* cin, uint16_t* out, void* stream) {
+    ChunkRef R;
+    mm_status s = chunk_args(coef, halo_in, nrows, c1, n1, col0, nc, nout, shift, &R);
+    if (s != MM_OK) return s;
+    if (!cin || !out) return set_err(MM_E_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        LaunchScope ls("carry_apply", st);
+        k_chunk_apply<<<(int)nrows, 256, 0, st>>>(R, cin, out);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
 }

@@ -105,3 +105,111 @@ class ShardedNtt:
     def row_block_positions(self) -> range:
         """Positions of the bit-mirrored output held by this rank."""
         return range(self.rank * self.r2 * self.n1, (self.rank + 1) * self.r2 * self.n1)
+
+
+class ShardedIntMul:
+    """One integer product a b sharded over the ranks of `group`.
+
+    a, b: 16-bit little-endian limbs (every rank holds both: 2 B per limb), the
+    product runs over p = 2^64 - 2^32 + 1 as in mm_int_mul_u16 (P:971-973 with
+    one prime, R7).  Per rank: the column pass reads its columns of
+    the zero-padded limb vectors in place (mm_ntt_fwd_cols_u16); one all-to-all
+    per operand; one fused row kernel (steps 3-4 of both operands, pointwise
+    product, inverse steps 4-3 and twiddle, mm_ntt_pmul_rows_seg); one
+    all-to-all back; the inverse column pass (n^-1).  Rank g then holds the
+    coefficients c_j, j = r n1 + g c1 + i, as n2 chunks of c1 consecutive j.
+    Carries (evaluation at 2^16): each chunk needs the 4 coefficients before it
+    (a ring send of [n2][4] words to the next rank), per-chunk (generate,
+    propagate) pairs are all-gathered ([G][n2] words) and scanned in natural
+    chunk order on every rank, then applied locally.  Output: the limbs of
+    a b at the same positions, [n2][c1] 16-bit words (limb_indices()).
+
+    `backend` supplies carry_chunks_{halo,reduce,scan,apply} (the library by
+    default; the CPU tests pass a reference)."""
+
+    def __init__(self, plan, na: int, nb: int, group=None, rank=None, world=None, backend=None):
+        self.nt = ShardedNtt(plan, group, rank, world)
+        self.plan, self.group = plan, group
+        self.na, self.nb = na, nb
+        self.nc, self.nout = na + nb - 1, na + nb
+        n1, n2 = self.nt.n1, self.nt.n2
+        if self.nout > n1 * n2:
+            raise ValueError(f"na + nb = {self.nout} limbs exceed the transform length {n1 * n2}")
+        if self.nt.c1 < 4:
+            raise ValueError("column blocks must hold at least 4 columns (carry halo)")
+        if backend is None:
+            import paper_1407_3383_b200 as backend
+        self.be = backend
+
+    # ---- phases (each local; the collectives sit between them)
+    def forward_cols(self, limbs: torch.Tensor) -> torch.Tensor:
+        nt = self.nt
+        y = torch.empty((nt.n2, nt.c1), dtype=torch.uint64, device=limbs.device)
+        self.plan.fwd_cols_u16(limbs, y, nt.rank * nt.c1, nt.c1)
+        return y.reshape(-1)
+
+    def products(self, recv_a: torch.Tensor, recv_b: torch.Tensor) -> torch.Tensor:
+        nt = self.nt
+        send = torch.empty_like(recv_a)
+        self.plan.pmul_rows_seg(recv_a, recv_b, send, nt.rank * nt.r2, nt.r2, nt.c1, nt.r2 * nt.c1)
+        return send
+
+    def coefficients(self, recv_c: torch.Tensor) -> torch.Tensor:
+        return self.nt.inverse_cols(recv_c)
+
+    def carry_halo(self, coef: torch.Tensor) -> torch.Tensor:
+        halo = torch.empty((coef.shape[0], 4), dtype=coef.dtype, device=coef.device)
+        return self.be.carry_chunks_halo(coef, halo)
+
+    def carry_reduce(self, coef: torch.Tensor, halo_in: torch.Tensor) -> torch.Tensor:
+        nt = self.nt
+        agg = torch.empty(coef.shape[0], dtype=torch.uint32, device=coef.device)
+        return self.be.carry_chunks_reduce(coef, halo_in, nt.n1, nt.rank * nt.c1, self.nc, self.nout,
+                                           nt.rank == 0, agg)
+
+    def carry_scan(self, agg_all: torch.Tensor) -> torch.Tensor:
+        return self.be.carry_chunks_scan(agg_all, self.nt.G, self.nt.n2)
+
+    def carry_apply(self, coef: torch.Tensor, halo_in: torch.Tensor, cin: torch.Tensor) -> torch.Tensor:
+        nt = self.nt
+        out = torch.empty(coef.shape, dtype=torch.uint16, device=coef.device)
+        return self.be.carry_chunks_apply(coef, halo_in, nt.n1, nt.rank * nt.c1, self.nc, self.nout, nt.rank == 0,
+                                          cin, out)
+
+    # ---- collectives
+    def _a2a(self, send: torch.Tensor) -> torch.Tensor:
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(_bits(recv), _bits(send), group=self.group)
+        return recv
+
+    def _ring(self, halo_out: torch.Tensor) -> torch.Tensor:
+        """halo_in = halo_out of rank g - 1 (rank 0 gets the last rank's)."""
+        G, g = self.nt.G, self.nt.rank
+        if G == 1:
+            return halo_out.clone()
+        halo_in = torch.empty_like(halo_out)
+        grp = self.group
+        nxt = dist.get_global_rank(grp, (g + 1) % G) if grp is not None else (g + 1) % G
+        prv = dist.get_global_rank(grp, (g - 1) % G) if grp is not None else (g - 1) % G
+        ops = [dist.P2POp(dist.isend, _bits(halo_out), nxt, grp), dist.P2POp(dist.irecv, _bits(halo_in), prv, grp)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return halo_in
+
+    def __call__(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        if a.numel() != self.na or b.numel() != self.nb:
+            raise ValueError("operand sizes differ from the plan")
+        recv_a = self._a2a(self.forward_cols(a))
+        recv_b = self._a2a(self.forward_cols(b))
+        coef = self.coefficients(self._a2a(self.products(recv_a, recv_b)))
+        halo_in = self._ring(self.carry_halo(coef))
+        agg = self.carry_reduce(coef, halo_in)
+        agg_all = torch.empty(self.nt.G * agg.numel(), dtype=agg.dtype, device=agg.device)
+        dist.all_gather_into_tensor(_bits(agg_all), _bits(agg), group=self.group)
+        self.carry_scan(agg_all)
+        cin = agg_all[self.nt.rank * self.nt.n2:(self.nt.rank + 1) * self.nt.n2]
+        return self.carry_apply(coef, halo_in, cin)
+
+    def limb_indices(self) -> torch.Tensor:
+        """Limb indices j of this rank's output block, as [n2][c1]."""
+        return self.nt.column_block_indices()

@@ -101,6 +101,98 @@ class RefPlan:
         self._put(out, Y)
 
 
+    # ---- sharded integer product blocks (same semantics as the library's)
+    def fwd_cols_u16(self, limbs, out, col0, ncols):
+        L = limbs.numpy().view(np.uint16).astype(np.uint64)
+        full = np.zeros(self.n1 * self.n2, dtype=np.uint64)
+        full[:L.size] = L
+        X = full.reshape(self.n2, self.n1)[:, col0:col0 + ncols].copy()
+        self.fwd_cols(torch.from_numpy(X.view(np.int64)), out, col0, ncols)
+        return out
+
+    def pmul_rows_seg(self, a, b, out, row0, nrows, seg_len, seg_stride):
+        O, p = self.O, self.p
+        ta = torch.empty((nrows, self.n1), dtype=torch.int64)
+        tb = torch.empty((nrows, self.n1), dtype=torch.int64)
+        self.fwd_rows_seg(a, ta, row0, nrows, seg_len, seg_stride)
+        self.fwd_rows_seg(b, tb, row0, nrows, seg_len, seg_stride)
+        C = O.vec_mulmod(self._np(ta).reshape(-1), self._np(tb).reshape(-1), p).reshape(nrows, self.n1)
+        self.inv_rows_seg(torch.from_numpy(C.astype(np.uint64).view(np.int64)), out, row0, nrows, seg_len,
+                          seg_stride)
+        return out
+
+
+class RefCarry:
+    """Reference for the chunked carry kernels: digits of c_j at 2^16, the
+    (generate, propagate) chain, evaluated straight from the definitions."""
+
+    @staticmethod
+    def _coef(coef, halo, r, i, shift):
+        if i >= 0:
+            return int(coef[r, i])
+        hr = r - 1 if shift else r
+        return int(halo[hr, 4 + i]) if hr >= 0 else 0
+
+    def _wg(self, coef, halo, n1, col0, nc, r, i, shift):
+        def s_at(ii):
+            jg = r * n1 + col0 + ii
+            return sum((self._coef(coef, halo, r, ii - t, shift) >> (16 * t)) & 0xFFFF
+                       for t in range(4) if 0 <= jg - t < nc)
+        sj = s_at(i)
+        sp = s_at(i - 1) if r * n1 + col0 + i > 0 else 0
+        u = (sj & 0xFFFF) + (sp >> 16)
+        return u & 0xFFFF, u >> 16
+
+    @staticmethod
+    def _u(t):
+        return t.numpy().view(np.uint64) if t.element_size() == 8 else t.numpy().view(np.uint32)
+
+    def carry_chunks_halo(self, coef, halo_out):
+        C = self._u(coef)
+        halo_out.copy_(torch.from_numpy(C[:, -4:].copy().view(np.int64)).view(halo_out.dtype))
+        return halo_out
+
+    def carry_chunks_reduce(self, coef, halo, n1, col0, nc, nout, shift, agg):
+        C, H = self._u(coef), self._u(halo)
+        res = []
+        for r in range(C.shape[0]):
+            G, P = 0, 1
+            for i in range(C.shape[1]):
+                if r * n1 + col0 + i >= nout:
+                    continue
+                w, g = self._wg(C, H, n1, col0, nc, r, i, shift)
+                G, P = g | (int(w == 0xFFFF) & G), int(w == 0xFFFF) & P
+            res.append(G | (P << 1))
+        agg.copy_(torch.tensor(res, dtype=torch.int32).view(agg.dtype))
+        return agg
+
+    def carry_chunks_scan(self, agg_all, G, nrows):
+        A = agg_all.numpy().view(np.uint32)
+        carry, out = 0, A.copy()
+        for q in range(G * nrows):
+            at = (q % G) * nrows + q // G
+            out[at] = carry
+            gp = int(A[at])
+            carry = (gp & 1) | ((gp >> 1) & carry)
+        agg_all.copy_(torch.from_numpy(out.view(np.int32)).view(agg_all.dtype))
+        return agg_all
+
+    def carry_chunks_apply(self, coef, halo, n1, col0, nc, nout, shift, cin, out):
+        C, H = self._u(coef), self._u(halo)
+        Ci = cin.numpy().view(np.uint32)
+        O = np.zeros(C.shape, dtype=np.uint16)
+        for r in range(C.shape[0]):
+            carry = int(Ci[r])
+            for i in range(C.shape[1]):
+                if r * n1 + col0 + i >= nout:
+                    continue
+                w, g = self._wg(C, H, n1, col0, nc, r, i, shift)
+                O[r, i] = (w + carry) & 0xFFFF
+                carry = g | (int(w == 0xFFFF) & carry)
+        out.copy_(torch.from_numpy(O.view(np.int16)).view(out.dtype))
+        return out
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -142,3 +234,36 @@ def _worker(rank, world, port, p, g, k, k2, dtype_bits):
 @pytest.mark.parametrize("p,g,k,k2,bits", [(P30, 3, 8, 4, 32), (PG, 7, 9, 4, 64)])
 def test_sharded_ntt_gloo(world, p, g, k, k2, bits):
     mp.spawn(_worker, args=(world, _free_port(), p, g, k, k2, bits), nprocs=world, join=True)
+
+
+def _int_worker(rank, world, port, k, k2, na, nb, all_ones):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1407_3383_b200.dist import ShardedIntMul
+        plan = RefPlan(PG, 7, k, k2)
+        sh = ShardedIntMul(plan, na, nb, backend=RefCarry())
+        if all_ones:
+            a = np.full(na, 0xFFFF, dtype=np.uint16)
+            b = np.full(nb, 0xFFFF, dtype=np.uint16)
+        else:
+            a, b = gen.limbs16(31, 1, na), gen.limbs16(31, 2, nb)
+        out = sh(torch.from_numpy(a.view(np.int16)), torch.from_numpy(b.view(np.int16)))
+        prod = int.from_bytes(a.tobytes(), "little") * int.from_bytes(b.tobytes(), "little")
+        ref = np.frombuffer(prod.to_bytes(2 * (na + nb), "little"), dtype=np.uint16)
+        full = np.zeros(1 << k, dtype=np.uint16)
+        full[:na + nb] = ref
+        idx = sh.limb_indices().numpy()
+        got = out.numpy().view(np.uint16)
+        assert np.array_equal(got, full[idx]), f"rank {rank}: limb block mismatch"
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("na,nb,ones", [(500, 400, False), (512, 512, True), (3, 700, False)])
+def test_sharded_int_mul_gloo(world, na, nb, ones):
+    # the sharded integer product with cross-rank carries
+    mp.spawn(_int_worker, args=(world, _free_port(), 10, 4, na, nb, ones), nprocs=world, join=True)
