@@ -156,6 +156,21 @@ mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void *a, s
                          const void *b, size_t lb, size_t ldb, void *c, size_t ldc, size_t batch, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Polynomial matrix product: C = A B with A
+ * an m x kk and B a kk x n matrix of polynomials over Z/pZ.  A:
+ * [m][kk][da] coefficients, B: [kk][n][db], C: [m][n][da + db - 1] (entries
+ * row-major, coefficients contiguous, all device memory owned by the
+ * caller).  Every entry is transformed once (TFT order, length L =
+ * 2^ceil(log2(da + db - 1)), zero padded), the L pointwise m x kk x n
+ * matrix products over Z/pZ run on the GPU (exact 64-bit sums, one
+ * reduction per entry), and the m n entries of C are transformed back.
+ * 32-bit p < 2^30 with 2^log2(L) | p - 1; g generates (Z/pZ)^*.  The
+ * library owns an (m kk + kk n + m n) L word workspace per stream;
+ * m kk + kk n <= 51200 (MM_E_UNSUPPORTED_SIZE otherwise). */
+mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t *A, const uint32_t *B, uint32_t *C, size_t m,
+                         size_t kk, size_t n, size_t da, size_t db, void *stream);
+
+/* ------------------------------------------------------------------------
  * Integer product (P:971-973 Kronecker segmentation, one
  * prime p = 2^64 - 2^32 + 1, R7): a (na limbs) and b (nb limbs)
  * are little-endian 16-bit limbs; c receives exactly na + nb limbs of a b.

@@ -281,3 +281,23 @@ def int_mul_ntt_u16(a, b, p=GOLDILOCKS, g=7):
 def limbs_mod(a, q):
     a = _u16(a)
     return lib().or_limbs_mod(_p(a), a.size, q)
+
+
+def poly_matmul_naive(A, B, p):
+    """Polynomial matrix product by its definition: C[i][j] =
+    sum_l A[i][l] B[l][j] in (Z/pZ)[x], every entry product a schoolbook
+    product (P:950), sums mod p.  A: [m][kk][da], B: [kk][n][db] residues;
+    returns [m][n][da + db - 1] (uint64)."""
+    A, B = np.asarray(A), np.asarray(B)
+    m, kk, da = A.shape
+    kk2, n, db = B.shape
+    if kk != kk2:
+        raise ValueError("inner dimensions differ")
+    C = np.zeros((m, n, da + db - 1), dtype=np.uint64)
+    for i in range(m):
+        for j in range(n):
+            acc = np.zeros(da + db - 1, dtype=np.uint64)
+            for l in range(kk):
+                acc = vec_addmod(acc, poly_mul_schoolbook(A[i, l], B[l, j], p), p)
+            C[i, j] = acc
+    return C

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -48,6 +48,7 @@ EXPORTS = {
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_poly_matmul": (_ST, [_u64, _u64, _P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
     "mm_int_mul_u32": (_ST, [_P, _sz, _P, _sz, _P, _P]),
     "mm_poly_mul_host": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_mul_ld": (_ST, [_i32, _u64, _u64, _P, _sz, _sz, _P, _sz, _sz, _P, _sz, _sz, _P]),
@@ -343,6 +344,19 @@ def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | 
     _check(lib().mm_poly_mul_ld(word_bits, int(p), int(g), _ptr_rows(a2), la, lda, _ptr_rows(b2), lb, ldb,
                                 _ptr_rows(o2), ldc, batch, _stream(a)))
     return out if a.dim() > 1 else out.reshape(-1)
+
+
+def poly_matmul(A: torch.Tensor, B: torch.Tensor, p: int, g: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Polynomial matrix product mod p (mm_poly_matmul):
+    A [m, kk, da], B [kk, n, db] (uint32 residues) -> C [m, n, da + db - 1]."""
+    if A.dim() != 3 or B.dim() != 3 or A.shape[1] != B.shape[0]:
+        raise ValueError("expected A [m, kk, da] and B [kk, n, db]")
+    m, kk, da = A.shape
+    n, db = B.shape[1], B.shape[2]
+    if out is None:
+        out = torch.empty((m, n, da + db - 1), dtype=A.dtype, device=A.device)
+    _check(lib().mm_poly_matmul(int(p), int(g), _ptr(A), _ptr(B), _ptr(out), m, kk, n, da, db, _stream(A)))
+    return out
 
 
 def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.Tensor | None = None,

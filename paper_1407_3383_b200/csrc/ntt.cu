@@ -385,6 +385,49 @@ __global__ void __launch_bounds__(256) k_chunk_apply(ChunkRef R, const uint32_t*
     }
 }
 
+// ---------------------------------------------------------------- polynomial matrix product
+// At every evaluation point f < L: Chat_f = Ahat_f Bhat_f, an (m x kk) (kk x n)
+// product over Z/pZ.  A CTA owns FB consecutive points and stages the
+// matching slices of Ahat [m kk][L] and Bhat [kk n][L] in shared memory as
+// [f][row][col]; each output sums kk products of values < 2^32 exactly in 64
+// bits plus a carry count, reduced once: (carry 2^64 + lo) mod p.
+__global__ void __launch_bounds__(256) k_point_matmul(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+                                                      uint32_t* __restrict__ C, int m, int kk, int n, long long L,
+                                                      int FB, uint32_t p, uint64_t r64) {
+    extern __shared__ uint32_t sm[];
+    const int sa = m * kk, sb = kk * n;
+    uint32_t* SA = sm;                        // [FB][m][kk]
+    uint32_t* SB = sm + (size_t)FB * sa;      // [FB][kk][n]
+    for (long long f0 = (long long)blockIdx.x * FB; f0 < L; f0 += (long long)gridDim.x * FB) {
+        const int nf = (int)(L - f0 < FB ? L - f0 : FB);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nf * sa; e += blockDim.x) {
+            const int f = e % nf, rc = e / nf;          // consecutive threads: consecutive points
+            SA[f * sa + rc] = A[(long long)rc * L + f0 + f];
+        }
+        for (int e = threadIdx.x; e < nf * sb; e += blockDim.x) {
+            const int f = e % nf, rc = e / nf;
+            SB[f * sb + rc] = B[(long long)rc * L + f0 + f];
+        }
+        __syncthreads();
+        const int no = nf * m * n;
+        for (int o = threadIdx.x; o < no; o += blockDim.x) {
+            const int j = o % n, i = (o / n) % m, f = o / (m * n);
+            const uint32_t* a = SA + f * sa + i * kk;
+            const uint32_t* b = SB + f * sb + j;
+            uint64_t lo = 0;
+            uint32_t cy = 0;
+            for (int l = 0; l < kk; l++) {
+                const uint64_t t = (uint64_t)a[l] * b[l * n];
+                lo += t;
+                cy += lo < t;
+            }
+            const uint64_t r = (lo % p + (uint64_t)cy * r64) % p;
+            C[(long long)(i * n + j) * L + f0 + f] = (uint32_t)r;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- three-prime integer product
 // p1 = 998244353, p2 = 985661441, p3 = 943718401, 32-bit chunks (h = 32).
 struct Crt3 {
@@ -776,6 +819,105 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     c.in_rs = c.out_rs = 1ll << P->k1;
     c.in_bs = c.out_bs = n;
     c.in_len = c.out_len = n;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.scale = 1; c.sc = sc; c.canon = 1;
+    c.lvl = (const W*)P->lvl_i2;
+    return launch_cols<F, true, T, T>(f, c, st);
+}
+
+// ---- forward with zero-padded input rows / inverse with truncated output rows ----------
+// rows: `rows` transforms; input row r at in + r in_rs with in_len valid elements
+// (zeros beyond); output BITREV rows of n (canonical).
+template <class F>
+static mm_status fwd_pad_impl(mm_ntt_plan* P, const void* in, long long rows, long long in_rs, long long in_len,
+                              void* out, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    const long long n = 1ll << P->k;
+    if (P->k2 == 0) {
+        RowArgs<F> a{};
+        a.in = in; a.out = out;
+        a.nrows = rows;
+        a.in_rs = in_rs; a.out_rs = n;
+        a.in_len = in_len; a.out_len = n;
+        a.k = P->k;
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_f1;
+        return launch_rows<F, false, T, T>(f, a, st);
+    }
+    ColArgs<F> c{};
+    c.in = in; c.out = out;
+    c.ncols = 1ll << P->k1;
+    c.nbatch = rows;
+    c.in_rs = c.out_rs = 1ll << P->k1;
+    c.in_bs = in_rs; c.out_bs = n;
+    c.in_len = in_len; c.out_len = n;
+    c.n1 = 1ll << P->k1;
+    c.k = P->k2;
+    c.fs = 1;
+    c.lvl = (const W*)P->lvl_f2;
+    c.fs_lo = (const W*)P->fs_lo_f;
+    c.fs_hi = (const W*)P->fs_hi_f;
+    c.fs_full = (const W*)P->fs_full_f;
+    c.fs_h = P->fs_h;
+    mm_status s = launch_cols<F, false, T, T>(f, c, st);
+    if (s != MM_OK) return s;
+    RowArgs<F> a{};
+    a.in = out; a.out = out;
+    a.nrows = rows << P->k2;
+    a.in_rs = a.out_rs = 1ll << P->k1;
+    a.in_len = a.out_len = 1ll << P->k1;
+    a.k = P->k1;
+    a.canon = 1;
+    a.lvl = (const W*)P->lvl_f1;
+    return launch_rows<F, false, T, T>(f, a, st);
+}
+// BITREV input rows of n (in place allowed for the row pass: `in` is overwritten
+// on the four-step path); output row r at out + r out_rs, first out_len
+// coefficients, times n^-1, canonical.
+template <class F>
+static mm_status inv_trunc_impl(mm_ntt_plan* P, void* in, long long rows, void* out, long long out_rs,
+                                long long out_len, cudaStream_t st) {
+    typedef typename F::T T;
+    typedef typename F::W W;
+    F f = make_field<F>(P);
+    const long long n = 1ll << P->k;
+    W sc = host_w<W>(P->ninv, P->p);
+    if (P->k2 == 0) {
+        RowArgs<F> a{};
+        a.in = in; a.out = out;
+        a.nrows = rows;
+        a.in_rs = n; a.out_rs = out_rs;
+        a.in_len = n; a.out_len = out_len;
+        a.k = P->k;
+        a.scale = 1; a.sc = sc;
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_i1;
+        return launch_rows<F, true, T, T>(f, a, st);
+    }
+    RowArgs<F> a{};
+    a.in = in; a.out = in;
+    a.nrows = rows << P->k2;
+    a.in_rs = a.out_rs = 1ll << P->k1;
+    a.in_len = a.out_len = 1ll << P->k1;
+    a.k = P->k1;
+    a.fs = 1; a.k2 = P->k2; a.row0 = 0;
+    a.lvl = (const W*)P->lvl_i1;
+    a.fs_lo = (const W*)P->fs_lo_i;
+    a.fs_hi = (const W*)P->fs_hi_i;
+    a.fs_full = (const W*)P->fs_full_i;
+    a.fs_h = P->fs_h;
+    mm_status s = launch_rows<F, true, T, T>(f, a, st);
+    if (s != MM_OK) return s;
+    ColArgs<F> c{};
+    c.in = in; c.out = out;
+    c.ncols = 1ll << P->k1;
+    c.nbatch = rows;
+    c.in_rs = c.out_rs = 1ll << P->k1;
+    c.in_bs = n; c.out_bs = out_rs;
+    c.in_len = n; c.out_len = out_len;
     c.n1 = 1ll << P->k1;
     c.k = P->k2;
     c.scale = 1; c.sc = sc; c.canon = 1;
@@ -1532,4 +1674,50 @@ extern "C" mm_status mm_carry_chunks_apply(const uint64_t* coef, const uint64_t*
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
+}
+
+// Polynomial matrix product: C = A B for an m x kk matrix A and a
+// kk x n matrix B of polynomials over Z/pZ (entries of A: da coefficients,
+// of B: db), C entries have da + db - 1 coefficients.  Every entry is
+// transformed once (length L = 2^ceil(log2(da + db - 1)), zero padded), the
+// L pointwise matrix products run over Z/pZ, the m n entries of C are
+// transformed back.  32-bit p < 2^30 with 2^log2(L) | p - 1.
+extern "C" mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t* A, const uint32_t* B, uint32_t* C,
+                                    size_t m, size_t kk, size_t n, size_t da, size_t db, void* stream) {
+    if (!A || !B || !C) return set_err(MM_E_ARG, "null argument");
+    if (m == 0 || kk == 0 || n == 0 || da == 0 || db == 0) return set_err(MM_E_ARG, "empty operands");
+    const size_t lc = da + db - 1;
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k == 0) k = 1;
+    mm_status s = check_modulus(32, p, k);
+    if (s != MM_OK) return s;
+    const long long L = 1ll << k;
+    const size_t words = (size_t)(m * kk + kk * n) * 1;   // per evaluation point in shared memory
+    const size_t smem_cap = 200 * 1024 / 4;
+    if (words > smem_cap) return set_err(MM_E_UNSUPPORTED_SIZE, "m kk + kk n = %zu exceeds %zu", words, smem_cap);
+    int FB = (int)(smem_cap / words);
+    if (FB > 32) FB = 32;
+    uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
+    mm_ntt_plan* P = nullptr;
+    if ((s = cached_plan(32, p, k, omega, &P)) != MM_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    void* ws = nullptr;
+    if ((s = stream_ws2(st, (size_t)(m * kk + kk * n + m * n) * L * 4, &ws)) != MM_OK) return s;
+    uint32_t* Ah = (uint32_t*)ws;
+    uint32_t* Bh = Ah + m * kk * L;
+    uint32_t* Ch = Bh + kk * n * L;
+    if ((s = fwd_pad_impl<Fp32>(P, A, (long long)(m * kk), (long long)da, (long long)da, Ah, st)) != MM_OK) return s;
+    if ((s = fwd_pad_impl<Fp32>(P, B, (long long)(kk * n), (long long)db, (long long)db, Bh, st)) != MM_OK) return s;
+    const size_t smem = (size_t)FB * words * 4;
+    MM_CUDA_TRY(cudaFuncSetAttribute(k_point_matmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long tiles = (L + FB - 1) / FB;
+    const int grid = (int)(tiles < num_sms() * 4 ? tiles : num_sms() * 4);
+    const uint64_t r64 = (uint64_t)(((u128)1 << 64) % p);
+    {
+        LaunchScope ls("point_matmul", st);
+        k_point_matmul<<<grid, 256, smem, st>>>(Ah, Bh, Ch, (int)m, (int)kk, (int)n, L, FB, (uint32_t)p, r64);
+    }
+    MM_LAUNCH_CHECK();
+    return inv_trunc_impl<Fp32>(P, Ch, (long long)(m * n), C, (long long)lc, (long long)lc, st);
 }

@@ -325,6 +325,41 @@ def test_poly_mul_c3_full_sampled(mm, O):
         assert np.array_equal(u64(ch[r]), O.poly_mul_ntt(ah[r], bh[r], p, g)), r
 
 
+# ------------------------------------------------------------------ polynomial matrix product
+@pytest.mark.parametrize("m,kk,n,da,db,p,g", [(3, 3, 3, 8, 8, 469762049, 3), (1, 1, 1, 1, 1, P30, 3),
+                                              (4, 5, 3, 100, 37, P30, 3), (2, 3, 2, 3000, 2000, 469762049, 3),
+                                              (5, 2, 7, 33, 1, P30, 3)])
+def test_poly_matmul(mm, O, m, kk, n, da, db, p, g):
+    # P:962-969 vs the naive matrix of schoolbook products (single-pass and four-step sizes)
+    A = residues(m * 100 + da, 1, m * kk * da, p).reshape(m, kk, da)
+    B = residues(n * 100 + db, 2, kk * n * db, p).reshape(kk, n, db)
+    C = u64(host(mm.poly_matmul(dev(A), dev(B), p, g)))
+    assert np.array_equal(C, O.poly_matmul_naive(A, B, p))
+
+
+def test_poly_matmul_table15_sampled(mm, O):
+    # Table 15 shape: 32 x 32 matrices, degrees < 2^15 over 469762049; every entry
+    # checked by evaluation at a random point (C(r) = A(r) B(r) as matrices over Z/pZ)
+    p, g, N, d = 469762049, 3, 32, 1 << 15
+    A = gen.residues_torch(15, 1, N * N * d, p, DEV).view(torch.uint32).reshape(N, N, d)
+    B = gen.residues_torch(15, 2, N * N * d, p, DEV).view(torch.uint32).reshape(N, N, d)
+    C = host(mm.poly_matmul(A, B, p, g))
+    Ah, Bh = host(A), host(B)
+    rng = random.Random(15)
+    r = rng.randrange(1, p)
+    Ar = np.array([[O.poly_eval(Ah[i, l], r, p) for l in range(N)] for i in range(N)], dtype=object)
+    Br = np.array([[O.poly_eval(Bh[l, j], r, p) for j in range(N)] for l in range(N)], dtype=object)
+    ref = (Ar @ Br) % p
+    for i in range(0, N, 5):
+        for j in range(N):
+            assert O.poly_eval(C[i, j], r, p) == ref[i, j], (i, j)
+    # one entry in full: sum of 32 oracle products (the oracle's NTT product, pinned)
+    acc = np.zeros(2 * d - 1, dtype=np.uint64)
+    for l in range(N):
+        acc = O.vec_addmod(acc, O.poly_mul_ntt(Ah[0, l], Bh[l, 0], p, g), p)
+    assert np.array_equal(u64(C[0, 0]), acc)
+
+
 # ------------------------------------------------------------------ int_mul
 def _to_int(limbs):
     return int.from_bytes(np.asarray(limbs, dtype="<u2").tobytes(), "little")

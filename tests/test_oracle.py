@@ -433,3 +433,38 @@ def test_carry_u16(O):
     coef = [rng.randrange(1 << 56) for _ in range(100)]
     out = O.carry_u16(np.array(coef, dtype=np.uint64), 104)
     assert _to_int(out) == sum(c << (16 * i) for i, c in enumerate(coef))
+
+
+# ------------------------------------------------------------------ polynomial matrix product
+def test_poly_matmul_naive_pins(O):
+    p = 469762049                       # Table 15's prime
+    rng = np.random.default_rng(15)
+    # degree 0: the ordinary matrix product over Z/pZ (numpy object integers)
+    A = rng.integers(0, p, size=(3, 4, 1), dtype=np.uint64)
+    B = rng.integers(0, p, size=(4, 2, 1), dtype=np.uint64)
+    ref = (A[:, :, 0].astype(object) @ B[:, :, 0].astype(object)) % p
+    assert np.array_equal(O.poly_matmul_naive(A, B, p)[:, :, 0].astype(object), ref)
+    # identity polynomial matrix x B = B (SPEC poly_mat_mul example)
+    I = np.zeros((3, 3, 1), dtype=np.uint64)
+    for i in range(3):
+        I[i, i, 0] = 1
+    B = rng.integers(0, p, size=(3, 3, 8), dtype=np.uint64)
+    assert np.array_equal(O.poly_matmul_naive(I, B, p), B)
+    # entries against Python polynomial arithmetic (x-adic evaluation at 2^64)
+    A = rng.integers(0, p, size=(2, 3, 5), dtype=np.uint64)
+    B = rng.integers(0, p, size=(3, 2, 4), dtype=np.uint64)
+    C = O.poly_matmul_naive(A, B, p)
+    for i in range(2):
+        for j in range(2):
+            coef = [0] * 8
+            for l in range(3):
+                for u in range(5):
+                    for v in range(4):
+                        coef[u + v] += int(A[i, l, u]) * int(B[l, j, v])
+            assert [int(c) for c in C[i, j]] == [c % p for c in coef]
+    # associativity (SPEC property)
+    X = rng.integers(0, p, size=(2, 2, 3), dtype=np.uint64)
+    Y = rng.integers(0, p, size=(2, 2, 2), dtype=np.uint64)
+    Z = rng.integers(0, p, size=(2, 2, 2), dtype=np.uint64)
+    assert np.array_equal(O.poly_matmul_naive(O.poly_matmul_naive(X, Y, p), Z, p),
+                          O.poly_matmul_naive(X, O.poly_matmul_naive(Y, Z, p), p))
