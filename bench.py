@@ -397,6 +397,19 @@ def extras_run(mm, torch, dev, peaks):
     out["poly_matmul_d2^15_p469762049"] = dict(pm, note="paper Table 15 (one i7-4770 core, context only): "
                                                         "n = 8: 0.15 s, n = 32: 4.7 s")
 
+    # integer matrix product (Table 17: n x n, entries of 32 x 2^15 bits)
+    im = {}
+    for N in (8, 32):
+        nl = 1 << 15
+        A = gen.limbs16_torch(17, 1, 2 * N * N * nl, dev).view(torch.uint32).reshape(N, N, nl)
+        B = gen.limbs16_torch(17, 2, 2 * N * N * nl, dev).view(torch.uint32).reshape(N, N, nl)
+        Cm = torch.empty((N, N, 2 * nl + 1), dtype=torch.uint32, device=dev)
+        msi = tloop(lambda: mm.int_matmul_u32(A, B, out=Cm), 3)
+        im[f"n{N}"] = {"ms": round(msi, 3)}
+        del A, B, Cm
+    out["int_matmul_32x2^15bit"] = dict(im, note="paper Table 17 (one i7-4770 core, context only): "
+                                                 "n = 8: 0.44 s, n = 32: 13 s")
+
     # the paper's three-prime integer product at
     # Table 16's largest size, 32 x 2^20-bit operands, beside the Goldilocks path
     n32 = 1 << 20

@@ -190,6 +190,15 @@ mm_status mm_int_mul_u16(const uint16_t *a, size_t na, const uint16_t *b, size_t
  * so na + nb - 1 <= 2^22 (MM_E_SIZE_OVERFLOW otherwise).  Device pointers,
  * c must not alias a or b; the library owns its workspace (per stream). */
 mm_status mm_int_mul_u32(const uint32_t *a, size_t na, const uint32_t *b, size_t nb, uint32_t *c, void *stream);
+/* Integer matrix product (Table 17): C = A B for an m x kk and a
+ * kk x n matrix of integers in 32-bit little-endian limbs (A: [m][kk][na],
+ * B: [kk][n][nb], C: [m][n][na + nb + 1] -- an entry is a sum of kk
+ * products, so it takes one limb more than a product; device memory).  The three-prime
+ * method of mm_int_mul_u32 with the pointwise stage a matrix product over
+ * each prime (mm_poly_matmul), Garner CRT, carries.  Needs na + nb - 1 <=
+ * 2^22 and kk min(na, nb) (2^32 - 1)^2 < p1 p2 p3 (MM_E_SIZE_OVERFLOW). */
+mm_status mm_int_matmul_u32(const uint32_t *A, const uint32_t *B, uint32_t *C, size_t m, size_t kk, size_t n,
+                            size_t na, size_t nb, void *stream);
 
 /* ------------------------------------------------------------------------
  * Four-step building blocks for the distributed transform (SURVEY a6/a7,

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -49,6 +49,7 @@ EXPORTS = {
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_matmul": (_ST, [_u64, _u64, _P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
+    "mm_int_matmul_u32": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
     "mm_int_mul_u32": (_ST, [_P, _sz, _P, _sz, _P, _P]),
     "mm_poly_mul_host": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_mul_ld": (_ST, [_i32, _u64, _u64, _P, _sz, _sz, _P, _sz, _sz, _P, _sz, _sz, _P]),
@@ -405,6 +406,19 @@ def carry_chunks_scan(agg_all, G, nrows):
 def carry_chunks_apply(coef, halo, n1, col0, nc, nout, shift, cin, out):
     _check(lib().mm_carry_chunks_apply(_ptr(coef), _ptr(halo), coef.shape[0], coef.shape[1], n1, col0, nc, nout,
                                        int(shift), _ptr(cin), _ptr(out), _stream(coef)))
+    return out
+
+
+def int_matmul_u32(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Integer matrix product (mm_int_matmul_u32): A [m, kk, na],
+    B [kk, n, nb] 32-bit limbs -> C [m, n, na + nb + 1]."""
+    if A.dim() != 3 or B.dim() != 3 or A.shape[1] != B.shape[0]:
+        raise ValueError("expected A [m, kk, na] and B [kk, n, nb]")
+    m, kk, na = A.shape
+    n, nb = B.shape[1], B.shape[2]
+    if out is None:
+        out = torch.empty((m, n, na + nb + 1), dtype=A.dtype, device=A.device)
+    _check(lib().mm_int_matmul_u32(_ptr(A), _ptr(B), _ptr(out), m, kk, n, na, nb, _stream(A)))
     return out
 
 

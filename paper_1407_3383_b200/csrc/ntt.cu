@@ -141,6 +141,26 @@ struct Dig32x3 {
         return s;
     }
 };
+// many independent products back to back: entry e owns limbs [e nout, (e+1) nout)
+// and coefficients w[3 (e nc + k) ..], k < nc; digit sums never cross entries
+// (each entry's value fits its nout limbs, so its carry out is 0).
+struct Dig32x3Batch {
+    typedef uint32_t Out;
+    enum { W = 32 };
+    const uint32_t* w;
+    long long nc, nout;
+    __device__ __forceinline__ uint64_t s_at(long long j) const {
+        const long long e = j / nout, jl = j - e * nout;
+        const uint32_t* we = w + 3 * e * nc;
+        uint64_t s = 0;
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            long long k = jl - t;
+            if (k >= 0 && k < nc) s += we[3 * k + t];
+        }
+        return s;
+    }
+};
 template <class D>
 __device__ __forceinline__ void carry_gp(const D& d, long long j, uint32_t& w, uint32_t& g) {
     constexpr uint64_t M = (D::W == 32) ? 0xFFFFFFFFull : ((1ull << D::W) - 1);
@@ -1040,13 +1060,23 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
     return MM_OK;
 }
 
-// a second per-stream workspace for drivers that call product_impl (which owns the first)
-static std::map<WsKey, std::pair<void*, size_t>> g_ws2;
-static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) {
+// further per-stream workspaces for drivers that call product_impl (which owns
+// the first): slot 1 for int_mul_u32 / poly_matmul, slot 2 for int_matmul
+struct WsSlotKey {
+    int dev, slot;
+    cudaStream_t st;
+    bool operator<(const WsSlotKey& o) const {
+        if (dev != o.dev) return dev < o.dev;
+        if (slot != o.slot) return slot < o.slot;
+        return st < o.st;
+    }
+};
+static std::map<WsSlotKey, std::pair<void*, size_t>> g_ws_slots;
+static mm_status stream_ws_slot(cudaStream_t st, int slot, size_t bytes, void** out) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(g_cache_mu);
-    auto& e = g_ws2[WsKey{dev, st}];
+    auto& e = g_ws_slots[WsSlotKey{dev, slot, st}];
     if (e.second < bytes) {
         if (e.first) {
             MM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1060,6 +1090,7 @@ static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) {
     *out = e.first;
     return MM_OK;
 }
+static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) { return stream_ws_slot(st, 1, bytes, out); }
 
 // n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
 static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, long long lda, const uint32_t* b,
@@ -1441,6 +1472,7 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
 // reduce -> scan -> apply over nout output digits; agg: one word per CARRY_B digits
 template <class D>
 static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D::Out* out, cudaStream_t st) {
+    // digit-sum lookbehind at position j: j - 1 (carry_gp) -- every policy handles j = 0
     const long long nblk = (nout + CARRY_B - 1) / CARRY_B;
     {
         LaunchScope ls("carry_reduce", st);
@@ -1720,4 +1752,58 @@ extern "C" mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t* A, c
     }
     MM_LAUNCH_CHECK();
     return inv_trunc_impl<Fp32>(P, Ch, (long long)(m * n), C, (long long)lc, (long long)lc, st);
+}
+
+// Integer matrix product (Table 17): C = A B
+// for matrices of integers given as 32-bit limbs (entries of A: na limbs,
+// of B: nb limbs; C entries na + nb limbs) -- the three-prime FFT product of
+// mm_int_mul_u32 with the pointwise stage a matrix product (mm_poly_matmul
+// per prime), then Garner CRT and one batched carry chain.  C entries have
+// na + nb + 1 limbs (a sum of kk <= 2^32 products).
+extern "C" mm_status mm_int_matmul_u32(const uint32_t* A, const uint32_t* B, uint32_t* C, size_t m, size_t kk, size_t n,
+                                       size_t na, size_t nb, void* stream) {
+    if (!A || !B || !C) return set_err(MM_E_ARG, "null argument");
+    if (m == 0 || kk == 0 || n == 0 || na == 0 || nb == 0) return set_err(MM_E_ARG, "empty operands");
+    // an entry is a sum of kk products, < kk 2^(32 (na + nb)): one more limb than a product
+    const size_t lc = na + nb - 1, nout = na + nb + 1;
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k > 22) return set_err(MM_E_SIZE_OVERFLOW, "na + nb - 1 > 2^22 (three-prime transform limit)");
+    // every coefficient of an entry <= kk min(na, nb) (2^32 - 1)^2 < p1 p2 p3
+    if ((double)kk * (double)(na < nb ? na : nb) >= 3.3e7)
+        return set_err(MM_E_SIZE_OVERFLOW, "kk min(na, nb) too large for three 30-bit primes");
+    static const uint32_t PR[3] = {998244353u, 985661441u, 943718401u}, GEN[3] = {3, 3, 7};
+    Crt3 K;
+    K.p1 = PR[0]; K.p2 = PR[1]; K.p3 = PR[2];
+    K.i12 = (uint32_t)hpowmod(PR[0] % PR[1], PR[1] - 2, PR[1]);
+    K.i13 = (uint32_t)hpowmod(PR[0] % PR[2], PR[2] - 2, PR[2]);
+    K.i23 = (uint32_t)hpowmod(PR[1] % PR[2], PR[2] - 2, PR[2]);
+    K.p12 = (uint64_t)PR[0] * PR[1];
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t sa = m * kk * na, sb = kk * n * nb, sc = m * n * lc;
+    const size_t nall = m * n * nout, nblk = (nall + CARRY_B - 1) / CARRY_B;
+    void* ws = nullptr;
+    mm_status s = stream_ws_slot(st, 2, (3 * (sa + sb) + 3 * sc + 3 * sc + nblk + 64) * 4, &ws);
+    if (s != MM_OK) return s;
+    uint32_t* RA = (uint32_t*)ws;           // [3][sa]
+    uint32_t* RB = RA + 3 * sa;             // [3][sb]
+    uint32_t* RC = RB + 3 * sb;             // [3][sc]
+    uint32_t* Wd = RC + 3 * sc;             // [sc][3]
+    uint32_t* agg = Wd + 3 * sc;
+    const int grid = num_sms() * 8;
+    {
+        LaunchScope ls("crt_residues", st);
+        k_residues3<<<grid, 256, 0, st>>>(A, (long long)sa, RA, (long long)sa, K);
+        k_residues3<<<grid, 256, 0, st>>>(B, (long long)sb, RB, (long long)sb, K);
+    }
+    MM_LAUNCH_CHECK();
+    for (int i = 0; i < 3; i++)
+        if ((s = mm_poly_matmul(PR[i], GEN[i], RA + i * sa, RB + i * sb, RC + i * sc, m, kk, n, na, nb, stream)) != MM_OK)
+            return s;
+    {
+        LaunchScope ls("crt_garner", st);
+        k_crt3<<<grid, 256, 0, st>>>(RC, (long long)sc, (long long)sc, Wd, K);
+    }
+    MM_LAUNCH_CHECK();
+    return carry_run(Dig32x3Batch{Wd, (long long)lc, (long long)nout}, (long long)nall, agg, C, st);
 }

@@ -383,6 +383,24 @@ def test_int_mul_u32_three_prime(mm, O, na, nb):
     assert _to_int32(c) == _to_int32(a) * _to_int32(b)
 
 
+@pytest.mark.parametrize("m,kk,n,na,nb", [(2, 2, 2, 3, 3), (3, 4, 2, 100, 50), (1, 1, 1, 1, 1), (2, 3, 4, 2000, 3000)])
+def test_int_matmul_u32(mm, O, m, kk, n, na, nb):
+    # P:981-989 vs Python integers: C_ij = sum_l A_il B_lj
+    A = np.stack([_limbs32(1000 * i + na, na) for i in range(m * kk)]).reshape(m, kk, na)
+    B = np.stack([_limbs32(2000 * i + nb, nb) for i in range(kk * n)]).reshape(kk, n, nb)
+    C = host(mm.int_matmul_u32(dev(A), dev(B)))
+    for i in range(m):
+        for j in range(n):
+            ref = sum(_to_int32(A[i, l]) * _to_int32(B[l, j]) for l in range(kk))
+            assert _to_int32(C[i, j]) == ref, (i, j)
+    # all limbs 0xFFFFFFFF: every coefficient at kk min(na,nb) (2^32-1)^2
+    A = np.full((m, kk, na), 0xFFFFFFFF, dtype=np.uint32)
+    B = np.full((kk, n, nb), 0xFFFFFFFF, dtype=np.uint32)
+    C = host(mm.int_matmul_u32(dev(A), dev(B)))
+    ref = kk * ((1 << (32 * na)) - 1) * ((1 << (32 * nb)) - 1)
+    assert all(_to_int32(C[i, j]) == ref for i in range(m) for j in range(n))
+
+
 @pytest.mark.parametrize("N", [1, 2, 4097, 1 << 16])
 def test_int_mul_u32_all_ones(mm, O, N):
     # (2^(32N) - 1)^2: every coefficient at its maximum N (2^32 - 1)^2 (closed form)
