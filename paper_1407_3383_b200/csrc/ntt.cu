@@ -409,41 +409,196 @@ __global__ void __launch_bounds__(256) k_chunk_apply(ChunkRef R, const uint32_t*
 // At every evaluation point f < L: Chat_f = Ahat_f Bhat_f, an (m x kk) (kk x n)
 // product over Z/pZ.  A CTA owns FB consecutive points and stages the
 // matching slices of Ahat [m kk][L] and Bhat [kk n][L] in shared memory as
-// [f][row][col]; each output sums kk products of values < 2^32 exactly in 64
-// bits plus a carry count, reduced once: (carry 2^64 + lo) mod p.
-__global__ void __launch_bounds__(256) k_point_matmul(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
+// [f][row][col]; each output sums kk products of residues exactly (64-bit
+// accumulators, high words folded every 16 terms), reduced once.
+// 4 x 4 register blocks: a thread owns C[i0..i0+3][j0..j0+3] at one point and
+// loads 4 + 4 shared values per 16 products.
+// 4-byte global -> shared copy that does not block the issuing thread (LDGSTS):
+// the staging loops issue all their loads back to back
+__device__ __forceinline__ void cp_async4s(uint32_t* dst, const uint32_t* src) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+// v mod p for any v < 2^64 by Barrett with mu = floor(2^64 / p): q = hi(v mu)
+// underestimates floor(v / p) by at most 2 (p < 2^31)
+__device__ __forceinline__ uint32_t mod64_barrett(uint64_t v, uint32_t p, uint64_t mu) {
+    const uint64_t q = __umul64hi(v, mu);
+    uint64_t r = v - q * p;
+    r = r >= p ? r - p : r;
+    r = r >= p ? r - p : r;
+    return (uint32_t)r;
+}
+// (hi 2^32 + lo) mod p, hi < 2^64, lo < 2^32
+__device__ __forceinline__ uint32_t mod96_barrett(uint64_t hi, uint64_t lo, uint32_t p, uint64_t mu) {
+    const uint64_t t = mod64_barrett(hi, p, mu);
+    return mod64_barrett((t << 32) | lo, p, mu);
+}
+__global__ void __launch_bounds__(256) k_point_matmul_any(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
                                                       uint32_t* __restrict__ C, int m, int kk, int n, long long L,
                                                       int FB, uint32_t p, uint64_t r64) {
     extern __shared__ uint32_t sm[];
     const int sa = m * kk, sb = kk * n;
     uint32_t* SA = sm;                        // [FB][m][kk]
     uint32_t* SB = sm + (size_t)FB * sa;      // [FB][kk][n]
+    const int mb = (m + 3) >> 2, nb = (n + 3) >> 2;
     for (long long f0 = (long long)blockIdx.x * FB; f0 < L; f0 += (long long)gridDim.x * FB) {
         const int nf = (int)(L - f0 < FB ? L - f0 : FB);
         __syncthreads();
         for (int e = threadIdx.x; e < nf * sa; e += blockDim.x) {
             const int f = e % nf, rc = e / nf;          // consecutive threads: consecutive points
-            SA[f * sa + rc] = A[(long long)rc * L + f0 + f];
+            cp_async4s(SA + f * sa + rc, A + (long long)rc * L + f0 + f);
         }
         for (int e = threadIdx.x; e < nf * sb; e += blockDim.x) {
             const int f = e % nf, rc = e / nf;
-            SB[f * sb + rc] = B[(long long)rc * L + f0 + f];
+            cp_async4s(SB + f * sb + rc, B + (long long)rc * L + f0 + f);
         }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
-        const int no = nf * m * n;
-        for (int o = threadIdx.x; o < no; o += blockDim.x) {
-            const int j = o % n, i = (o / n) % m, f = o / (m * n);
-            const uint32_t* a = SA + f * sa + i * kk;
-            const uint32_t* b = SB + f * sb + j;
-            uint64_t lo = 0;
-            uint32_t cy = 0;
-            for (int l = 0; l < kk; l++) {
-                const uint64_t t = (uint64_t)a[l] * b[l * n];
-                lo += t;
-                cy += lo < t;
+        const int nblk = nf * mb * nb;
+        for (int o = threadIdx.x; o < nblk; o += blockDim.x) {
+            const int jb = o % nb, ib = (o / nb) % mb, f = o / (mb * nb);
+            const int i0 = ib * 4, j0 = jb * 4;
+            const uint32_t* a = SA + f * sa;
+            const uint32_t* bb = SB + f * sb;
+            // products < 2^60 (residues < p < 2^30): 16 of them fit a u64 on top of a
+            // value < 2^32, so every 16 terms the high word moves to hi (IMAD.WIDE.U32
+            // accumulates in 64 bits in one instruction)
+            uint64_t acc[4][4], hi[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) { acc[u][v] = 0; hi[u][v] = 0; }
+            const uint32_t* ar[4];
+            bool rv[4], cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                rv[u] = i0 + u < m;
+                cv[u] = j0 + u < n;
+                ar[u] = a + (rv[u] ? i0 + u : 0) * kk;
             }
-            const uint64_t r = (lo % p + (uint64_t)cy * r64) % p;
-            C[(long long)(i * n + j) * L + f0 + f] = (uint32_t)r;
+            const int jc = j0 + 3 < n ? j0 : 0;
+            for (int l0 = 0; l0 < kk; l0 += 16) {
+                const int le = kk - l0 < 16 ? kk - l0 : 16;
+                for (int l = l0; l < l0 + le; l++) {
+                    uint32_t x[4], y[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) x[u] = rv[u] ? ar[u][l] : 0u;
+                    if (j0 + 3 < n) {
+#pragma unroll
+                        for (int v = 0; v < 4; v++) y[v] = bb[l * n + jc + v];
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < 4; v++) y[v] = cv[v] ? bb[l * n + j0 + v] : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+#pragma unroll
+                        for (int v = 0; v < 4; v++) acc[u][v] += (uint64_t)x[u] * y[v];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        hi[u][v] += acc[u][v] >> 32;
+                        acc[u][v] &= 0xFFFFFFFFull;
+                    }
+            }
+            const uint64_t r32 = (uint64_t)(((uint64_t)1 << 32) % p);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++)
+                    if (rv[u] && cv[v])
+                        C[(long long)((i0 + u) * n + j0 + v) * L + f0 + f] =
+                            (uint32_t)(((hi[u][v] % p) * r32 + acc[u][v]) % p);
+        }
+    }
+}
+
+// [R][Cn] -> [Cn][R] u32 transpose through 32 x 33 shared tiles (coalesced both
+// ways).  With rm > 0 the R input rows are an rm x rk matrix (row i rk + l) and
+// land at output column l rm + i (its transpose), else at column r.
+__global__ void __launch_bounds__(256) k_transpose32(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                     long long R, long long Cn, int rm = 0, int rk = 1) {
+    __shared__ uint32_t t[32][33];
+    const long long tiles_c = (Cn + 31) / 32, tiles = ((R + 31) / 32) * tiles_c;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (long long b = blockIdx.x; b < tiles; b += gridDim.x) {
+        const long long r0 = (b / tiles_c) * 32, c0 = (b % tiles_c) * 32;
+        for (int y = ty; y < 32; y += 8)
+            if (r0 + y < R && c0 + tx < Cn) t[y][tx] = in[(r0 + y) * Cn + c0 + tx];
+        __syncthreads();
+        long long oc = r0 + tx;
+        if (rm > 0 && oc < R) {
+            const long long i = oc / rk, l = oc - i * rk;
+            oc = l * rm + i;
+        }
+        for (int y = ty; y < 32; y += 8)
+            if (c0 + y < Cn && r0 + tx < R) out[(c0 + y) * R + oc] = t[tx][y];
+        __syncthreads();
+    }
+}
+// point-major operands: A_f = At[f][m kk], B_f = Bt[f][kk n]; a CTA copies the
+// slices of FB consecutive points contiguously (16-byte loads), each thread
+// owns 4 x 4 output blocks: per term 4 broadcast words of A and one 16-byte
+// load of B (m, n multiples of 4); output Ct[f][m n].
+__global__ void __launch_bounds__(256, 2) k_point_matmul_pm(const uint32_t* __restrict__ At,
+                                                            const uint32_t* __restrict__ Bt, uint32_t* __restrict__ Ct,
+                                                            int m, int kk, int n, long long L, int FB, uint32_t p,
+                                                            uint64_t mu) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int sa = m * kk, sb = kk * n;
+    const int mb = m >> 2, nb = n >> 2;
+    uint32_t* SA = sm;                  // [FB][m][kk]
+    uint32_t* SB = sm + FB * sa;        // [FB][kk][n]
+    for (long long f0 = (long long)blockIdx.x * FB; f0 < L; f0 += (long long)gridDim.x * FB) {
+        const int nf = (int)(L - f0 < FB ? L - f0 : FB);
+        __syncthreads();
+        const uint4* gA = (const uint4*)(At + f0 * sa);
+        for (int e = threadIdx.x; e < nf * sa / 4; e += blockDim.x) ((uint4*)SA)[e] = gA[e];
+        const uint4* gB = (const uint4*)(Bt + f0 * sb);
+        for (int e = threadIdx.x; e < nf * sb / 4; e += blockDim.x) ((uint4*)SB)[e] = gB[e];
+        __syncthreads();
+        const int nblk = nf * mb * nb;
+        for (int o = threadIdx.x; o < nblk; o += blockDim.x) {
+            const int jb = o % nb, ib = (o / nb) % mb, f = o / (mb * nb);
+            const uint32_t* a = SA + f * sa + ib * 4 * kk;
+            const uint32_t* bb = SB + f * sb + jb * 4;
+            uint64_t acc[4][4], hi[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int v = 0; v < 4; v++) { acc[u][v] = 0; hi[u][v] = 0; }
+            for (int l0 = 0; l0 < kk; l0 += 16) {
+                const int le = kk - l0 < 16 ? kk - l0 : 16;
+#pragma unroll 4
+                for (int l = l0; l < l0 + le; l++) {
+                    const uint4 yb = *(const uint4*)(bb + l * n);
+                    const uint32_t x[4] = {a[l], a[kk + l], a[2 * kk + l], a[3 * kk + l]};
+                    const uint32_t y[4] = {yb.x, yb.y, yb.z, yb.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+#pragma unroll
+                        for (int v = 0; v < 4; v++) acc[u][v] += (uint64_t)x[u] * y[v];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        hi[u][v] += acc[u][v] >> 32;
+                        acc[u][v] &= 0xFFFFFFFFull;
+                    }
+            }
+            uint32_t* cf = Ct + (f0 + f) * (long long)(m * n) + (ib * 4) * n + jb * 4;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                uint4 r;
+                r.x = mod96_barrett(hi[u][0], acc[u][0], p, mu);
+                r.y = mod96_barrett(hi[u][1], acc[u][1], p, mu);
+                r.z = mod96_barrett(hi[u][2], acc[u][2], p, mu);
+                r.w = mod96_barrett(hi[u][3], acc[u][3], p, mu);
+                *(uint4*)(cf + u * n) = r;
+            }
         }
     }
 }
@@ -1728,8 +1883,15 @@ extern "C" mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t* A, c
     const size_t words = (size_t)(m * kk + kk * n) * 1;   // per evaluation point in shared memory
     const size_t smem_cap = 200 * 1024 / 4;
     if (words > smem_cap) return set_err(MM_E_UNSUPPORTED_SIZE, "m kk + kk n = %zu exceeds %zu", words, smem_cap);
-    int FB = (int)(smem_cap / words);
-    if (FB > 32) FB = 32;
+    // points per CTA: a power of two, >= 8 (32-byte row segments in the staging
+    // loads) when the slices fit ~64 KiB, >= 256 / (4 x 4 blocks per point)
+    const size_t blocks_per_point = ((m + 3) / 4) * ((n + 3) / 4);
+    int FB = 1, lgF = 0;
+    const size_t cap_words = (m % 4 == 0 && n % 4 == 0) ? 8 * 1024 : 16 * 1024;   // per buffer (x2 when vectorised)
+    while (FB < 256 && ((size_t)FB * blocks_per_point < 256 || FB < 8) && (size_t)(2 * FB) * words <= cap_words) {
+        FB *= 2;
+        lgF++;
+    }
     uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
     mm_ntt_plan* P = nullptr;
     if ((s = cached_plan(32, p, k, omega, &P)) != MM_OK) return s;
@@ -1742,13 +1904,55 @@ extern "C" mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t* A, c
     if ((s = fwd_pad_impl<Fp32>(P, A, (long long)(m * kk), (long long)da, (long long)da, Ah, st)) != MM_OK) return s;
     if ((s = fwd_pad_impl<Fp32>(P, B, (long long)(kk * n), (long long)db, (long long)db, Bh, st)) != MM_OK) return s;
     const size_t smem = (size_t)FB * words * 4;
-    MM_CUDA_TRY(cudaFuncSetAttribute(k_point_matmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long tiles = (L + FB - 1) / FB;
-    const int grid = (int)(tiles < num_sms() * 4 ? tiles : num_sms() * 4);
+    const bool v4 = m % 4 == 0 && n % 4 == 0;
+    const uint64_t mu = (uint64_t)(((u128)1 << 64) / p);
+    if (v4) {
+        // point-major operands: transpose [entries][L] -> [L][entries] (coalesced
+        // slices per point), products, transpose back for the inverse transforms
+        void* ws3 = nullptr;
+        if ((s = stream_ws_slot(st, 3, (size_t)(m * kk + kk * n + m * n) * L * 4, &ws3)) != MM_OK) return s;
+        uint32_t* At = (uint32_t*)ws3;
+        uint32_t* Bt = At + m * kk * L;
+        uint32_t* Ct = Bt + kk * n * L;
+        const int tg = num_sms() * 8;
+        {
+            LaunchScope ls("transpose", st);
+            k_transpose32<<<tg, 256, 0, st>>>(Ah, At, (long long)(m * kk), L);
+            k_transpose32<<<tg, 256, 0, st>>>(Bh, Bt, (long long)(kk * n), L);
+        }
+        MM_LAUNCH_CHECK();
+        int FBp = 1;
+        while (FBp < 64 && (size_t)(2 * FBp) * words <= 12 * 1024 && (size_t)FBp * ((m / 4) * (n / 4)) < 256) FBp *= 2;
+        const size_t smem_p = (size_t)FBp * words * 4;
+        MM_CUDA_TRY(cudaFuncSetAttribute(k_point_matmul_pm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_point_matmul_pm, 256, smem_p);
+        if (per < 1) per = 1;
+        const long long tl = (L + FBp - 1) / FBp;
+        const int gp = (int)(tl < (long long)num_sms() * per ? tl : (long long)num_sms() * per);
+        {
+            LaunchScope ls("point_matmul", st);
+            k_point_matmul_pm<<<gp, 256, smem_p, st>>>(At, Bt, Ct, (int)m, (int)kk, (int)n, L, FBp, (uint32_t)p, mu);
+        }
+        MM_LAUNCH_CHECK();
+        {
+            LaunchScope ls("transpose", st);
+            k_transpose32<<<tg, 256, 0, st>>>(Ct, Ch, L, (long long)(m * n));
+        }
+        MM_LAUNCH_CHECK();
+        return inv_trunc_impl<Fp32>(P, Ch, (long long)(m * n), C, (long long)lc, (long long)lc, st);
+    }
+    auto pm_kern = (void*)k_point_matmul_any;
+    MM_CUDA_TRY(cudaFuncSetAttribute(pm_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pm_kern, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = (int)(tiles < (long long)num_sms() * per_sm ? tiles : (long long)num_sms() * per_sm);
     const uint64_t r64 = (uint64_t)(((u128)1 << 64) % p);
     {
         LaunchScope ls("point_matmul", st);
-        k_point_matmul<<<grid, 256, smem, st>>>(Ah, Bh, Ch, (int)m, (int)kk, (int)n, L, FB, (uint32_t)p, r64);
+        k_point_matmul_any<<<grid, 256, smem, st>>>(Ah, Bh, Ch, (int)m, (int)kk, (int)n, L, FB, (uint32_t)p, r64);
     }
     MM_LAUNCH_CHECK();
     return inv_trunc_impl<Fp32>(P, Ch, (long long)(m * n), C, (long long)lc, (long long)lc, st);
