@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(NT, 3) k_col_inv(const __grid_constant__ CUten
 }
 
 // ---------------------------------------------------------------- fused product rows
-// Tile = 16 rows of 256; thread (r, lo) = (tid >> 4, tid & 15).  Shared rows
+// Tile = 16 rows of 256; thread (r, lo) = (tid >> 4, tid & 15): a warp owns rows
+// 2w and 2w + 1 and every shared exchange stays inside them, so the phases
+// are separated by __syncwarp, not CTA barriers (warps drift freely and
+// interleave their multiply- and add-heavy phases).  Shared rows
 // are padded by one 16-byte chunk per 8 (chunk q at q + (q >> 3)) with a row
 // pitch of 76 chunks (= 4 mod 8): the strided 4-byte accesses of the table
 // groups (16 lanes x 4 chunks per row, two rows per warp) and the 16-byte
@@ -390,6 +393,15 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
     __syncthreads();
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row = tile * 16 + r;
+        {   // warm L2 with the next tile's rows (one 128-byte line per thread per
+            // operand) so its phase-A loads hit L2 instead of HBM
+            const long long nt = tile + gridDim.x;
+            if (nt < ntiles) {
+                const long long off = nt * 16 * 256 + threadIdx.x * 16;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.A + off));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + off));
+            }
+        }
         uint32_t v[2][16];
 #pragma unroll
         for (int t = 0; t < 16; t++) {
@@ -403,7 +415,7 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
             sa[ix] = v[0][t];
             sb[ix] = v[1][t];
         }
-        __syncthreads();
+        __syncwarp();
         // constant group: 16 consecutive spectrum values of both operands
 #pragma unroll
         for (int i = 0; i < 4; i++) {
@@ -423,7 +435,7 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
             const int ix = r * ROWP + pad_word(16 * lo + 4 * i);
             *(uint4*)(sa + ix) = make_uint4(v[0][4 * i], v[0][4 * i + 1], v[0][4 * i + 2], v[0][4 * i + 3]);
         }
-        __syncthreads();
+        __syncwarp();
 #pragma unroll
         for (int t = 0; t < 16; t++) v[0][t] = sa[r * ROWP + pad_word(lo + 16 * t)];
         dit_tab<false>(v[0], lo, twi, f);
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
         uint32_t* dst = a.C + row * 256 + lo;
 #pragma unroll
         for (int t = 0; t < 16; t++) dst[16 * t] = mulw(v[0][t], __ldg(fsr + 16 * t), f);
-        __syncthreads();
+        __syncwarp();
     }
 }
 
