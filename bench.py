@@ -295,7 +295,7 @@ def extras_run(mm, torch, dev, peaks):
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
     issue = {}
-    for kind, nm in enumerate(["IMAD", "IMAD.HI", "IADD3", "VIADDMNMX", "IMAD.HI+2xIADD3"]):
+    for kind, nm in enumerate(["IMAD", "IMAD.HI", "IADD3", "VIADDMNMX", "IMAD.HI+2xIADD3", "DFMA"]):
         r = mm.probe_issue(kind, 4000)
         issue[nm] = round(r / (nsm * clk), 3)
     out["alu_probe"] = {"bfly32_G_per_s": round(b32 / 1e9, 1), "bfly64_G_per_s": round(b64 / 1e9, 1),
@@ -353,6 +353,20 @@ def extras_run(mm, torch, dev, peaks):
     out["C1_16x2^10_fwd_inv_plus_poly511"] = {"us_per_call": round(ms * 1e3, 2),
                                              "us_per_call_cuda_graph": round(ms_graph * 1e3, 2),
                                              "Gbutterfly_per_s_graph": round(bf / (ms_graph * 1e-3) / 1e9, 2)}
+
+    # FP64 FMA reduction (Functions 16-18), 2^27 doubles, p = 63 2^44 + 1
+    p50, nf = 1108307720798209, 1 << 27
+    xf = (gen.residues_torch(9, 1, nf, p50, dev).view(torch.int64)).to(torch.float64)
+    yf = (gen.residues_torch(9, 2, nf, p50, dev).view(torch.int64)).to(torch.float64)
+    zf = torch.empty_like(xf)
+    MF = mm.ModF64(p50)
+    c3f = {}
+    for name, fn in [("modadd_f64", lambda: MF.add(xf, yf, out=zf)), ("modmul_f64", lambda: MF.mul(xf, yf, out=zf))]:
+        msf = tloop(fn, 10)
+        c3f[name] = {"Gelem_per_s": round(nf / (msf * 1e-3) / 1e9, 1), "ms": round(msf, 4),
+                     "hbm_frac": round(nf * 24 / (msf * 1e-3) / 1e9 / hbm, 3)}
+    out["f64_elementwise_2^27_p63x2^44+1"] = c3f
+    del xf, yf, zf
 
     # C3 with the packed output layout (ldc = 2^16 - 1: rows not 32-byte aligned)
     a3 = gen.residues_torch(gen.config_seed(3), 1, C3_BATCH * C3_D, P30, dev).view(torch.uint32).reshape(C3_BATCH, C3_D)

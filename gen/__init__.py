@@ -16,7 +16,8 @@ Two bit-identical backends implement the same integer recipe:
 Recipe:
   w_i   = mix64(key + (i + 1) * GAMMA),   key = seed ^ (stream * STREAM_MULT)
   p < 2^32 : r_i = floor(w_i * p / 2^64)           (multiply-high, uniform to 2^-32)
-  p >= 2^32: r_i = w_i - p if w_i >= p else w_i    (bias <= (2^64 - p) / 2^64)
+  2^32 <= p < 2^62: r_i = (w_i >> 1) mod p         (bias <= p / 2^63)
+  p >= 2^62: r_i = w_i - p if w_i >= p else w_i    (bias <= (2^64 - p) / 2^64)
   limbs    : low 16 bits of w_i
 """
 from __future__ import annotations
@@ -62,6 +63,8 @@ def _map_np(w, p):
             lo = ((w & np.uint64(0xFFFFFFFF)) * P) >> np.uint64(32)
             return ((hi + lo) >> np.uint64(32)).astype(np.uint32)
     P = np.uint64(p)
+    if p < (1 << 62):
+        return ((w >> np.uint64(1)) % P).astype(np.uint64)
     with np.errstate(over="ignore"):
         return np.where(w >= P, w - P, w).astype(np.uint64)
 
@@ -119,6 +122,8 @@ def residues_torch(seed: int, stream: int, count: int, p: int, device, start: in
             lo = _shr((w & 0xFFFFFFFF) * p, 32)
             r = _shr(hi + lo, 32)
             out[off:off + n] = (r - ((r >> 31) << 32)).to(torch.int32)   # to signed 32-bit pattern
+        elif p < (1 << 62):
+            out[off:off + n] = torch.remainder(_shr(w, 1), p)            # non-negative int64
         else:
             flip = -(1 << 63)
             ge = (w ^ flip) >= (_s64(p) ^ flip)                          # unsigned compare

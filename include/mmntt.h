@@ -49,6 +49,7 @@ typedef enum { MM_MUL_BARRETT = 0, MM_MUL_SHOUP = 1, MM_MUL_MONTGOMERY = 2 } mm_
 typedef enum { MM_ORDER_NATURAL = 0, MM_ORDER_BITREV = 1 } mm_order;
 
 typedef struct mm_mod32 mm_mod32;
+typedef struct mm_modf64 mm_modf64;
 typedef struct mm_ntt_plan mm_ntt_plan;
 
 /* Thread-local description of the last non-OK status. */
@@ -156,6 +157,24 @@ mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void *a, s
                          const void *b, size_t lb, size_t ldb, void *c, size_t ldc, size_t batch, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Modular vectors over IEEE doubles (paper §3; SURVEY §8(f)
+ * item 3): residues of an odd p < 2^50 held as integral doubles in [0, p).
+ *   mm_modf64_create : u = 1.0 / p rounded to nearest; p >= 2^50
+ *       -> MM_E_PROFILE (Function 16 needs m <= l - 2 = 50).
+ *   mm_modadd_f64 : Function 17, a = x + y, b = a - p, blend on
+ *       the sign of b.       mm_modsub_f64 : the same for x - y (+ p).
+ *   mm_modmul_f64 : Function 16 / 18: h = x y, l = fma(x, y, -h),
+ *       c = floor(h u), e = fma(-c, p, h) + l, one correction each way
+ *       (Proposition 13).
+ * Device vectors, n elements, async on stream, in place allowed; outputs in
+ * [0, p) for inputs in [0, p) (trusted precondition). */
+mm_status mm_modf64_create(uint64_t p, mm_modf64 **ctx);
+void mm_modf64_destroy(mm_modf64 *ctx);
+mm_status mm_modadd_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
+mm_status mm_modsub_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
+mm_status mm_modmul_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
+
+/* ------------------------------------------------------------------------
  * Polynomial matrix product: C = A B with A
  * an m x kk and B a kk x n matrix of polynomials over Z/pZ.  A:
  * [m][kk][da] coefficients, B: [kk][n][db], C: [m][n][da + db - 1] (entries
@@ -244,7 +263,7 @@ unsigned long long mm_launch_count(void);
 mm_status mm_probe_butterfly(int word_bits, int iters, double *ms, double *bfly, void *stream);
 /* Instruction-issue probe: 8 independent dependency chains per thread of one
  * SASS class (kind 0 IMAD, 1 IMAD.HI, 2 IADD3, 3 VIADDMNMX, 4 IMAD.HI + 2
- * IADD3 interleaved) over a full grid.  Returns the kernel time (*ms) and the
+ * IADD3 interleaved, 5 DFMA) over a full grid.  Returns the kernel time (*ms) and the
  * warp instructions of that class executed (*ops); ops / (ms x SMs x clock)
  * is the per-SM issue rate that prices each instruction of the butterfly. */
 mm_status mm_probe_issue(int kind, int iters, double *ms, double *ops, void *stream);

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "ModF64", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -35,6 +35,11 @@ EXPORTS = {
     "mm_version": (ctypes.c_char_p, []),
     "mm_mod32_create": (_ST, [_u32, ctypes.POINTER(_P)]),
     "mm_mod32_destroy": (None, [_P]),
+    "mm_modf64_create": (_ST, [_u64, ctypes.POINTER(_P)]),
+    "mm_modf64_destroy": (None, [_P]),
+    "mm_modadd_f64": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modsub_f64": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modmul_f64": (_ST, [_P, _P, _P, _P, _sz, _P]),
     "mm_mod32_info": (_ST, [_P, ctypes.POINTER(_u64)]),
     "mm_modadd_u32": (_ST, [_P, _P, _P, _P, _sz, _P]),
     "mm_modsub_u32": (_ST, [_P, _P, _P, _P, _sz, _P]),
@@ -136,6 +141,39 @@ def _esz(t: torch.Tensor) -> int:
 
 
 # ------------------------------------------------------------------ modulus context
+class ModF64:
+    """Modulus context for residues held as IEEE doubles (mm_modf64_create,
+    paper §3): odd p < 2^50, FMA-based products (Functions 16-18)."""
+
+    def __init__(self, p: int):
+        self.p = int(p)
+        h = ctypes.c_void_p()
+        _check(lib().mm_modf64_create(self.p, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_modf64_destroy(h)
+            self._h = None
+
+    def _run(self, name, x, y, out):
+        if x.dtype != torch.float64 or y.dtype != torch.float64:
+            raise ValueError("float64 residues expected")
+        z = torch.empty_like(x) if out is None else out
+        _check(getattr(lib(), name)(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def add(self, x, y, out=None):
+        return self._run("mm_modadd_f64", x, y, out)
+
+    def sub(self, x, y, out=None):
+        return self._run("mm_modsub_f64", x, y, out)
+
+    def mul(self, x, y, out=None):
+        return self._run("mm_modmul_f64", x, y, out)
+
+
 class Mod32:
     """32-bit modulus context (mm_mod32_create): Table-3 Barrett profile and
     Montgomery constants precomputed once."""
@@ -289,7 +327,7 @@ def probe_butterfly(word_bits: int = 32, iters: int = 2000) -> float:
 
 def probe_issue(kind: int, iters: int = 2000) -> float:
     """Warp instructions / s of one SASS class (0 IMAD, 1 IMAD.HI, 2 IADD3,
-    3 VIADDMNMX, 4 IMAD.HI + 2 IADD3) over a full grid."""
+    3 VIADDMNMX, 4 IMAD.HI + 2 IADD3, 5 DFMA) over a full grid."""
     ms, ops = ctypes.c_double(), ctypes.c_double()
     _check(lib().mm_probe_issue(kind, iters, ctypes.byref(ms), ctypes.byref(ops), _stream()))
     return ops.value / (ms.value * 1e-3)

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) k_probe_bfly64(int iters, uint64_t* sink)
 //   kind 0: mul.lo.u32 -> IMAD       kind 1: mul.hi.u32 -> IMAD.HI
 //   kind 2: 3-input add -> IADD3     kind 3: min(a + b, c) -> VIADDMNMX
 //   kind 4: IMAD.HI + 2 IADD3 interleaved (pipe overlap)
+//   kind 5: fma.rn.f64 -> DFMA (the FP64 pipe of Functions 16 / 18)
 template <int KIND>
 __global__ void __launch_bounds__(256) k_probe_issue(uint32_t seed, int iters, uint32_t* sink) {
     uint32_t x[8];
@@ -93,6 +94,22 @@ __global__ void __launch_bounds__(256) k_probe_issue(uint32_t seed, int iters, u
     for (int i = 0; i < 8; i++) acc ^= x[i];
     if (acc == 0x12345678u) sink[0] = acc;
 }
+__global__ void __launch_bounds__(256) k_probe_dfma(double seed, int iters, double* sink) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = seed * (threadIdx.x + 1) + i;
+    const double k = 0.999999, c = 1e-9;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+#pragma unroll
+            for (int i = 0; i < 8; i++) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[i]) : "d"(k), "d"(c));
+    }
+    double acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc += x[i];
+    if (acc == 1234.5) sink[0] = acc;
+}
 
 }  // namespace mm
 
@@ -102,7 +119,7 @@ using namespace mm;
 // instructions of the probed class executed (per SM per clock = ops /
 // (ms 1e-3 x SMs x clock)).
 extern "C" mm_status mm_probe_issue(int kind, int iters, double* ms, double* ops, void* stream) {
-    if (!ms || !ops || iters <= 0 || kind < 0 || kind > 4) return set_err(MM_E_ARG, "bad probe arguments");
+    if (!ms || !ops || iters <= 0 || kind < 0 || kind > 5) return set_err(MM_E_ARG, "bad probe arguments");
     cudaStream_t st = (cudaStream_t)stream;
     int blocks = num_sms() * 8, threads = 256;
     void* sink = nullptr;
@@ -118,7 +135,8 @@ extern "C" mm_status mm_probe_issue(int kind, int iters, double* ms, double* ops
             case 1: k_probe_issue<1><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
             case 2: k_probe_issue<2><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
             case 3: k_probe_issue<3><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
-            default: k_probe_issue<4><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            case 4: k_probe_issue<4><<<blocks, threads, 0, st>>>(12345u, iters, (uint32_t*)sink); break;
+            default: k_probe_dfma<<<blocks, threads, 0, st>>>(1.5, iters, (double*)sink); break;
         }
     }
     cudaEventRecord(b, st);

@@ -11,7 +11,7 @@ PG = (1 << 64) - (1 << 32) + 1
 
 
 def test_numpy_torch_identical():
-    for p in (P30, P32, PG, 7):
+    for p in (P30, P32, PG, 7, 1108307720798209, (1 << 50) - 27, (1 << 40) + 15):
         a = gen.residues(gen.config_seed(3), 1, 100_003, p)
         t = gen.residues_torch(gen.config_seed(3), 1, 100_003, p, "cpu")
         t = t.numpy().view(np.uint32 if p < (1 << 32) else np.uint64)

@@ -132,6 +132,35 @@ def test_elementwise_full_c2_sampled(mm, O):
     assert np.array_equal(pick(z), O.vec_mulmod(xs, ys, p))
 
 
+# ------------------------------------------------------------------ FP64 reduction (paper §3)
+P50 = 1108307720798209          # 63 2^44 + 1, Table 12's prime
+
+
+@pytest.mark.parametrize("p", [P50, (1 << 50) - 27, P30, 7])
+def test_modf64(mm, O, p):
+    # Functions 16-18 over doubles vs the oracle (u128 %), random + boundary residues
+    n = (1 << 18) + 3
+    x = residues(config_seed(2), 7, n, p)
+    y = residues(config_seed(2), 8, n, p)
+    B = sorted({0, 1, 2, (p - 1) // 2, (p + 1) // 2, p - 2, p - 1})
+    x = np.concatenate([x, np.array([a for a in B for _ in B], dtype=np.uint64)])
+    y = np.concatenate([y, np.array([b for _ in B for b in B], dtype=np.uint64)])
+    M = mm.ModF64(p)
+    xt = torch.from_numpy(x.astype(np.float64)).to(DEV)
+    yt = torch.from_numpy(y.astype(np.float64)).to(DEV)
+    for op, ref in [(M.add, O.vec_addmod(x, y, p)), (M.sub, O.vec_submod(x, y, p)), (M.mul, O.vec_mulmod(x, y, p))]:
+        z = host(op(xt, yt))
+        assert np.array_equal(z, np.floor(z)), "non-integral result"
+        assert np.array_equal(z.astype(np.uint64), ref)
+    z = host(M.mul(xt[1:], yt[1:]))           # unaligned vectors: scalar tail path
+    assert np.array_equal(z.astype(np.uint64), O.vec_mulmod(x[1:], y[1:], p))
+
+
+def test_modf64_rejects_wide_prime(mm):
+    with pytest.raises(Exception):
+        mm.ModF64((1 << 61) - 1)
+
+
 # ------------------------------------------------------------------ NTT
 def _ntt_roundtrip(mm, O, bits, p, g, k, batch, seed=5):
     w = O.root_of_unity(g, k, p)
