@@ -368,6 +368,26 @@ def extras_run(mm, torch, dev, peaks):
     out["f64_elementwise_2^27_p63x2^44+1"] = c3f
     del xf, yf, zf
 
+    # the same batched forward NTT (64 x 2^20) over the three residue types:
+    # 32-bit Shoup (p < 2^30), FP64 Function 16 (Table 12's 50-bit prime), Goldilocks
+    cmp = {}
+    kk20, bt = 20, 64
+    for tag, bits, pp, g, dt in [("u32_p998244353", 32, P30, 3, None), ("f64_p63x2^44+1", 52, 1108307720798209, 11, "f"),
+                                 ("u64_goldilocks", 64, PG, 7, None)]:
+        xs = gen.residues_torch(10, 1, bt << kk20, pp, dev)
+        if dt == "f":
+            xs = xs.to(torch.float64)
+        elif bits == 32:
+            xs = xs.view(torch.uint32)
+        else:
+            xs = xs.view(torch.uint64)
+        pl = mm.NttPlan(bits, pp, kk20, root_of_unity(pp, g, kk20), bt)
+        ys = torch.empty_like(xs)
+        msn = tloop(lambda: pl.forward(xs, out=ys, order=mm.BITREV), 10)
+        cmp[tag] = {"ms": round(msn, 4), "Gbutterfly_per_s": round(bt * (1 << (kk20 - 1)) * kk20 / (msn * 1e-3) / 1e9, 1)}
+        del xs, ys, pl
+    out["ntt_fwd_64x2^20_by_residue_type"] = cmp
+
     # C3 with the packed output layout (ldc = 2^16 - 1: rows not 32-byte aligned)
     a3 = gen.residues_torch(gen.config_seed(3), 1, C3_BATCH * C3_D, P30, dev).view(torch.uint32).reshape(C3_BATCH, C3_D)
     b3 = gen.residues_torch(gen.config_seed(3), 2, C3_BATCH * C3_D, P30, dev).view(torch.uint32).reshape(C3_BATCH, C3_D)

@@ -111,6 +111,10 @@ mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, 
  * longer ones use Algorithm 1 with l = n as a two-pass four-step
  * n = n2 x n1 (column pass + twiddle, row pass).
  * Creating a plan builds the twiddle tables on the device (one sync). */
+/* word_bits selects the residue type: 32 (uint32_t, p < 2^30), 64 (uint64_t,
+ * p = 2^64 - 2^32 + 1) or 52 (double holding integers in [0, p), odd prime
+ * p < 2^50: Function 16 products and Function 17 sums on the FP64 pipe,
+ * paper §3 / Table 12; four-step blocks and int_mul take 32 / 64 only). */
 mm_status mm_ntt_plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch,
                              mm_ntt_plan **plan);
 void mm_ntt_plan_destroy(mm_ntt_plan *plan);

@@ -233,7 +233,9 @@ class Mod32:
 
 # ------------------------------------------------------------------ NTT plans
 class NttPlan:
-    """Batched NTT of length 2^log2n over p with root omega (mm_ntt_plan_create)."""
+    """Batched NTT of length 2^log2n over p with root omega (mm_ntt_plan_create).
+    word_bits: 32 (uint32, p < 2^30), 64 (uint64, p = 2^64 - 2^32 + 1) or 52
+    (float64 residues of an odd prime p < 2^50, FMA products, paper §3)."""
 
     def __init__(self, word_bits: int, p: int, log2n: int, omega: int, batch: int = 1):
         self.word_bits, self.p, self.log2n, self.omega, self.batch = word_bits, int(p), log2n, int(omega), batch
@@ -254,7 +256,7 @@ class NttPlan:
         return dict(n1=int(out[0]), n2=int(out[1]), passes=int(out[2]), ws_bytes=int(out[3]))
 
     def _chk(self, x):
-        if x.numel() != self.n * self.batch or _esz(x) * 8 != self.word_bits:
+        if x.numel() != self.n * self.batch or _esz(x) * 8 != (32 if self.word_bits == 32 else 64):
             raise ValueError(f"expected {self.batch}x{self.n} elements of {self.word_bits} bits")
 
     def forward(self, x, out=None, order=BITREV):
@@ -365,7 +367,7 @@ def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | 
     Row-strided 2-D views are passed through as leading dimensions
     (mm_poly_mul_ld), e.g. out = c_pad[:, :la+lb-1] of a [batch, ldc] tensor."""
     if word_bits is None:
-        word_bits = _esz(a) * 8
+        word_bits = 52 if a.dtype == torch.float64 else _esz(a) * 8
     a2, b2 = _rows(a), _rows(b)
     batch, la = a2.shape
     if b2.shape[0] != batch:
@@ -406,7 +408,7 @@ def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.T
     if a.is_cuda or b.is_cuda:
         raise ValueError("poly_mul_host takes host tensors")
     if word_bits is None:
-        word_bits = _esz(a) * 8
+        word_bits = 52 if a.dtype == torch.float64 else _esz(a) * 8
     a2 = a.reshape(-1, a.shape[-1]).contiguous()
     b2 = b.reshape(-1, b.shape[-1]).contiguous()
     batch, la = a2.shape

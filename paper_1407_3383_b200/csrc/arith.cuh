@@ -253,4 +253,52 @@ struct FpG {
     __device__ __forceinline__ uint64_t mul_redc(uint64_t x, uint64_t y) const { return mul(x, y); }
 };
 
+// ----------------------------------------------------------------- FP64
+// Residues of an odd prime p < 2^50 held as integral doubles in [0, p) (paper
+// §3): products by Function 16 (m <= l - 2 = 50), sums by
+// Function 17, every value canonical (2p can exceed 2^50, so no lazy range).
+// Round-to-nearest intrinsics keep the compiler from contracting the
+// sequences the proofs (Propositions 10-13) cover.
+struct FpD {
+    typedef double T;
+    typedef double W;        // twiddle w (Function 16 with a2 = w)
+    double p, u;             // u = 1.0 / p rounded to nearest
+    __device__ __forceinline__ double add(double x, double y) const {
+        const double a = __dadd_rn(x, y);
+        const double b = __dsub_rn(a, p);
+        return b < 0.0 ? a : b;
+    }
+    __device__ __forceinline__ double sub(double x, double y) const {
+        const double a = __dsub_rn(x, y);
+        return a < 0.0 ? __dadd_rn(a, p) : a;
+    }
+    __device__ __forceinline__ double mulw(double x, double w) const {   // Function 16
+        const double h = __dmul_rn(x, w);
+        const double l = __fma_rn(x, w, -h);
+        const double c = floor(__dmul_rn(h, u));
+        const double d = __fma_rn(-c, p, h);
+        double e = __dadd_rn(d, l);
+        e = e >= p ? __dsub_rn(e, p) : e;
+        return e < 0.0 ? __dadd_rn(e, p) : e;
+    }
+    __device__ __forceinline__ void dif(double& x, double& y, W w) const {
+        const double s = add(x, y), d = sub(x, y);
+        x = s;
+        y = mulw(d, w);
+    }
+    __device__ __forceinline__ void dit(double& x, double& y, W w) const {
+        const double t = mulw(y, w);
+        y = sub(x, t);
+        x = add(x, t);
+    }
+    __device__ __forceinline__ void dif1(double& x, double& y) const {
+        const double s = add(x, y), d = sub(x, y);
+        x = s;
+        y = d;
+    }
+    __device__ __forceinline__ void dit1(double& x, double& y) const { dif1(x, y); }
+    __device__ __forceinline__ double canon(double x) const { return x; }
+    __device__ __forceinline__ double mul_redc(double x, double y) const { return mulw(x, y); }
+};
+
 }  // namespace mm

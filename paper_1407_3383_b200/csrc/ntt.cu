@@ -59,6 +59,25 @@ __device__ __forceinline__ void tw_set(uint2* t, long long i, uint32_t w, uint32
     t[i] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));   // (w, psi)
 }
 __device__ __forceinline__ void tw_set(uint64_t* t, long long i, uint64_t w, uint64_t) { t[i] = w; }
+// FP64 plans (word_bits 52): exponents in exact integer arithmetic mod p < 2^50,
+// tables hold the residues as doubles
+struct D50 {
+    uint64_t v;
+    __host__ __device__ D50(uint64_t x = 0) : v(x) {}
+};
+__device__ __forceinline__ uint64_t dmulmod50(uint64_t a, uint64_t b, uint64_t p) {
+    return (uint64_t)(((unsigned __int128)a * b) % p);
+}
+__device__ __forceinline__ void tw_set(double* t, long long i, D50 w, uint64_t) { t[i] = (double)w.v; }
+__device__ D50 tw_pow(D50 w, uint64_t e, uint64_t p) {
+    uint64_t r = 1, b = w.v % p;
+    while (e) {
+        if (e & 1) r = dmulmod50(r, b, p);
+        b = dmulmod50(b, b, p);
+        e >>= 1;
+    }
+    return D50(r);
+}
 __device__ __forceinline__ uint64_t tw_pow(uint32_t w, uint64_t e, uint64_t p) { return dpow32(w, e, (uint32_t)p); }
 __device__ __forceinline__ uint64_t tw_pow(uint64_t w, uint64_t e, uint64_t) { return dpowG(w, e); }
 
@@ -680,6 +699,12 @@ template <> Fp32 make_field<Fp32>(const mm_ntt_plan* P) {
     return f;
 }
 template <> FpG make_field<FpG>(const mm_ntt_plan*) { return FpG(); }
+template <> FpD make_field<FpD>(const mm_ntt_plan* P) {
+    FpD f;
+    f.p = (double)P->p;
+    f.u = 1.0 / f.p;
+    return f;
+}
 
 static inline uint2 mkw32(uint64_t w, uint64_t p) {
     return make_uint2((uint32_t)w, (uint32_t)(((u128)w << 32) / p));
@@ -687,6 +712,7 @@ static inline uint2 mkw32(uint64_t w, uint64_t p) {
 template <class W> static W host_w(uint64_t w, uint64_t p);
 template <> uint2 host_w<uint2>(uint64_t w, uint64_t p) { return mkw32(w, p); }
 template <> uint64_t host_w<uint64_t>(uint64_t w, uint64_t) { return w; }
+template <> double host_w<double>(uint64_t w, uint64_t) { return (double)w; }
 
 static size_t esize(int word_bits) { return word_bits == 32 ? 4 : 8; }
 
@@ -706,6 +732,11 @@ extern template mm_status launch_cols<FpG, true, uint64_t, uint64_t>(const FpG&,
 extern template mm_status launch_cols<FpG, false, uint16_t, uint64_t>(const FpG&, const ColArgs<FpG>&, cudaStream_t);
 extern template mm_status launch_pmul<FpG, uint64_t, uint64_t>(const FpG&, const PmulArgs<FpG>&, cudaStream_t);
 extern template mm_status launch_pmul<FpG, uint16_t, uint64_t>(const FpG&, const PmulArgs<FpG>&, cudaStream_t);
+extern template mm_status launch_rows<FpD, false, double, double>(const FpD&, const RowArgs<FpD>&, cudaStream_t);
+extern template mm_status launch_rows<FpD, true, double, double>(const FpD&, const RowArgs<FpD>&, cudaStream_t);
+extern template mm_status launch_cols<FpD, false, double, double>(const FpD&, const ColArgs<FpD>&, cudaStream_t);
+extern template mm_status launch_cols<FpD, true, double, double>(const FpD&, const ColArgs<FpD>&, cudaStream_t);
+extern template mm_status launch_pmul<FpD, double, double>(const FpD&, const PmulArgs<FpD>&, cudaStream_t);
 
 // ---- plan construction
 // entries 1..15 of the level table of a length-2^k transform with root r: tw[m + i] = r^(i 2^k / 2m)
@@ -820,8 +851,13 @@ static mm_status check_modulus(int word_bits, uint64_t p, int log2n) {
     } else if (word_bits == 64) {
         if (p != FpG::P) return set_err(MM_E_INVALID_MODULUS, "64-bit NTT supports only p = 2^64 - 2^32 + 1");
         if (log2n < 1 || log2n > 25) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,25]", log2n);
+    } else if (word_bits == 52) {
+        if (p < 3 || !(p & 1) || !hprime(p)) return set_err(MM_E_INVALID_MODULUS, "p=%llu is not an odd prime", (unsigned long long)p);
+        if (p >= (1ull << 50))
+            return set_err(MM_E_PROFILE, "FP64 NTT needs p < 2^50 (Function 16: m <= l - 2), got %llu", (unsigned long long)p);
+        if (log2n < 1 || log2n > 25) return set_err(MM_E_UNSUPPORTED_SIZE, "log2n=%d out of [1,25]", log2n);
     } else {
-        return set_err(MM_E_ARG, "word_bits must be 32 or 64");
+        return set_err(MM_E_ARG, "word_bits must be 32, 64 or 52 (FP64 residues)");
     }
     if (log2n > two_adicity(p)) return set_err(MM_E_UNSUPPORTED_SIZE, "2^%d does not divide p-1", log2n);
     return MM_OK;
@@ -857,7 +893,9 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
     P->ninv = hpowmod(n % p, p - 2, p);
     P->ninv_r = word_bits == 32 ? hmulmod(P->ninv, ((u128)1 << 32) % p, p) : P->ninv;
     P->pinv = word_bits == 32 ? inv_mod_2_32((uint32_t)p) : 0;
-    s = word_bits == 32 ? build_tables<uint2, uint32_t>(P) : build_tables<uint64_t, uint64_t>(P);
+    s = word_bits == 32   ? build_tables<uint2, uint32_t>(P)
+        : word_bits == 52 ? build_tables<double, D50>(P)
+                          : build_tables<uint64_t, uint64_t>(P);
     if (s != MM_OK) {
         free_plan(P);
         return s;
@@ -1406,6 +1444,7 @@ extern "C" mm_status mm_ntt_forward(const mm_ntt_plan* plan, const void* in, voi
     if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
     mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
     cudaStream_t st = (cudaStream_t)stream;
+    if (P->word_bits == 52) return fwd_impl<FpD>(P, in, out, order, st);
     return P->word_bits == 32 ? fwd_impl<Fp32>(P, in, out, order, st) : fwd_impl<FpG>(P, in, out, order, st);
 }
 
@@ -1414,12 +1453,14 @@ extern "C" mm_status mm_ntt_inverse(const mm_ntt_plan* plan, const void* in, voi
     if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
     mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
     cudaStream_t st = (cudaStream_t)stream;
+    if (P->word_bits == 52) return inv_impl<FpD>(P, in, out, order, st);
     return P->word_bits == 32 ? inv_impl<Fp32>(P, in, out, order, st) : inv_impl<FpG>(P, in, out, order, st);
 }
 
 static mm_status dist_check(const mm_ntt_plan* P, const void* in, void* out, size_t off, size_t cnt, bool cols) {
     if (!P || !in || !out) return set_err(MM_E_ARG, "null argument");
     if (P->k2 == 0) return set_err(MM_E_UNSUPPORTED_SIZE, "four-step blocks need log2n > %d", MAX_BLOCK_LOG);
+    if (P->word_bits == 52) return set_err(MM_E_ARG, "four-step blocks are built for 32- and 64-bit plans");
     size_t lim = cols ? (1ull << P->k1) : (1ull << P->k2);
     if (cnt == 0 || off + cnt > lim) return set_err(MM_E_ARG, "block [%zu, %zu) out of range %zu", off, off + cnt, lim);
     return MM_OK;
@@ -1523,6 +1564,10 @@ extern "C" mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const
         return product_impl<Fp32, uint32_t, uint32_t>(P, (const uint32_t*)a, (long long)la, (const uint32_t*)b,
                                                       (long long)lb, (uint32_t*)c, (long long)lc, (long long)batch, st,
                                                       (long long)lda, (long long)ldb, (long long)ldc);
+    if (word_bits == 52)
+        return product_impl<FpD, double, double>(P, (const double*)a, (long long)la, (const double*)b, (long long)lb,
+                                                 (double*)c, (long long)lc, (long long)batch, st, (long long)lda,
+                                                 (long long)ldb, (long long)ldc);
     return product_impl<FpG, uint64_t, uint64_t>(P, (const uint64_t*)a, (long long)la, (const uint64_t*)b, (long long)lb,
                                                  (uint64_t*)c, (long long)lc, (long long)batch, st, (long long)lda,
                                                  (long long)ldb, (long long)ldc);
@@ -1574,7 +1619,7 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
                                       size_t lb, void* c, size_t batch, void* stream) {
     if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
     if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
-    if (word_bits != 32 && word_bits != 64) return set_err(MM_E_ARG, "word_bits must be 32 or 64");
+    if (word_bits != 32 && word_bits != 64 && word_bits != 52) return set_err(MM_E_ARG, "word_bits must be 32, 64 or 52");
     const size_t es = esize(word_bits), lc = la + lb - 1;
     const size_t q = 128 / es, ldc = (lc + q - 1) / q * q;
     const size_t per = (la + lb + ldc) * es;

@@ -23,6 +23,7 @@ constexpr size_t SMEM_MAX = 227 * 1024;  // max dynamic shared memory per CTA on
 template <class F> struct Cfg;
 template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, COLC = 32, V = 4 }; };
 template <> struct Cfg<FpG> { enum { RL = 3, BUDGET = 4096, COLC = 16, V = 2 }; };
+template <> struct Cfg<FpD> { enum { RL = 3, BUDGET = 4096, COLC = 16, V = 2 }; };
 
 // Column tiles of L <= 512 points use the interleaved layout [j][c] with C
 // transforms of 128 bytes per row (the global row-major order of the column
@@ -125,6 +126,7 @@ template <class W> __device__ __forceinline__ void stage_twiddles(W* dst, const 
 template <class T> struct Vec;
 template <> struct Vec<uint32_t> { typedef uint4 type; enum { N = 4 }; };
 template <> struct Vec<uint64_t> { typedef ulonglong2 type; enum { N = 2 }; };
+template <> struct Vec<double> { typedef double2 type; enum { N = 2 }; };
 
 template <class T> __device__ __forceinline__ void vget(const typename Vec<T>::type& v, T* out);
 template <> __device__ __forceinline__ void vget<uint32_t>(const uint4& v, uint32_t* o) {
@@ -136,6 +138,10 @@ template <> __device__ __forceinline__ void vget<uint64_t>(const ulonglong2& v, 
 template <class T> __device__ __forceinline__ typename Vec<T>::type vmake(const T* i);
 template <> __device__ __forceinline__ uint4 vmake<uint32_t>(const uint32_t* i) { return make_uint4(i[0], i[1], i[2], i[3]); }
 template <> __device__ __forceinline__ ulonglong2 vmake<uint64_t>(const uint64_t* i) { return make_ulonglong2(i[0], i[1]); }
+template <> __device__ __forceinline__ void vget<double>(const double2& v, double* o) {
+    o[0] = v.x; o[1] = v.y;
+}
+template <> __device__ __forceinline__ double2 vmake<double>(const double* i) { return make_double2(i[0], i[1]); }
 
 // V consecutive twiddles (8 bytes each) with 16-byte loads
 template <class W, int V> __device__ __forceinline__ void ld_wvec(const W* p, W* w) {

@@ -191,6 +191,36 @@ def test_ntt64_sizes(mm, O, k):
     _ntt_roundtrip(mm, O, 64, PG, 7, k, batch=3 if k < 18 else 1)
 
 
+def _f64_roundtrip(mm, O, p, g, k, batch):
+    w = O.root_of_unity(g, k, p)
+    x = residues(9, k, batch << k, p).reshape(batch, 1 << k)
+    plan = mm.NttPlan(52, p, k, w, batch)
+    xt = torch.from_numpy(x.astype(np.float64)).to(DEV)
+    nat = O.ntt_rows(x, w, p)
+    yn = host(plan.forward(xt, out=torch.empty_like(xt), order=mm.NATURAL))
+    assert np.array_equal(yn.astype(np.uint64), nat), (k, "natural")
+    yb = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    assert np.array_equal(host(yb).astype(np.uint64), np.stack([O.to_bitrev(r) for r in nat])), (k, "bitrev")
+    assert np.array_equal(host(plan.inverse(yb.clone(), order=mm.BITREV)).astype(np.uint64), x)
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 10, 12, 13, 16, 18, 20])
+def test_ntt_f64_sizes(mm, O, k):
+    # Table 12's prime 63 2^44 + 1 (generator 11) with FP64 residues (paper §3)
+    _f64_roundtrip(mm, O, P50, 11, k, batch=3 if k < 18 else 1)
+
+
+def test_poly_mul_f64(mm, O):
+    for la, lb, batch in [(1, 1, 1), (511, 513, 2), (3000, 5000, 1), (1 << 15, 1 << 15, 1)]:
+        a = residues(la, 1, la * batch, P50).reshape(batch, la)
+        b = residues(lb, 2, lb * batch, P50).reshape(batch, lb)
+        c = host(mm.poly_mul(torch.from_numpy(a.astype(np.float64)).to(DEV),
+                             torch.from_numpy(b.astype(np.float64)).to(DEV), P50, 11))
+        for r in range(batch):
+            ref = O.poly_mul_schoolbook(a[r], b[r], P50) if la * lb <= 1 << 22 else O.poly_mul_ntt(a[r], b[r], P50, 11)
+            assert np.array_equal(c[r].astype(np.uint64), ref), (la, lb, r)
+
+
 @pytest.mark.parametrize("bits,p,g", [(32, P30, 3), (32, 469762049, 3), (64, PG, 7)])
 def test_ntt_edge_rows(mm, O, bits, p, g):
     for k in (4, 10, 14):
