@@ -368,6 +368,18 @@ def extras_run(mm, torch, dev, peaks):
     out["f64_elementwise_2^27_p63x2^44+1"] = c3f
     del xf, yf, zf
 
+    # C3-fwd: 4096 forward NTTs of length 2^16 (TFT order), and the inverse
+    pl16 = mm.NttPlan(32, P30, 16, root_of_unity(P30, G30, 16), 4096)
+    x16 = gen.residues_torch(gen.config_seed(3), 3, 4096 << 16, P30, dev).view(torch.uint32)
+    y16 = torch.empty_like(x16)
+    msf = tloop(lambda: pl16.forward(x16, out=y16, order=mm.BITREV), 10)
+    msi = tloop(lambda: pl16.inverse(y16, out=x16, order=mm.BITREV), 10)
+    bf16 = 4096 * (1 << 15) * 16
+    out["C3_fwd_4096x2^16"] = {"forward_ms": round(msf, 4), "forward_Gbutterfly_per_s": round(bf16 / (msf * 1e-3) / 1e9, 1),
+                               "inverse_ms": round(msi, 4), "inverse_Gbutterfly_per_s": round(bf16 / (msi * 1e-3) / 1e9, 1),
+                               "hbm_frac_2pass": round(4 * 4096 * (1 << 16) * 4 / (msf * 1e-3) / 1e9 / hbm, 3)}
+    del x16, y16, pl16
+
     # the same batched forward NTT (64 x 2^20) over the three residue types:
     # 32-bit Shoup (p < 2^30), FP64 Function 16 (Table 12's 50-bit prime), Goldilocks
     cmp = {}

@@ -55,7 +55,20 @@ struct ColInvArgs {
     Fld f;
 };
 
+// plain row passes for the standalone transforms (mm_ntt_forward / inverse, k = 16)
+struct RowArgs32 {
+    const uint32_t* in;
+    uint32_t* out;
+    long long nrows;    // rows of 256
+    const uint2* lvl;   // row level table (forward or inverse root)
+    const uint2* fsi;   // inverse only: [i2 * 256 + j1] = w^-(j1 [i2]_8) n^-1
+    Tw15 tc;            // lvl[1..15]
+    Fld f;
+};
+
 mm_status launch_col_fwd(const ColFwdArgs& a, cudaStream_t st);
+mm_status launch_row_fwd(const RowArgs32& a, cudaStream_t st);
+mm_status launch_row_inv(const RowArgs32& a, cudaStream_t st);
 mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st);
 mm_status launch_col_inv(const ColInvArgs& a, cudaStream_t st);
 

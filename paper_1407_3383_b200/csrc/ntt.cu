@@ -682,6 +682,7 @@ struct mm_ntt_plan {
     // specialised 2^16 = 256 x 256 path (ntt_fast32.cu), 32-bit only
     bool fast16 = false;
     void* fs_pm_i = nullptr;   // inverse step-2 table times n^-1 2^32
+    void* fs_ni_i = nullptr;   // inverse step-2 table times n^-1 (standalone inverse)
     mm::f32::Tw15 tw_f1, tw_i1, tw_f2, tw_i2;   // level-table entries 1..15 (host copies)
     void* ws = nullptr;      // lazily allocated workspace (bit-mirror permutations)
     size_t ws_bytes = 0;
@@ -821,10 +822,13 @@ static mm_status build_tables(mm_ntt_plan* P) {
             tw15(&P->tw_f2, r2, P->k2, p);
             tw15(&P->tw_i2, r2i, P->k2, p);
             MM_CUDA_TRY(cudaMalloc(&P->fs_pm_i, ((size_t)1 << k) * sizeof(uint2)));
+            MM_CUDA_TRY(cudaMalloc(&P->fs_ni_i, ((size_t)1 << k) * sizeof(uint2)));
             {
                 LaunchScope ls("twiddle_fs_table", 0);
                 k_fs_table_scaled32<<<256, 256>>>((uint2*)P->fs_pm_i, P->k1, P->k2, (uint32_t)winv,
                                                   (uint32_t)P->ninv_r, (uint32_t)p);
+                k_fs_table_scaled32<<<256, 256>>>((uint2*)P->fs_ni_i, P->k1, P->k2, (uint32_t)winv,
+                                                  (uint32_t)P->ninv, (uint32_t)p);
             }
             MM_LAUNCH_CHECK();
             P->fast16 = true;
@@ -837,7 +841,7 @@ static mm_status build_tables(mm_ntt_plan* P) {
 static void free_plan(mm_ntt_plan* P) {
     if (!P) return;
     void* bufs[] = {P->lvl_f1,  P->lvl_i1,  P->lvl_f2,    P->lvl_i2,    P->fs_lo_f, P->fs_hi_f,
-                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->fs_pm_i, P->ws};
+                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->fs_pm_i, P->fs_ni_i, P->ws};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -937,6 +941,40 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         a.lvl = (const W*)P->lvl_f1;
         return launch_rows<F, false, T, T>(f, a, st);
     }
+    if constexpr (sizeof(T) == 4) {
+        if (P->fast16 && ((uintptr_t)out & 15) == 0) {
+            // 2^16 = 256 x 256: the specialised column and row passes (ntt_fast32.cu)
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::ColFwdArgs cf{};
+            cf.in = (const uint32_t*)in; cf.out = (uint32_t*)out;
+            cf.nbatch = (long long)P->batch;
+            cf.in_bs = cf.in_len = cf.out_bs = n;
+            cf.lvl = (const uint2*)P->lvl_f2;
+            cf.fs = (const uint2*)P->fs_full_f;
+            cf.tc = P->tw_f2;
+            cf.f = ff;
+            mm_status s = f32::launch_col_fwd(cf, st);
+            if (s != MM_OK) return s;
+            f32::RowArgs32 ra{};
+            ra.in = (const uint32_t*)out; ra.out = (uint32_t*)out;
+            ra.nrows = (long long)P->batch << 8;
+            ra.lvl = (const uint2*)P->lvl_f1;
+            ra.tc = P->tw_f1;
+            ra.f = ff;
+            if ((s = f32::launch_row_fwd(ra, st)) != MM_OK) return s;
+            if (order == MM_ORDER_NATURAL) {
+                size_t bytes = (size_t)n * P->batch * sizeof(T);
+                if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
+                {
+                    LaunchScope ls("bitrev_permute", st);
+                    k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)out, (T*)P->ws, P->k, (long long)P->batch);
+                }
+                MM_LAUNCH_CHECK();
+                MM_CUDA_TRY(cudaMemcpyAsync(out, P->ws, bytes, cudaMemcpyDeviceToDevice, st));
+            }
+            return MM_OK;
+        }
+    }
     // column pass: in -> out, then row pass: out -> out (bit-mirrored result)
     ColArgs<F> c{};
     c.in = in; c.out = out;
@@ -1009,6 +1047,28 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         }
         MM_LAUNCH_CHECK();
         src = P->ws;
+    }
+    if constexpr (sizeof(T) == 4) {
+        if (P->fast16 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::RowArgs32 ra{};
+            ra.in = (const uint32_t*)src; ra.out = (uint32_t*)out;
+            ra.nrows = (long long)P->batch << 8;
+            ra.lvl = (const uint2*)P->lvl_i1;
+            ra.fsi = (const uint2*)P->fs_ni_i;
+            ra.tc = P->tw_i1;
+            ra.f = ff;
+            if ((s = f32::launch_row_inv(ra, st)) != MM_OK) return s;
+            f32::ColInvArgs ci{};
+            ci.in = (const uint32_t*)out; ci.out = (uint32_t*)out;
+            ci.nbatch = (long long)P->batch;
+            ci.in_bs = n;
+            ci.out_bs = ci.out_len = n;
+            ci.lvl = (const uint2*)P->lvl_i2;
+            ci.tc = P->tw_i2;
+            ci.f = ff;
+            return f32::launch_col_inv(ci, st);
+        }
     }
     // inverse row pass (DIT over j1 + twiddle w^-(j1 [i2])): src -> out
     RowArgs<F> a{};

@@ -448,6 +448,76 @@ __global__ void __launch_bounds__(NT, 4) k_row_pmul(RowPmulArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- plain row passes (k = 16 transforms)
+// Forward: steps 3-4 of a row (DIF, table group then constant group), output
+// canonical in the TFT order.  Inverse: DIT (constant group then table group)
+// and the inverse step-2 twiddle with n^-1 folded in.  Warp-private rows as in
+// k_row_pmul.
+__global__ void __launch_bounds__(NT, 4) k_row_fwd(RowArgs32 a) {
+    __shared__ uint2 tw[256];
+    __shared__ __align__(16) uint32_t sa[16 * ROWP];
+    for (int i = threadIdx.x; i < 256; i += NT) tw[i] = a.lvl[i];
+    const int r = threadIdx.x >> 4, lo = threadIdx.x & 15;
+    const long long ntiles = a.nrows >> 4;
+    const Fld f = a.f;
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row = tile * 16 + r;
+        uint32_t v[1][16];
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[0][t] = __ldg(a.in + row * 256 + lo + 16 * t);
+        dif_tab<1>(v, lo, tw, f, false);
+#pragma unroll
+        for (int t = 0; t < 16; t++) sa[r * ROWP + pad_word(lo + 16 * t)] = v[0][t];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint4 x = *(const uint4*)(sa + r * ROWP + pad_word(16 * lo + 4 * i));
+            v[0][4 * i] = x.x; v[0][4 * i + 1] = x.y; v[0][4 * i + 2] = x.z; v[0][4 * i + 3] = x.w;
+        }
+        dif_const(v[0], a.tc, f);
+        uint4* dst = (uint4*)(a.out + row * 256 + 16 * lo);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            dst[i] = make_uint4(canon4(v[0][4 * i], f), canon4(v[0][4 * i + 1], f), canon4(v[0][4 * i + 2], f),
+                                canon4(v[0][4 * i + 3], f));
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(NT, 4) k_row_inv(RowArgs32 a) {
+    __shared__ uint2 tw[256];
+    __shared__ __align__(16) uint32_t sa[16 * ROWP];
+    for (int i = threadIdx.x; i < 256; i += NT) tw[i] = a.lvl[i];
+    const int r = threadIdx.x >> 4, lo = threadIdx.x & 15;
+    const long long ntiles = a.nrows >> 4;
+    const Fld f = a.f;
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row = tile * 16 + r;
+        uint32_t v[16];
+        const uint4* src = (const uint4*)(a.in + row * 256 + 16 * lo);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint4 x = __ldg(src + i);
+            v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
+        }
+        dit_const(v, a.tc, f);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            *(uint4*)(sa + r * ROWP + pad_word(16 * lo + 4 * i)) = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[t] = sa[r * ROWP + pad_word(lo + 16 * t)];
+        dit_tab<false>(v, lo, tw, f);
+        const uint2* fsr = a.fsi + (row & 255) * 256 + lo;
+        uint32_t* dst = a.out + row * 256 + lo;
+#pragma unroll
+        for (int t = 0; t < 16; t++) dst[16 * t] = mulw(v[t], __ldg(fsr + 16 * t), f);
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
     int per_sm = 0;
@@ -522,6 +592,24 @@ mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st) {
     {
         LaunchScope ls("pmul_rows_fourstep", st);
         k_row_pmul<<<grid_of(k_row_pmul, a.nrows / 16, 0), NT, 0, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_row_fwd(const RowArgs32& a, cudaStream_t st) {
+    if (a.nrows % 16 || (((uintptr_t)a.out) & 15)) return set_err(MM_E_ARG, "row pass needs 16-row tiles, aligned rows");
+    {
+        LaunchScope ls("ntt_rows_fwd", st);
+        k_row_fwd<<<grid_of(k_row_fwd, a.nrows / 16, 0), NT, 0, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_row_inv(const RowArgs32& a, cudaStream_t st) {
+    if (a.nrows % 16 || (((uintptr_t)a.in) & 15)) return set_err(MM_E_ARG, "row pass needs 16-row tiles, aligned rows");
+    {
+        LaunchScope ls("ntt_rows_inv", st);
+        k_row_inv<<<grid_of(k_row_inv, a.nrows / 16, 0), NT, 0, st>>>(a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
