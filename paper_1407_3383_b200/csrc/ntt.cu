@@ -1109,6 +1109,28 @@ static mm_status fwd_pad_impl(mm_ntt_plan* P, const void* in, long long rows, lo
     typedef typename F::W W;
     F f = make_field<F>(P);
     const long long n = 1ll << P->k;
+    if constexpr (sizeof(T) == 4) {
+        if (P->fast16 && ((uintptr_t)out & 15) == 0) {   // 256 x 256: the specialised passes
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::ColFwdArgs cf{};
+            cf.in = (const uint32_t*)in; cf.out = (uint32_t*)out;
+            cf.nbatch = rows;
+            cf.in_bs = in_rs; cf.in_len = in_len; cf.out_bs = n;
+            cf.lvl = (const uint2*)P->lvl_f2;
+            cf.fs = (const uint2*)P->fs_full_f;
+            cf.tc = P->tw_f2;
+            cf.f = ff;
+            mm_status s = f32::launch_col_fwd(cf, st);
+            if (s != MM_OK) return s;
+            f32::RowArgs32 ra{};
+            ra.in = (const uint32_t*)out; ra.out = (uint32_t*)out;
+            ra.nrows = rows << 8;
+            ra.lvl = (const uint2*)P->lvl_f1;
+            ra.tc = P->tw_f1;
+            ra.f = ff;
+            return f32::launch_row_fwd(ra, st);
+        }
+    }
     if (P->k2 == 0) {
         RowArgs<F> a{};
         a.in = in; a.out = out;
@@ -1158,6 +1180,30 @@ static mm_status inv_trunc_impl(mm_ntt_plan* P, void* in, long long rows, void* 
     F f = make_field<F>(P);
     const long long n = 1ll << P->k;
     W sc = host_w<W>(P->ninv, P->p);
+    if constexpr (sizeof(T) == 4) {
+        if (P->fast16 && ((uintptr_t)in & 15) == 0) {
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::RowArgs32 ra{};
+            ra.in = (const uint32_t*)in; ra.out = (uint32_t*)in;
+            ra.nrows = rows << 8;
+            ra.lvl = (const uint2*)P->lvl_i1;
+            ra.fsi = (const uint2*)P->fs_ni_i;
+            ra.tc = P->tw_i1;
+            ra.f = ff;
+            mm_status s = f32::launch_row_inv(ra, st);
+            if (s != MM_OK) return s;
+            f32::ColInvArgs ci{};
+            ci.in = (const uint32_t*)in; ci.out = (uint32_t*)out;
+            ci.nbatch = rows;
+            ci.in_bs = n;
+            ci.out_bs = out_rs;
+            ci.out_len = out_len;
+            ci.lvl = (const uint2*)P->lvl_i2;
+            ci.tc = P->tw_i2;
+            ci.f = ff;
+            return f32::launch_col_inv(ci, st);
+        }
+    }
     if (P->k2 == 0) {
         RowArgs<F> a{};
         a.in = in; a.out = out;
