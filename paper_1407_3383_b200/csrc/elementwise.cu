@@ -26,6 +26,7 @@ enum Op { OP_ADD, OP_SUB, OP_MUL_BARRETT, OP_MUL_SHOUP, OP_MUL_MONT, OP_SHOUP_PR
 struct ModDev {
     uint32_t p, pinv, r2;
     Barrett32 bar;
+    uint64_t mu;         // floor(2^64 / p): the Shoup companion without a division
 };
 
 template <int OP, bool FULL>
@@ -38,7 +39,11 @@ __device__ __forceinline__ uint32_t apply(const ModDev& m, uint32_t x, uint32_t 
         return umin32(d, d - m.p);
     }();
     if (OP == OP_MUL_MONT) return mul_mont(x, y, m.p, m.pinv);
-    if (OP == OP_SHOUP_PRE) return (uint32_t)(((uint64_t)y << 32) / m.p);   // psi
+    if (OP == OP_SHOUP_PRE) {   // psi = floor(y 2^32 / p) by a reciprocal: q = hi(a mu) <= floor(a / p) <= q + 1
+        const uint64_t a = (uint64_t)y << 32;
+        uint64_t q = __umul64hi(a, m.mu);
+        return (uint32_t)(a - q * m.p >= m.p ? q + 1 : q);
+    }
     if (OP == OP_TO_MONT) return mul_mont(x, m.r2, m.p, m.pinv);            // x 2^32 mod p
     return mul_mont(x, 1u, m.p, m.pinv);                                    // OP_FROM_MONT
 }
@@ -123,7 +128,7 @@ static mm_status range_check(const uint32_t* v, size_t n, uint32_t p, cudaStream
 template <int OP, bool FULL>
 static mm_status launch(const mm_mod32* c, const uint32_t* x, const uint32_t* y, const uint32_t* ys, uint32_t* z,
                         size_t n, cudaStream_t st) {
-    ModDev m{c->p, c->pinv, c->r2, c->bar};
+    ModDev m{c->p, c->pinv, c->r2, c->bar, (uint64_t)(((unsigned __int128)1 << 64) / c->p)};
     bool aligned = ((uintptr_t)x | (uintptr_t)y | (uintptr_t)ys | (uintptr_t)z) % 16 == 0;
     size_t nv = aligned ? n / 4 : 0;
     if (nv) {
