@@ -14,6 +14,7 @@
 #include "ntt_kernels.cuh"
 #include "fast32.h"
 #include <new>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -306,6 +307,103 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_apply(D d, long long nout, co
         long long j = j0 + e;
         if (j < nout) out[j] = (typename D::Out)(w[e] + C);    // mod 2^W by the cast
         C = g[e] | ((all_ones<D>(w[e]) ? 1u : 0u) & C);
+    }
+}
+
+// Dig16 fast path: a CTA stages the coefficients [jb - 4, jb + CARRY_B) of its
+// limb block in shared memory once (coalesced, one pad word per 16 so the
+// 16-apart thread windows do not collide), then every thread forms its 16 digit
+// sums from a 20-coefficient register window (the generic path reloads 8
+// coefficients per limb from global memory).
+constexpr int C16_SM = CARRY_B + 4 + (CARRY_B + 4) / 16 + 1;
+__device__ __forceinline__ int c16_pad(int r) { return r + (r >> 4); }
+__device__ __forceinline__ void c16_stage(uint64_t* sc, const uint64_t* __restrict__ c, long long nc, long long jb) {
+    for (int r = threadIdx.x; r < CARRY_B + 4; r += blockDim.x) {
+        const long long k = jb - 4 + r;
+        sc[c16_pad(r)] = (k >= 0 && k < nc) ? c[k] : 0ull;
+    }
+}
+// w[e], g[e] for limbs j = jb + 16 t + e (see the Dig16 comment above)
+__device__ __forceinline__ void c16_wg(const uint64_t* sc, uint32_t* w, uint32_t* g) {
+    uint64_t cc[20];
+#pragma unroll
+    for (int u = 0; u < 20; u++) cc[u] = sc[c16_pad(16 * threadIdx.x + u)];
+    uint32_t S[17];
+#pragma unroll
+    for (int q = 0; q < 17; q++) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) t += (uint32_t)(cc[q + 3 - u] >> (16 * u)) & 0xFFFFu;
+        S[q] = t;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const uint32_t v = (S[e + 1] & 0xFFFFu) + (S[e] >> 16);
+        w[e] = v & 0xFFFFu;
+        g[e] = v >> 16;
+    }
+}
+__global__ void __launch_bounds__(CARRY_T) k_carry16_reduce(const uint64_t* __restrict__ c, long long nc, long long nout,
+                                                            uint32_t* __restrict__ agg) {
+    __shared__ uint64_t sc[C16_SM];
+    __shared__ uint32_t sh[64];
+    const long long jb = (long long)blockIdx.x * CARRY_B;
+    c16_stage(sc, c, nc, jb);
+    __syncthreads();
+    uint32_t w[16], g[16];
+    c16_wg(sc, w, g);
+    uint32_t acc = 2u;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const long long j = jb + 16 * threadIdx.x + e;
+        acc = gp_comb(acc, j < nout ? (g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) << 1)) : 2u);
+    }
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = gp_comb(y, x);
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t v = 2u;
+        for (int q = 0; q < (int)(blockDim.x >> 5); q++) v = gp_comb(v, sh[q]);
+        agg[blockIdx.x] = v;
+    }
+}
+__global__ void __launch_bounds__(CARRY_T) k_carry16_apply(const uint64_t* __restrict__ c, long long nc, long long nout,
+                                                           const uint32_t* __restrict__ cin_blk, uint16_t* __restrict__ out) {
+    __shared__ uint64_t sc[C16_SM];
+    __shared__ uint32_t sh[64];
+    const long long jb = (long long)blockIdx.x * CARRY_B;
+    c16_stage(sc, c, nc, jb);
+    __syncthreads();
+    uint32_t w[16], g[16];
+    c16_wg(sc, w, g);
+    uint32_t acc = 2u;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const long long j = jb + 16 * threadIdx.x + e;
+        acc = gp_comb(acc, j < nout ? (g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) << 1)) : 2u);
+    }
+    uint32_t C = block_carry_in(acc, cin_blk[blockIdx.x], sh);
+    const long long j0 = jb + 16 * threadIdx.x;
+    uint32_t o[8];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const uint32_t limb = (w[e] + C) & 0xFFFFu;
+        C = g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) & C);
+        if (e & 1) o[e >> 1] |= limb << 16; else o[e >> 1] = limb;
+    }
+    if (j0 + 16 <= nout && ((((uintptr_t)(out + j0)) & 15) == 0)) {   // two 16-byte stores
+        uint4* d = (uint4*)(out + j0);
+        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; e++)
+            if (j0 + e < nout) out[j0 + e] = (uint16_t)(o[e >> 1] >> (16 * (e & 1)));
     }
 }
 
@@ -1780,6 +1878,24 @@ template <class D>
 static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D::Out* out, cudaStream_t st) {
     // digit-sum lookbehind at position j: j - 1 (carry_gp) -- every policy handles j = 0
     const long long nblk = (nout + CARRY_B - 1) / CARRY_B;
+    if constexpr (std::is_same<D, Dig16>::value) {   // shared-memory staged 16-bit limb path
+        {
+            LaunchScope ls("carry_reduce", st);
+            k_carry16_reduce<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg);
+        }
+        MM_LAUNCH_CHECK();
+        {
+            LaunchScope ls("carry_scan", st);
+            k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
+        }
+        MM_LAUNCH_CHECK();
+        {
+            LaunchScope ls("carry_apply", st);
+            k_carry16_apply<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg, out);
+        }
+        MM_LAUNCH_CHECK();
+        return MM_OK;
+    }
     {
         LaunchScope ls("carry_reduce", st);
         k_carry_reduce<D><<<(int)nblk, CARRY_T, 0, st>>>(d, nout, agg);
