@@ -500,6 +500,28 @@ def sharded_run(mm, torch, dev, world, rank):
     bfly = 8 * (1 << (k - 1)) * k
     out["C4_sharded_8x2^24_fwd"] = {"ms": round(ms, 3), "Gbutterfly_per_s": round(bfly / (ms * 1e-3) / 1e9, 1),
                                     "scaling": "strong", "ranks": world}
+    # the same with the transpose fused into the column pass (CUDA IPC peer stores)
+    try:
+        from paper_1407_3383_b200.dist import peer_pointers
+        import torch.distributed as dist
+        recv = torch.empty(sh.n2 * sh.c1, dtype=torch.uint64, device=dev)
+        ptrs = peer_pointers(recv)
+        rows = torch.empty((sh.r2, sh.n1), dtype=torch.uint64, device=dev)
+
+        def c4p():
+            for x in xs:
+                sh.forward_p2p(x, recv, ptrs)
+                torch.cuda.synchronize()
+                dist.barrier()
+                sh.plan.fwd_rows_seg(recv, rows, sh.rank * sh.r2, sh.r2, sh.c1, sh.r2 * sh.c1)
+
+        msp = timed(c4p, 3, 3, world) / 3
+        out["C4_sharded_8x2^24_fwd_p2p"] = {"ms": round(msp, 3),
+                                            "Gbutterfly_per_s": round(bfly / (msp * 1e-3) / 1e9, 1),
+                                            "scaling": "strong", "ranks": world,
+                                            "note": "column pass stores into peer receive buffers; host barrier"}
+    except Exception as e:
+        out["C4_sharded_p2p_error"] = repr(e)[:200]
     del xs
     # C5: one 2^28-bit x 2^28-bit product sharded over all ranks
     n = 1 << 24

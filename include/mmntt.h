@@ -288,6 +288,23 @@ mm_status mm_ntt_fwd_rows_seg(const mm_ntt_plan *plan, const void *in, void *out
 mm_status mm_ntt_inv_rows_seg(const mm_ntt_plan *plan, const void *in, void *out, size_t row0, size_t nrows,
                               size_t out_seg_len, size_t out_seg_stride, void *stream);
 
+/* Fused column pass + transpose over peer memory (SURVEY §8(e) stretch):
+ * Algorithm 1 steps 1-2 on columns [col0, col0 + ncols) of rank `rank` of G,
+ * with row t of the block stored straight into peer_recv[t / (n2 / G)] at
+ * segment `rank` -- exactly the receive layout of the equal-split
+ * all-to-all, so mm_ntt_fwd_rows_seg consumes it unchanged.  peer_recv[h]:
+ * G <= 8 device pointers valid in this process (CUDA IPC-opened peer
+ * buffers over NVLink, or local buffers), 16-byte aligned.  The caller
+ * orders all ranks' writes before the row pass. */
+mm_status mm_ntt_fwd_cols_p2p(const mm_ntt_plan *plan, const void *in, void *const *peer_recv, int G, int rank,
+                              size_t col0, size_t ncols, void *stream);
+/* CUDA IPC plumbing for it: a 64-byte handle of a device allocation, opened
+ * in another process of the same node as a peer pointer (lazy peer access),
+ * closed when done. */
+mm_status mm_ipc_get_handle(const void *dev_ptr, void *handle_out);
+mm_status mm_ipc_open_handle(const void *handle, void **dev_ptr);
+mm_status mm_ipc_close(void *dev_ptr);
+
 /* Sharded integer product blocks (paper_1407_3383_b200/dist.py
  * ShardedIntMul; 64-bit Goldilocks plans):
  *   mm_ntt_fwd_cols_u16 : Algorithm 1 steps 1-2 on columns

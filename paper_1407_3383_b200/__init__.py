@@ -63,6 +63,10 @@ EXPORTS = {
     "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
+    "mm_ipc_get_handle": (_ST, [_P, _P]),
+    "mm_ipc_open_handle": (_ST, [_P, ctypes.POINTER(_P)]),
+    "mm_ipc_close": (_ST, [_P]),
+    "mm_ntt_fwd_cols_p2p": (_ST, [_P, _P, _P, _i32, _i32, _sz, _sz, _P]),
     "mm_ntt_fwd_cols_u16": (_ST, [_P, _P, _sz, _P, _sz, _sz, _P]),
     "mm_ntt_pmul_rows_seg": (_ST, [_P, _P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_carry_chunks_halo": (_ST, [_P, _sz, _sz, _P, _P]),
@@ -294,6 +298,12 @@ class NttPlan:
         _check(lib().mm_ntt_inv_rows_seg(self._h, _ptr(x), _ptr(out), row0, nrows, seg_len, seg_stride, _stream(x)))
         return out
 
+    def fwd_cols_p2p(self, x, peer_ptrs, rank, col0, ncols):
+        """Column pass whose rows land directly in the peers' receive buffers
+        (peer_ptrs: G device addresses; segment `rank` of each)."""
+        arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(q) for q in peer_ptrs])
+        _check(lib().mm_ntt_fwd_cols_p2p(self._h, _ptr(x), arr, len(peer_ptrs), rank, col0, ncols, _stream(x)))
+
     def fwd_cols_u16(self, limbs, out, col0, ncols):
         """Steps 1-2 on columns [col0, col0 + ncols) of the zero-padded 16-bit limb
         vector viewed as [n2][n1] (widened to the 64-bit field); out [n2][ncols]."""
@@ -423,6 +433,24 @@ def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.T
                                   ctypes.c_void_p(st.cuda_stream)))
     st.synchronize()
     return out
+
+
+# ------------------------------------------------------------------ CUDA IPC (peer-scatter path)
+def ipc_handle(t: torch.Tensor) -> bytes:
+    """64-byte CUDA IPC handle of the allocation holding t (t at its start)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().mm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    _check(lib().mm_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int):
+    _check(lib().mm_ipc_close(ctypes.c_void_p(ptr)))
 
 
 # ------------------------------------------------------------------ chunked carries (sharded int_mul)

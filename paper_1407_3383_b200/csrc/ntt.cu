@@ -14,6 +14,7 @@
 #include "ntt_kernels.cuh"
 #include "fast32.h"
 #include <new>
+#include <string.h>
 #include <type_traits>
 #include <map>
 #include <mutex>
@@ -2277,4 +2278,77 @@ extern "C" mm_status mm_int_matmul_u32(const uint32_t* A, const uint32_t* B, uin
     }
     MM_LAUNCH_CHECK();
     return carry_run(Dig32x3Batch{Wd, (long long)lc, (long long)nout}, (long long)nall, agg, C, st);
+}
+
+// ---- fused column pass + transpose over peer memory ---------------------------------
+// Rank g's column pass (Algorithm 1 steps 1-2 on columns [col0, col0 + ncols))
+// stores row t of its block straight into the receive buffer of the rank that
+// owns row block h = t / (n2 / G), at segment g: peer_recv[h] + g r2 ncols +
+// (t - h r2) ncols + c -- the layout NCCL's all-to-all would deliver, so the
+// row pass (mm_ntt_fwd_rows_seg) reads it unchanged.  peer_recv[h] are device
+// pointers valid in this process (cudaIpcOpenMemHandle'd peer buffers on one
+// node, or local buffers for one-GPU tests); the caller orders the writes
+// before the row pass (stream / cross-rank barrier).
+extern "C" mm_status mm_ntt_fwd_cols_p2p(const mm_ntt_plan* plan, const void* in, void* const* peer_recv, int G,
+                                         int rank, size_t col0, size_t ncols, void* stream) {
+    mm_status s = dist_check(plan, in, peer_recv ? peer_recv[0] : nullptr, col0, ncols, true);
+    if (s != MM_OK) return s;
+    if (G < 1 || G > 8 || rank < 0 || rank >= G) return set_err(MM_E_ARG, "G must be in [1, 8], rank in [0, G)");
+    mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
+    const long long n2 = 1ll << P->k2, r2 = n2 / G;
+    if (r2 * G != n2 || (r2 & (r2 - 1))) return set_err(MM_E_ARG, "n2 = %lld not split into powers of two by %d", n2, G);
+    int sh = 0;
+    while ((1ll << sh) < r2) sh++;
+    cudaStream_t st = (cudaStream_t)stream;
+    auto run = [&](auto fld) -> mm_status {
+        typedef decltype(fld) F;
+        typedef typename F::T T;
+        typedef typename F::W W;
+        F f = make_field<F>(P);
+        ColArgs<F> c{};
+        c.in = in; c.out = peer_recv[0];
+        c.ncols = (long long)ncols;
+        c.nbatch = 1;
+        c.in_rs = c.out_rs = (long long)ncols;
+        c.in_bs = c.out_bs = 0;
+        c.in_len = c.out_len = 1ll << P->k;
+        c.col0 = (long long)col0;
+        c.n1 = 1ll << P->k1;
+        c.k = P->k2;
+        c.fs = 1;
+        c.lvl = (const W*)P->lvl_f2;
+        c.fs_lo = (const W*)P->fs_lo_f;
+        c.fs_hi = (const W*)P->fs_hi_f;
+        c.fs_full = (const W*)P->fs_full_f;
+        c.fs_h = P->fs_h;
+        c.npeers = G;
+        c.peer_shift = sh;
+        for (int h = 0; h < G; h++) {
+            if (!peer_recv[h] || ((uintptr_t)peer_recv[h] & 15)) return set_err(MM_E_ARG, "peer buffer %d null or unaligned", h);
+            // segment `rank` of rank h's buffer, re-based so that row t lands at t ncols
+            c.peer_out[h] = (void*)((T*)peer_recv[h] + (long long)rank * r2 * (long long)ncols - (long long)h * r2 * (long long)ncols);
+        }
+        return launch_cols<F, false, T, T>(f, c, st);
+    };
+    return P->word_bits == 32 ? run(Fp32{}) : run(FpG{});
+}
+
+// CUDA IPC plumbing for the peer-scatter path (one node, one process per GPU)
+extern "C" mm_status mm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */) {
+    if (!dev_ptr || !handle_out) return set_err(MM_E_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    MM_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    memcpy(handle_out, &h, sizeof(h));
+    return MM_OK;
+}
+extern "C" mm_status mm_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr) {
+    if (!handle || !dev_ptr) return set_err(MM_E_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    MM_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MM_OK;
+}
+extern "C" mm_status mm_ipc_close(void* dev_ptr) {
+    MM_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+    return MM_OK;
 }

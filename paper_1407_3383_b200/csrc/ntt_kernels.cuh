@@ -92,6 +92,11 @@ template <class F> struct ColArgs {
     const W* fs_hi;
     const W* fs_full;
     int fs_h;
+    // peer scatter (sharded transforms): row t of the output block goes to
+    // peer_out[t >> peer_shift] + t out_rs + c -- the all-to-all receive
+    // buffers of the other ranks written in place (npeers = 0: plain out)
+    int npeers, peer_shift;
+    void* peer_out[8];
 };
 template <class F> struct PmulArgs {
     typedef typename F::W W;
@@ -545,7 +550,10 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                     for (int i = 0; i < V; i++)
                         v[u][i] = E::apply(f, v[u][i], w[u][i], a.fs_lo, a.fs_hi, a.fs_h,
                                            ((unsigned)lin0 + c + i) * bt, a.sc);
-                    if (t < tfull) {
+                    if (a.npeers) {         // fused transpose: store into the owning rank's receive buffer
+                        T* pb = (T*)a.peer_out[t >> a.peer_shift] + cl0;
+                        *(TV*)(pb + (unsigned)t * ors + c) = vmake<T>(v[u]);
+                    } else if (t < tfull) {
                         *(TV*)(ob + (unsigned)t * ors + c) = vmake<T>(v[u]);
                     } else {
 #pragma unroll
@@ -680,6 +688,7 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     a.vec_in = sizeof(TIn) == sizeof(T) && a.in_rs % V == 0 && (a.in_bs % V == 0 || a.nbatch == 1) && aligned16(a.in);
     a.vec_out = sizeof(TOut) == sizeof(T) && a.out_rs % V == 0 && (a.out_bs % V == 0 || a.nbatch == 1) &&
                 aligned16(a.out);
+    if (a.npeers && !a.vec_out) return set_err(MM_E_ARG, "peer scatter needs 16-byte aligned rows");
     auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;

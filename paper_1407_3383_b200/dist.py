@@ -67,6 +67,16 @@ class ShardedNtt:
         self.plan.fwd_rows_seg(recv, out, self.rank * self.r2, self.r2, self.c1, self.r2 * self.c1)
         return out
 
+    def forward_p2p(self, x_cols: torch.Tensor, recv: torch.Tensor, peer_ptrs) -> None:
+        """Steps 1-2 with the transpose fused into the stores: rows of my
+        column block go straight into the peers' receive buffers (peer_ptrs[h]
+        = device address of rank h's `recv`, e.g. CUDA IPC-opened; recv is my
+        own).  After every rank's call completes (a cross-rank barrier),
+        forward_rows(recv) finishes the transform -- no all-to-all."""
+        if tuple(x_cols.shape) != (self.n2, self.c1):
+            raise ValueError(f"expected a [{self.n2}, {self.c1}] column block")
+        self.plan.fwd_cols_p2p(x_cols, peer_ptrs, self.rank, self.rank * self.c1, self.c1)
+
     def forward(self, x_cols: torch.Tensor) -> torch.Tensor:
         send = self.forward_cols(x_cols)
         recv = torch.empty_like(send)
@@ -105,6 +115,17 @@ class ShardedNtt:
     def row_block_positions(self) -> range:
         """Positions of the bit-mirrored output held by this rank."""
         return range(self.rank * self.r2 * self.n1, (self.rank + 1) * self.r2 * self.n1)
+
+
+def peer_pointers(buf: torch.Tensor, group=None) -> list:
+    """Device addresses of every rank's `buf` as seen from this process (one
+    node): CUDA IPC handles all-gathered and opened (own rank: local).  The
+    tensor must start its allocation (fresh torch.empty)."""
+    import paper_1407_3383_b200 as mm
+    G, g = dist.get_world_size(group), dist.get_rank(group)
+    handles = [None] * G
+    dist.all_gather_object(handles, mm.ipc_handle(buf), group=group)
+    return [buf.data_ptr() if h == g else mm.ipc_open(handles[h]) for h in range(G)]
 
 
 class ShardedIntMul:

@@ -570,6 +570,36 @@ def test_fourstep_blocks_loopback(mm, O, bits, p, g, k, G):
                            blocks[r].view(torch.int64 if bits == 64 else torch.int32))
 
 
+@pytest.mark.parametrize("bits,p,g,k", [(32, P30, 3, 16), (64, PG, 7, 20)])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_fourstep_p2p_scatter(mm, O, bits, p, g, k, G):
+    """Fused column pass + transpose (mm_ntt_fwd_cols_p2p): G virtual ranks on one
+    GPU scatter their rows straight into each other's receive buffers; the
+    row pass on those buffers equals the single-GPU transform."""
+    from paper_1407_3383_b200.dist import ShardedNtt
+    w = O.root_of_unity(g, k, p)
+    plan = mm.NttPlan(bits, p, k, w, 1)
+    x = residues(13, k, 1 << k, p)
+    xt = dev(x)
+    ref = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    sh = [ShardedNtt(plan, rank=r, world=G) for r in range(G)]
+    n1, c1 = sh[0].n1, sh[0].c1
+    sv = torch.int64 if bits == 64 else torch.int32
+    xv = xt.view(sv).reshape(-1, n1)
+    blocks = [xv[:, r * c1:(r + 1) * c1].contiguous().view(xt.dtype) for r in range(G)]
+    recv = [torch.full_like(sh[r].forward_cols(blocks[r]), 0) for r in range(G)]
+    ptrs = [t.data_ptr() for t in recv]
+    for r in range(G):
+        sh[r].forward_p2p(blocks[r], recv[r], ptrs)
+    rows = [sh[h].forward_rows(recv[h]) for h in range(G)]
+    got = torch.cat([t.view(sv) for t in rows], dim=0).reshape(-1)
+    assert torch.equal(got, ref.view(sv))
+    # and equal to the NCCL-style path (loopback all-to-all of forward_cols)
+    recv2 = _loopback_exchange([sh[r].forward_cols(blocks[r]).view(sv) for r in range(G)], G)
+    for h in range(G):
+        assert torch.equal(recv[h].view(sv), recv2[h])
+
+
 def _loopback_int_mul(mm, a, b, k, G):
     """dist.ShardedIntMul on one GPU: G virtual ranks, loopback all-to-alls, ring
     and all-gather; returns the product limbs reassembled in natural order."""
@@ -620,3 +650,46 @@ def test_sharded_int_mul_c5_loopback(mm, O):
     rng = random.Random(5)
     q = rng.randrange(1 << 60, 1 << 61) | 1
     assert O.limbs_mod(host(got), q) == O.mulmod(O.limbs_mod(host(a), q), O.limbs_mod(host(b), q), q)
+
+
+def _ipc_worker(rank, world, port):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1407_3383_b200 as m
+        from paper_1407_3383_b200.dist import peer_pointers
+        torch.cuda.set_device(0)
+        buf = torch.zeros(1024, dtype=torch.int32, device="cuda")
+        ptrs = peer_pointers(buf)
+        # each rank writes its id into its slot of every peer's buffer through the opened pointers
+        for h, q in enumerate(ptrs):
+            src = torch.full((4,), rank + 1, dtype=torch.int32, device="cuda")
+            import ctypes
+            torch.cuda.synchronize()
+            ctypes.CDLL("libcudart.so").cudaMemcpy(ctypes.c_void_p(q + 16 * rank), ctypes.c_void_p(src.data_ptr()),
+                                                   ctypes.c_size_t(16), 3)
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = buf[:4 * world].view(world, 4).cpu()
+        assert all((got[r] == r + 1).all() for r in range(world)), got
+        dist.barrier()
+        for h, q in enumerate(ptrs):
+            if h != rank:
+                m.ipc_close(q)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_peer_pointers(mm):
+    # CUDA IPC plumbing of the peer-scatter path: two processes on one GPU
+    # exchange handles (gloo) and write into each other's buffers
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_ipc_worker, args=(2, port), nprocs=2, join=True)
