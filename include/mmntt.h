@@ -178,6 +178,17 @@ mm_status mm_modadd_f64(const mm_modf64 *ctx, const double *x, const double *y, 
 mm_status mm_modsub_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
 mm_status mm_modmul_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
 
+/* Truncated product (Algorithm 1 with l < n):
+ * the same c = a b mod p as mm_poly_mul (32-bit p < 2^30, packed rows),
+ * through a four-step layout of which only lambda = ceil(lc / n1) rows are
+ * transformed: column TFFTs of size lambda, lambda row transforms per
+ * operand and for the inverse, and an inverse column TFT (van der Hoeven)
+ * that rebuilds each column's lambda coefficients.  For lc just above a
+ * power of two this skips about half of the padded transform's row work.
+ * Products that fit one pass (lc <= 2^12) go to mm_poly_mul. */
+mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t *a, size_t la, const uint32_t *b, size_t lb,
+                          uint32_t *c, size_t batch, void *stream);
+
 /* ------------------------------------------------------------------------
  * Polynomial matrix product: C = A B with A
  * an m x kk and B a kk x n matrix of polynomials over Z/pZ.  A:

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "ModF64", "NttPlan", "poly_mul", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "ModF64", "NttPlan", "poly_mul", "poly_mul_tft", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -53,6 +53,7 @@ EXPORTS = {
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
+    "mm_poly_mul_tft": (_ST, [_u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_matmul": (_ST, [_u64, _u64, _P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
     "mm_int_matmul_u32": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
     "mm_int_mul_u32": (_ST, [_P, _sz, _P, _sz, _P, _P]),
@@ -394,6 +395,19 @@ def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | 
     ldc = o2.stride(0) if batch > 1 else lc
     _check(lib().mm_poly_mul_ld(word_bits, int(p), int(g), _ptr_rows(a2), la, lda, _ptr_rows(b2), lb, ldb,
                                 _ptr_rows(o2), ldc, batch, _stream(a)))
+    return out if a.dim() > 1 else out.reshape(-1)
+
+
+def poly_mul_tft(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Truncated-transform product mod p (mm_poly_mul_tft, Algorithm 1 with l < n):
+    a [batch, la], b [batch, lb] uint32 -> c [batch, la + lb - 1]."""
+    a2 = a.reshape(-1, a.shape[-1]) if a.dim() > 1 else a.reshape(1, -1)
+    b2 = b.reshape(-1, b.shape[-1]) if b.dim() > 1 else b.reshape(1, -1)
+    batch, la = a2.shape
+    lb = b2.shape[1]
+    if out is None:
+        out = torch.empty((batch, la + lb - 1), dtype=a.dtype, device=a.device)
+    _check(lib().mm_poly_mul_tft(int(p), int(g), _ptr(a2), la, _ptr(b2), lb, _ptr(out), batch, _stream(a)))
     return out if a.dim() > 1 else out.reshape(-1)
 
 

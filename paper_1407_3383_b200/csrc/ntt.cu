@@ -13,6 +13,7 @@
 #include "common.h"
 #include "ntt_kernels.cuh"
 #include "fast32.h"
+#include "tft.h"
 #include <new>
 #include <string.h>
 #include <type_traits>
@@ -2351,4 +2352,87 @@ extern "C" mm_status mm_ipc_open_handle(const void* handle /* 64 bytes */, void*
 extern "C" mm_status mm_ipc_close(void* dev_ptr) {
     MM_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
     return MM_OK;
+}
+
+// ---- truncated products (Algorithm 1 with l < n) ----
+// c = a b mod p for `batch` pairs, computing only lambda = ceil(lc / n1) of the
+// n2 rows of the four-step layout: the column pass keeps rows t < lambda of
+// each column TFFT (step 1 restricted to the first lambda outputs), the row
+// passes run on those lambda rows only (steps 3-4, pointwise product, inverse
+// rows + twiddle), and the inverse column TFT recovers the lambda
+// coefficients of every column from its lambda values (tft.cu).  Same
+// result as mm_poly_mul, with ~lambda / n2 of its row work.
+extern "C" mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t* a, size_t la, const uint32_t* b, size_t lb,
+                                     uint32_t* c, size_t batch, void* stream) {
+    if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
+    if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
+    const size_t lc = la + lb - 1;
+    int k = 0;
+    while ((1ull << k) < lc) k++;
+    if (k <= MAX_BLOCK_LOG) return mm_poly_mul(32, p, g, a, la, b, lb, c, batch, stream);   // one pass: nothing to truncate
+    mm_status s = check_modulus(32, p, k);
+    if (s != MM_OK) return s;
+    uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
+    mm_ntt_plan* P = nullptr;
+    if ((s = cached_plan(32, p, k, omega, &P)) != MM_OK) return s;
+    const long long n1 = 1ll << P->k1, lam = ((long long)lc + n1 - 1) / n1;
+    cudaStream_t st = (cudaStream_t)stream;
+    void* ws = nullptr;
+    if ((s = stream_ws(st, (size_t)(2 * lam * n1 * (long long)batch) * 4, &ws)) != MM_OK) return s;
+    uint32_t* WA = (uint32_t*)ws;
+    uint32_t* WB = WA + lam * n1 * (long long)batch;
+    Fp32 f = make_field<Fp32>(P);
+    for (int op = 0; op < 2; op++) {
+        ColArgs<Fp32> cc{};
+        cc.in = op == 0 ? (const void*)a : (const void*)b;
+        cc.out = op == 0 ? WA : WB;
+        cc.ncols = n1;
+        cc.nbatch = (long long)batch;
+        cc.in_rs = n1; cc.out_rs = n1;
+        cc.in_bs = op == 0 ? (long long)la : (long long)lb;
+        cc.out_bs = lam * n1;
+        cc.in_len = cc.in_bs;
+        cc.out_len = lam * n1;                 // rows t < lambda only (the TFFT of size lambda)
+        cc.n1 = n1;
+        cc.k = P->k2;
+        cc.fs = 1;
+        cc.lvl = (const uint2*)P->lvl_f2;
+        cc.fs_lo = (const uint2*)P->fs_lo_f;
+        cc.fs_hi = (const uint2*)P->fs_hi_f;
+        cc.fs_full = (const uint2*)P->fs_full_f;
+        cc.fs_h = P->fs_h;
+        if ((s = launch_cols<Fp32, false, uint32_t, uint32_t>(f, cc, st)) != MM_OK) return s;
+    }
+    PmulArgs<Fp32> m{};
+    m.a = WA; m.b = WB; m.c = WA;
+    m.nrows = (long long)batch * lam;
+    m.a_rs = m.b_rs = m.c_rs = n1;
+    m.la = m.lb = m.lc = n1;
+    m.k = P->k1;
+    m.fs = 1; m.k2 = P->k2; m.row0 = 0;
+    m.rows_per = lam;
+    // the row DIT is unscaled and the column TFT normalises itself: n1^-1 2^32 (REDC)
+    const uint64_t n1inv = hpowmod((uint64_t)n1 % p, p - 2, p);
+    m.sc = mkw32(hmulmod(n1inv, ((u128)1 << 32) % p, p), p);
+    m.lvl_f = (const uint2*)P->lvl_f1;
+    m.lvl_i = (const uint2*)P->lvl_i1;
+    m.fs_lo = (const uint2*)P->fs_lo_i;
+    m.fs_hi = (const uint2*)P->fs_hi_i;
+    m.fs_full = (const uint2*)P->fs_full_i;
+    m.fs_h = P->fs_h;
+    if ((s = launch_pmul<Fp32, uint32_t, uint32_t>(f, m, st)) != MM_OK) return s;
+    tft::ItftArgs it{};
+    it.in = WA; it.out = c;
+    it.nbatch = (long long)batch;
+    it.in_bs = lam * n1;
+    it.out_bs = it.out_len = (long long)lc;
+    it.n1 = n1;
+    it.k2 = P->k2;
+    it.lam = (int)lam;
+    it.p = (uint32_t)p;
+    it.lvl_f = (const uint2*)P->lvl_f2;
+    it.lvl_i = (const uint2*)P->lvl_i2;
+    it.inv2 = mkw32((p + 1) / 2, p);
+    for (int j = 0; j <= P->k2 && j < 11; j++) it.inv_pow2[j] = mkw32(hpowmod((p + 1) / 2, (uint64_t)j, p), p);
+    return tft::launch_col_itft(it, st);
 }

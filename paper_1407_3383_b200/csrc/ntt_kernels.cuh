@@ -79,6 +79,7 @@ template <class F> struct RowArgs {
     const W* fs_hi;
     const W* fs_full;     // full step-2 table [i2][j1] when small enough, else null
     int fs_h;
+    long long rows_per;   // > 0: truncated transforms of rows_per rows each (TFT), i2 = row mod rows_per
 };
 template <class F> struct ColArgs {
     typedef typename F::W W;
@@ -114,6 +115,7 @@ template <class F> struct PmulArgs {
     const W* fs_hi;
     const W* fs_full;
     int fs_h;
+    long long rows_per;   // > 0: truncated transforms of rows_per rows each (TFT), i2 = row mod rows_per
 };
 
 // Epilogue selector (compile time): bits 0-1 = step-2 twiddle (0 none, 1 full
@@ -286,7 +288,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
                                            long long rs, long long len, bool vec, bool perm, const typename F::W* fs_full,
                                            const typename F::W* fs_lo, const typename F::W* fs_hi, int fs_h,
                                            long long row0, int k2, const typename F::W& sc, int seglog = 0,
-                                           long long segstride = 0) {
+                                           long long segstride = 0, long long rows_per = 0) {
     typedef typename F::T T;
     typedef typename F::W W;
     typedef typename Vec<T>::type TV;
@@ -295,6 +297,10 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
     const long long rlim = nrows - r0;
     const unsigned i2mask = (1u << k2) - 1;
     const unsigned i2b = (unsigned)((row0 + r0) & i2mask);
+    // frequency row of tile row c (a truncated transform keeps rows_per rows per transform)
+    auto i2_of = [&](int c) -> unsigned {
+        return rows_per ? (unsigned)((row0 + r0 + c) % rows_per) : ((i2b + (unsigned)c) & i2mask);
+    };
     if (L >= V && sizeof(TOut) == sizeof(T) && vec && !perm) {
         constexpr int TOT = C * L / V;
         constexpr int NV = (TOT + NT - 1) / NT;
@@ -312,7 +318,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
                 RowVecMap<T, Lay, LOGL>::map(e, c, j);
 #pragma unroll
                 for (int i = 0; i < V; i++) v[u][i] = s[Lay::addr(c, j + i)];
-                if (E::FS == 1) ld_wvec<W, V>(fs_full + ((i2b + c) & i2mask) * L + j, w[u]);
+                if (E::FS == 1) ld_wvec<W, V>(fs_full + i2_of(c) * L + j, w[u]);
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
@@ -320,7 +326,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
                 int c, j;
                 RowVecMap<T, Lay, LOGL>::map(e < TOT ? e : 0, c, j);
                 if (e >= TOT || c >= rlim || j >= len) continue;
-                const unsigned i2r = brev((int)((i2b + c) & i2mask), k2);
+                const unsigned i2r = brev((int)i2_of(c), k2);
 #pragma unroll
                 for (int i = 0; i < V; i++) v[u][i] = E::apply(f, v[u][i], w[u][i], fs_lo, fs_hi, fs_h, (unsigned)(j + i) * i2r, sc);
                 if (j + V <= len) {
@@ -336,7 +342,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
         for (int e = threadIdx.x; e < C * L; e += NT) {
             const int c = e >> LOGL, j = e & (L - 1);
             if (c >= rlim || j >= len) continue;
-            const unsigned i2 = (i2b + c) & i2mask;
+            const unsigned i2 = i2_of(c);
             W wf{};
             if (E::FS == 1) wf = __ldg(fs_full + i2 * L + j);
             T x = E::apply(f, s[Lay::addr(c, perm ? brev(j, LOGL) : j)], wf, fs_lo, fs_hi, fs_h,
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
         else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
                                              !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
-                                             a.out_seg_log, a.out_seg_stride);
+                                             a.out_seg_log, a.out_seg_stride, a.rows_per);
         __syncthreads();
     }
 }
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
         tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twi);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
                                              a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc, a.out_seg_log,
-                                             a.out_seg_stride);
+                                             a.out_seg_stride, a.rows_per);
         __syncthreads();
     }
 }

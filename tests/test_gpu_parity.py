@@ -354,6 +354,28 @@ def test_poly_mul_host_pipeline(mm, O):
         assert np.array_equal(u64(c[r].numpy()), O.poly_mul_schoolbook(a[r], b[r], PG)), r
 
 
+@pytest.mark.parametrize("p,g", [(P30, 3), (469762049, 3)])
+def test_poly_mul_tft(mm, O, p, g):
+    # Algorithm 1 with l < n (truncated rows) + inverse column TFT: products of
+    # every length class -- lambda = 1, small, just over a power of two, full
+    rng = random.Random(p + 1)
+    cases = [(2049, 2049, 2), (4097, 1, 1), (2500, 2000, 3), (1 << 15, 3, 2), ((1 << 15) + 1, 1 << 15, 1),
+             (40000, 30000, 1), (30001, 20000, 2), (1 << 16, 1 << 16, 1), (70000, 60001, 1), (3, 5000, 2)]
+    for la, lb, batch in cases:
+        a = residues(rng.randrange(1 << 30), 1, la * batch, p).reshape(batch, la)
+        b = residues(rng.randrange(1 << 30), 2, lb * batch, p).reshape(batch, lb)
+        c = u64(host(mm.poly_mul_tft(dev(a), dev(b), p, g)))
+        cp = u64(host(mm.poly_mul(dev(a), dev(b), p, g)))
+        assert np.array_equal(c, cp), (la, lb)
+        for r in range(min(batch, 2)):
+            ref = O.poly_mul_schoolbook(a[r], b[r], p) if la * lb <= 1 << 22 else O.poly_mul_ntt(a[r], b[r], p, g)
+            assert np.array_equal(c[r], ref), (la, lb, r)
+    # maximal residues
+    a = np.full((1, 33000), p - 1, dtype=np.uint32)
+    c = u64(host(mm.poly_mul_tft(dev(a), dev(a), p, g)))
+    assert np.array_equal(c[0], O.poly_mul_ntt(a[0], a[0], p, g))
+
+
 def test_poly_mul_c3_small_batch(mm, O):
     p, g = P30, 3
     B, d = 8, 1 << 15
