@@ -443,6 +443,19 @@ def extras_run(mm, torch, dev, peaks):
     out["poly_matmul_d2^15_p469762049"] = dict(pm, note="paper Table 15 (one i7-4770 core, context only): "
                                                         "n = 8: 0.15 s, n = 32: 4.7 s")
 
+    # truncated products (lc just above a power of two) vs the padded transform
+    tf = {}
+    for la, bt in ((33000, 512), (40000, 512), (49152, 512)):
+        a3 = gen.residues_torch(gen.config_seed(3), 5, bt * la, P30, dev).view(torch.uint32).reshape(bt, la)
+        b3 = gen.residues_torch(gen.config_seed(3), 6, bt * la, P30, dev).view(torch.uint32).reshape(bt, la)
+        c3 = torch.empty((bt, 2 * la - 1), dtype=torch.uint32, device=dev)
+        msp = tloop(lambda: mm.poly_mul(a3, b3, P30, G30, out=c3), 5)
+        mst = tloop(lambda: mm.poly_mul_tft(a3, b3, P30, G30, out=c3), 5)
+        tf[f"{bt}x(la=lb={la})"] = {"padded_ms": round(msp, 3), "tft_ms": round(mst, 3),
+                                    "speedup": round(msp / mst, 3)}
+        del a3, b3, c3
+    out["tft_vs_padded_p998244353"] = tf
+
     # integer matrix product (Table 17: n x n, entries of 32 x 2^15 bits)
     im = {}
     for N in (8, 32):

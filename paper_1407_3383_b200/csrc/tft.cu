@@ -14,8 +14,13 @@
 //   l <  N/2: the first half's inputs u_i = x_i + y_i are known for i >= l;
 //             descend into the first half;
 // and on the way back recover x_i, y_i = (u_i +- v_i / w_i) / 2, resp.
-// x_i = u_i - y_i.  One warp runs the (uniform) control flow of one column,
-// held transposed in shared memory; values canonical in [0, p), p < 2^30.
+// x_i = u_i - y_i.  The control flow depends only on (n2, lambda), so one
+// CTA runs it for a tile of 32 columns together: the column tile sits in
+// shared memory as [t][32] (a warp touches one row, 32 banks), every step
+// spreads (butterfly, column) pairs over the block with a barrier between
+// steps, and the inverse blocks run two DIT levels per pass (radix 4 in
+// registers).  Twiddles are block-uniform (smem broadcast).  Values are
+// canonical in [0, p), p < 2^30.
 #include "common.h"
 #include "arith.cuh"
 #include "tft.h"
@@ -31,85 +36,123 @@ __device__ __forceinline__ uint32_t mulc(uint32_t x, uint2 w, uint32_t p) {   //
     return r >= p ? r - p : r;
 }
 
-constexpr int NT = 256;
+constexpr int NT = 256, C = 32;
 
-// inverse DIF block of size h (bit-mirrored values -> natural inputs), times h^-1
-__device__ __forceinline__ void full_inverse(uint32_t* s, int h, const uint2* twi, uint2 invh, uint32_t p, int lane) {
-    for (int m = 1; m < h; m <<= 1) {
-        for (int idx = lane; idx < h / 2; idx += 32) {
-            const int k = idx & (m - 1), j = ((idx - k) << 1) + k;
-            const uint32_t x = s[j], t = mulc(s[j + m], twi[m + k], p);
-            s[j] = addm(x, t, p);
-            s[j + m] = subm(x, t, p);
+// inverse DIT over rows [bb, bb + h) of the tile (bit-mirrored values ->
+// natural), times `scale` = h^-1: a radix-2 level first when log2 h is odd,
+// then pairs of levels (m, 2m) per pass
+__device__ __forceinline__ void full_inverse(uint32_t* s, int bb, int h, const uint2* twi, uint2 scale, uint32_t p) {
+    if (h == 1) return;
+    int m = 1;
+    const int lg = 31 - __clz(h);
+    if (lg & 1) {
+        const bool last = h == 2;
+        for (int e = threadIdx.x; e < (h >> 1) * C; e += NT) {
+            const int j = (e >> 5) << 1, c = e & (C - 1);
+            uint32_t* r = s + (bb + j) * C + c;
+            const uint32_t x = r[0], y = r[C];
+            uint32_t u = addm(x, y, p), v = subm(x, y, p);
+            if (last) { u = mulc(u, scale, p); v = mulc(v, scale, p); }
+            r[0] = u;
+            r[C] = v;
         }
-        __syncwarp();
+        __syncthreads();
+        m = 2;
     }
-    for (int i = lane; i < h; i += 32) s[i] = mulc(s[i], invh, p);
-    __syncwarp();
+    for (; m < h; m <<= 2) {
+        const bool last = 4 * m == h;
+        for (int e = threadIdx.x; e < (h >> 2) * C; e += NT) {
+            const int q = e >> 5, c = e & (C - 1), k = q & (m - 1), j = ((q - k) << 2) + k;
+            uint32_t* r = s + (bb + j) * C + c;
+            uint32_t x0 = r[0], x1 = r[m * C], x2 = r[2 * m * C], x3 = r[3 * m * C];
+            const uint2 w1 = twi[m + k], w2 = twi[2 * m + k], w3 = twi[3 * m + k];
+            uint32_t t = mulc(x1, w1, p);
+            x1 = subm(x0, t, p); x0 = addm(x0, t, p);
+            t = mulc(x3, w1, p);
+            x3 = subm(x2, t, p); x2 = addm(x2, t, p);
+            t = mulc(x2, w2, p);
+            x2 = subm(x0, t, p); x0 = addm(x0, t, p);
+            t = mulc(x3, w3, p);
+            x3 = subm(x1, t, p); x1 = addm(x1, t, p);
+            if (last) { x0 = mulc(x0, scale, p); x1 = mulc(x1, scale, p); x2 = mulc(x2, scale, p); x3 = mulc(x3, scale, p); }
+            r[0] = x0; r[m * C] = x1; r[2 * m * C] = x2; r[3 * m * C] = x3;
+        }
+        __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(NT) k_col_itft(ItftArgs a) {
     extern __shared__ uint32_t sm[];
-    const int n2 = 1 << a.k2, C = a.cols, pitch = n2 + 1;
+    const int n2 = 1 << a.k2;
+    uint2* twf = (uint2*)sm;          // column level tables (forward, inverse)
+    uint2* twi = twf + n2;
+    uint32_t* s = (uint32_t*)(twi + n2);
     const uint32_t p = a.p;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < n2; i += NT) { twf[i] = a.lvl_f[i]; twi[i] = a.lvl_i[i]; }
     const long long groups = a.n1 / C, ntiles = groups * a.nbatch;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long b = tile / groups;
         const long long col0 = (tile - b * groups) * C;
         const uint32_t* src = a.in + b * a.in_bs + col0;
-        // rows t < lambda of C columns -> sm[c pitch + t]; zeros beyond lambda (known inputs)
+        // rows t < lambda of 32 columns (canonicalised); rows beyond lambda are the known (zero) inputs
         for (int e = threadIdx.x; e < n2 * C; e += NT) {
-            const int t = e / C, c = e - t * C;
-            sm[c * pitch + t] = t < a.lam ? src[(long long)t * a.n1 + c] : 0u;
+            const int t = e >> 5, c = e & (C - 1);
+            uint32_t x = t < a.lam ? src[(long long)t * a.n1 + c] : 0u;
+            x = x >= 2 * p ? x - 2 * p : x;        // row-pass output is in [0, 4p)
+            s[e] = x >= p ? x - p : x;
         }
         __syncthreads();
-        for (int c = warp; c < C; c += NT / 32) {
-            uint32_t* s = sm + c * pitch;
-            int stb[12], stn[12], stl[12], stk[12], depth = 0;
-            int bb = 0, N = n2, l = a.lam, lg = a.k2;      // N = 2^lg
-            while (N > 1 && l > 0 && l < N) {
-                const int h = N >> 1;
-                if (l >= h) {
-                    full_inverse(s + bb, h, a.lvl_i, a.inv_pow2[lg - 1], p, lane);   // scale h^-1
-                    for (int i = l - h + lane; i < h; i += 32) {
-                        const uint32_t y = s[bb + h + i];
-                        const uint32_t x = subm(s[bb + i], y, p);
-                        s[bb + i] = x;
-                        s[bb + h + i] = mulc(subm(x, y, p), a.lvl_f[h + i], p);
-                    }
-                    __syncwarp();
-                    stb[depth] = bb; stn[depth] = N; stl[depth] = l; stk[depth] = 0; depth++;
-                    bb += h; N = h; l -= h; lg--;
-                } else {
-                    for (int i = l + lane; i < h; i += 32) s[bb + i] = addm(s[bb + i], s[bb + h + i], p);
-                    __syncwarp();
-                    stb[depth] = bb; stn[depth] = N; stl[depth] = l; stk[depth] = 1; depth++;
-                    N = h; lg--;
+        unsigned kinds = 0;
+        int bb = 0, N = n2, l = a.lam, lg = a.k2, depth = 0;      // N = 2^lg
+        while (N > 1 && l > 0 && l < N) {
+            const int h = N >> 1;
+            if (l >= h) {
+                full_inverse(s, bb, h, twi, a.inv_pow2[lg - 1], p);   // first half, scaled h^-1
+                for (int e = threadIdx.x; e < (2 * h - l) * C; e += NT) {
+                    const int i = l - h + (e >> 5), c = e & (C - 1);
+                    const uint32_t y = s[(bb + h + i) * C + c];
+                    const uint32_t x = subm(s[(bb + i) * C + c], y, p);
+                    s[(bb + i) * C + c] = x;
+                    s[(bb + h + i) * C + c] = mulc(subm(x, y, p), twf[h + i], p);
+                }
+                bb += h; l -= h;
+            } else {
+                kinds |= 1u << depth;
+                for (int e = threadIdx.x; e < (h - l) * C; e += NT) {
+                    const int i = l + (e >> 5), c = e & (C - 1);
+                    s[(bb + i) * C + c] = addm(s[(bb + i) * C + c], s[(bb + h + i) * C + c], p);
                 }
             }
-            if (l == N && N > 1) full_inverse(s + bb, N, a.lvl_i, a.inv_pow2[lg], p, lane);
-            while (depth > 0) {
-                depth--;
-                const int b0 = stb[depth], h = stn[depth] >> 1, l0 = stl[depth];
-                if (stk[depth] == 0) {
-                    for (int i = lane; i < l0 - h; i += 32) {
-                        const uint32_t u = s[b0 + i], t = mulc(s[b0 + h + i], a.lvl_i[h + i], p);   // t = v / w_i
-                        s[b0 + i] = mulc(addm(u, t, p), a.inv2, p);
-                        s[b0 + h + i] = mulc(subm(u, t, p), a.inv2, p);
-                    }
-                } else {
-                    for (int i = lane; i < l0; i += 32) s[b0 + i] = subm(s[b0 + i], s[b0 + h + i], p);
-                }
-                __syncwarp();
-            }
+            __syncthreads();
+            N = h; lg--; depth++;
         }
-        __syncthreads();
+        if (l == N) full_inverse(s, bb, N, twi, a.inv_pow2[lg], p);
+        while (depth > 0) {
+            depth--;
+            const int h = N;
+            N <<= 1;
+            if (kinds >> depth & 1) {      // first-half descent: x_i = u_i - y_i, i < l
+                for (int e = threadIdx.x; e < l * C; e += NT) {
+                    const int i = e >> 5, c = e & (C - 1);
+                    s[(bb + i) * C + c] = subm(s[(bb + i) * C + c], s[(bb + h + i) * C + c], p);
+                }
+            } else {                       // second-half descent: (u_i +- v_i / w_i) / 2, i < l
+                bb -= h;
+                for (int e = threadIdx.x; e < l * C; e += NT) {
+                    const int i = e >> 5, c = e & (C - 1);
+                    const uint32_t u = s[(bb + i) * C + c], t = mulc(s[(bb + h + i) * C + c], twi[h + i], p);
+                    s[(bb + i) * C + c] = mulc(addm(u, t, p), a.inv2, p);
+                    s[(bb + h + i) * C + c] = mulc(subm(u, t, p), a.inv2, p);
+                }
+                l += h;
+            }
+            __syncthreads();
+        }
         // coefficients c_{t n1 + col} for t < lambda, truncated to out_len
         uint32_t* dst = a.out + b * a.out_bs + col0;
         for (int e = threadIdx.x; e < a.lam * C; e += NT) {
-            const int t = e / C, c = e - t * C;
-            if ((long long)t * a.n1 + col0 + c < a.out_len) dst[(long long)t * a.n1 + c] = sm[c * pitch + t];
+            const int t = e >> 5, c = e & (C - 1);
+            if ((long long)t * a.n1 + col0 + c < a.out_len) dst[(long long)t * a.n1 + c] = s[e];
         }
         __syncthreads();
     }
@@ -119,12 +162,11 @@ mm_status launch_col_itft(const ItftArgs& a0, cudaStream_t st) {
     ItftArgs a = a0;
     if (a.k2 < 1 || a.k2 > 10) return set_err(MM_E_UNSUPPORTED_SIZE, "inverse TFT columns of 2^%d points", a.k2);
     const int n2 = 1 << a.k2;
-    a.cols = 8192 / n2 < 32 ? 8192 / n2 : 32;
-    if (a.cols < 8) a.cols = 8;
-    if (a.n1 % a.cols) return set_err(MM_E_UNSUPPORTED_SIZE, "n1 = %lld not a multiple of %d", a.n1, a.cols);
-    const size_t smem = (size_t)a.cols * (n2 + 1) * sizeof(uint32_t);
+    a.cols = C;
+    if (a.n1 % C) return set_err(MM_E_UNSUPPORTED_SIZE, "n1 = %lld not a multiple of %d", a.n1, C);
+    const size_t smem = (size_t)n2 * (C * sizeof(uint32_t) + 2 * sizeof(uint2));
     MM_CUDA_TRY(cudaFuncSetAttribute(k_col_itft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const long long tiles = a.n1 / a.cols * a.nbatch;
+    const long long tiles = a.n1 / C * a.nbatch;
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_col_itft, NT, smem);
     if (per < 1) per = 1;
