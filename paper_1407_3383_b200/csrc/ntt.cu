@@ -846,14 +846,18 @@ static void tw15(f32::Tw15* T, uint64_t r, int k, uint64_t p) {
     for (int m = 1; m <= 8; m <<= 1)
         for (int i = 0; i < m; i++) T->w[m + i] = mkw32(hpowmod(r, (uint64_t)i << (k - 1 - (31 - __builtin_clz(m))), p), p);
 }
+// Goldilocks plans append the natural powers w^e (e < L) after the level table:
+// gold.cuh's tiles read their 64-th-root and w_L^(b k_a) twiddles there.
 template <class W, class E>
 static mm_status build_level(void** dst, int k, E w, uint64_t p) {
     size_t L = (size_t)1 << k;
-    MM_CUDA_TRY(cudaMalloc(dst, L * sizeof(W)));
+    constexpr bool NAT = std::is_same<W, uint64_t>::value;
+    MM_CUDA_TRY(cudaMalloc(dst, (NAT ? 2 : 1) * L * sizeof(W)));
     int grid = (int)((L + 255) / 256 < 4096 ? (L + 255) / 256 : 4096);
     {
         LaunchScope ls("twiddle_level_table", 0);
         k_level_table<W, E><<<grid, 256>>>((W*)*dst, k, w, p);
+        if (NAT) k_pow_table<W, E><<<grid, 256>>>((W*)*dst + L, (long long)L, w, 1, p);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
@@ -907,8 +911,11 @@ static mm_status build_tables(mm_ntt_plan* P) {
         if ((s = build_pow<W, E>(&P->fs_hi_f, nhi, (E)w, 1ull << h, p)) != MM_OK) return s;
         if ((s = build_pow<W, E>(&P->fs_lo_i, nlo, (E)winv, 1, p)) != MM_OK) return s;
         if ((s = build_pow<W, E>(&P->fs_hi_i, nhi, (E)winv, 1ull << h, p)) != MM_OK) return s;
-        // full tables TW[i2 n1 + j1] = w^(+-j1 [i2]) when they stay L2-resident (<= 2 MiB)
-        if (((size_t)1 << k) * sizeof(W) <= (2u << 20)) {
+        // full tables TW[i2 n1 + j1] = w^(+-j1 [i2]) when they stay L2-resident (<= 2 MiB);
+        // Goldilocks plans always stream them (8 B per element read beside the
+        // column pass's 16: its kernels are ALU-bound, and one table word
+        // replaces two split-table loads and one of two products per element)
+        if (((size_t)1 << k) * sizeof(W) <= (2u << 20) || P->word_bits == 64) {
             if ((s = build_fs_full<W, E>(&P->fs_full_f, P->k1, P->k2, (E)w, p)) != MM_OK) return s;
             if ((s = build_fs_full<W, E>(&P->fs_full_i, P->k1, P->k2, (E)winv, p)) != MM_OK) return s;
         }

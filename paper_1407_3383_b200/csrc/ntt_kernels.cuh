@@ -12,13 +12,39 @@
 // All sizes are template parameters (LOGL); launchers dispatch on the
 // runtime log2 length.  Explicit instantiations live in ntt_inst*.cu.
 #pragma once
+#include <type_traits>
 #include "common.h"
 #include "ntt_core.cuh"
+#include "gold.cuh"
 
 namespace mm {
 
 constexpr int NT = 256;                  // threads per CTA for tile kernels
 constexpr size_t SMEM_MAX = 227 * 1024;  // max dynamic shared memory per CTA on sm_100
+
+// Goldilocks tiles of 2^11..2^13 points run gold.cuh's 8-point split with
+// delayed reduction (shared-memory layout: one pad word per 64 elements)
+template <class F, int LOGL> struct GoldT {
+    enum { v = std::is_same<F, FpG>::value && LOGL >= 11 && LOGL <= 13 };
+};
+template <class T, int LOGL, int C_> struct RowLayoutG {
+    static constexpr int L = 1 << LOGL;
+    static constexpr int C = C_;
+    static constexpr int SROW = [] {
+        int s = L + (L >> 6);
+        while ((s & 15) != 1) s++;      // consecutive c -> consecutive 8-byte bank pairs
+        return s;
+    }();
+    static constexpr int ELEMS = C * SROW;
+    static constexpr bool COL = false;
+    __device__ __forceinline__ static int addr(int c, int j) { return c * SROW + j + (j >> 6); }
+    template <int PER> __device__ __forceinline__ static void split(int ch, int& c, int& b) {
+        c = ch / PER;
+        b = ch % PER;
+    }
+    __device__ __forceinline__ static int chunk_base(int c, int base) { return c * SROW + base + (base >> 6); }
+    __host__ __device__ static constexpr int off(int x) { return x + (x >> 6); }
+};
 
 template <class F> struct Cfg;
 template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, COLC = 32, V = 4 }; };
@@ -37,12 +63,12 @@ template <class F, int LOGL> struct InterOK {
 template <class F, int LOGL> struct RowsTile {
     typedef typename F::T T;
     enum { C = (Cfg<F>::BUDGET >> LOGL) > 0 ? (Cfg<F>::BUDGET >> LOGL) : 1 };
-    typedef RowLayout<T, LOGL, C> Lay;
+    typedef typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayout<T, LOGL, C>>::type Lay;
 };
 template <class F, int LOGL> struct PmulTile {
     typedef typename F::T T;
     enum { C = ((Cfg<F>::BUDGET / 2) >> LOGL) > 0 ? ((Cfg<F>::BUDGET / 2) >> LOGL) : 1 };
-    typedef RowLayout<T, LOGL, C> Lay;
+    typedef typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayout<T, LOGL, C>>::type Lay;
 };
 // column tiles: one 128-byte line per matrix row when it fits in 64 KiB
 // (ColLayout), else a 32-byte sector per row transposed into padded rows.
@@ -61,7 +87,9 @@ template <class T, int LOGL, int C_> struct RowLayoutOdd : RowLayout<T, LOGL, C_
 template <class F, int LOGL> struct ColsTile {
     typedef typename F::T T;
     enum { C = InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
-    typedef typename std::conditional<InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>, RowLayoutOdd<T, LOGL, C>>::type Lay;
+    typedef typename std::conditional<
+        InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>,
+        typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayoutOdd<T, LOGL, C>>::type>::type Lay;
 };
 
 // ---------------------------------------------------------------- args
@@ -181,8 +209,27 @@ template <class F, int EPIV> struct Epi {
 
 // twiddles in shared memory when the CTA stays under ~100 KiB
 template <class F, int LOGL, int ELEMS, int NTAB> struct TwPlace {
-    enum { SMEM = (size_t)ELEMS * sizeof(typename F::T) + (size_t)NTAB * (1u << LOGL) * sizeof(typename F::W) <= 100 * 1024 };
+    enum { SMEM = !GoldT<F, LOGL>::v &&
+                  (size_t)ELEMS * sizeof(typename F::T) + (size_t)NTAB * (1u << LOGL) * sizeof(typename F::W) <= 100 * 1024 };
 };
+
+// The tile transform of a pass: Goldilocks tiles take gold.cuh's path when the
+// plan's w_64 is the one it is compiled for (full = gtab + L holds w_L^e), the
+// radix-2^RL groups of ntt_core.cuh otherwise.
+template <class F, class Lay, int LOGL, bool INV>
+__device__ __forceinline__ void run_tile(const F& f, typename F::T* s, const typename F::W* tw, const typename F::W* gtab) {
+    if constexpr (GoldT<F, LOGL>::v) {
+        const uint64_t* full = (const uint64_t*)gtab + (1 << LOGL);
+        constexpr uint64_t W64 = INV ? gold::Pow2Val<gold::S_INV>::v : gold::Pow2Val<gold::S_FWD>::v;
+        if (__ldg(full + ((1 << LOGL) >> 6)) == W64) {
+            if (INV) gold::tile_dit<Lay, LOGL, NT>((uint64_t*)s, full);
+            else gold::tile_dif<Lay, LOGL, NT>((uint64_t*)s, full);
+            return;
+        }
+    }
+    if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
+    else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
+}
 
 // ---------------------------------------------------------------- row-tile I/O
 // Vector index e -> (row c, first element j) of a row tile.  For 32-bit rows of
@@ -380,8 +427,7 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
         load_rows<F, Lay, LOGL, TIn>(s, (const TIn*)a.in, r0, a.nrows, a.in_rs, a.in_len, a.vec_in, INV && a.perm,
                                      a.in_seg_log, a.in_seg_stride);
         __syncthreads();
-        if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
-        else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
+        run_tile<F, Lay, LOGL, INV>(f, s, tw, a.lvl);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
                                              !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
                                              a.out_seg_log, a.out_seg_stride, a.rows_per);
@@ -522,8 +568,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
             }
         }
         __syncthreads();
-        if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, cur, tw);
-        else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, cur, tw);
+        run_tile<F, Lay, LOGL, INV>(f, cur, tw, a.lvl);
         col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
         TOut* outb = (TOut*)a.out + b * a.out_bs + cl0;
         if (a.vec_out && sizeof(TOut) == sizeof(T)) {
@@ -620,8 +665,8 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
         load_rows<F, Lay, LOGL, TIn>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false, a.in_seg_log,
                                      a.in_seg_stride);
         __syncthreads();
-        tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twf);
-        tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sb, twf);
+        run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
+        run_tile<F, Lay, LOGL, false>(f, sb, twf, a.lvl_f);
         {
             constexpr int R = L < 16 ? L : 16;
             constexpr int PER = L / R;
@@ -636,7 +681,7 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
             }
         }
         __syncthreads();
-        tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, sa, twi);
+        run_tile<F, Lay, LOGL, true>(f, sa, twi, a.lvl_i);
         store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
                                              a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc, a.out_seg_log,
                                              a.out_seg_stride, a.rows_per);
