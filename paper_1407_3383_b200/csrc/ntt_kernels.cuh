@@ -86,7 +86,9 @@ template <class T, int LOGL, int C_> struct RowLayoutOdd : RowLayout<T, LOGL, C_
 };
 template <class F, int LOGL> struct ColsTile {
     typedef typename F::T T;
-    enum { C = InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
+    // Goldilocks columns of 2^11 / 2^12 points: two per tile (33 / 66 KiB) so
+    // that four / three CTAs share an SM (their passes are latency-bound)
+    enum { C = GoldT<F, LOGL>::v ? 2 : InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
     typedef typename std::conditional<
         InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>,
         typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayoutOdd<T, LOGL, C>>::type>::type Lay;
