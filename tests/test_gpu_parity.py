@@ -281,6 +281,44 @@ def test_ntt_c4_sampled(mm, O):
     assert torch.equal(z.view(torch.int64), x.view(torch.int64))
 
 
+@pytest.mark.parametrize("k", [11, 12, 22, 23])
+@pytest.mark.parametrize("e", [1, 3, 65])
+def test_ntt64_gold_and_generic_tiles(mm, O, k, e):
+    # 2^11 / 2^12 / 2^13 Goldilocks tiles run gold.cuh when w^(n/64) = 2^39 (e = 1,
+    # and e = 65 = 1 mod 64 gives the same 64-th root), the generic radix-8 groups
+    # otherwise (e = 3); every path must equal the definition (oracle NTT)
+    w = pow(O.root_of_unity(7, k, PG), e, PG)
+    batch = 3 if k < 16 else 1
+    x = residues(6, k, batch << k, PG).reshape(batch, 1 << k)
+    plan = mm.NttPlan(64, PG, k, w, batch)
+    xt = dev(x)
+    nat = O.ntt_rows(x, w, PG)
+    yb = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    assert np.array_equal(u64(host(yb)), np.stack([O.to_bitrev(r) for r in nat])), (k, e)
+    assert np.array_equal(host(plan.inverse(yb.clone(), order=mm.BITREV)), x), (k, e)
+
+
+@pytest.mark.parametrize("k", [11, 12, 13, 24])
+def test_ntt64_gold_extreme_rows(mm, O, k):
+    # closed forms through the Goldilocks tiles: delta_0 -> ones, constant p - 1 ->
+    # (n (p-1), 0, ...), zeros -> zeros, delta_1 -> w^i; the all-(p-1) row drives
+    # every 3-word intermediate of gold.cuh to its largest values
+    n = 1 << k
+    w = O.root_of_unity(7, k, PG)
+    x = torch.zeros((4, n), dtype=torch.int64, device=DEV)
+    x[0, 0] = 1
+    x[1, :] = PG - 1 - (1 << 64)    # p - 1 as the int64 bit pattern
+    x[3, 1] = 1
+    plan = mm.NttPlan(64, PG, k, w, 4)
+    y = plan.forward(x, out=torch.empty_like(x), order=mm.NATURAL)
+    assert bool((y[0] == 1).all())
+    assert int(y[1, 0]) & ((1 << 64) - 1) == (n * (PG - 1)) % PG and not bool(y[1, 1:].any())
+    assert not bool(y[2].any())
+    assert [int(v) & ((1 << 64) - 1) for v in host(y[3, :8])] == [pow(w, i, PG) for i in range(8)]
+    z = plan.inverse(y, order=mm.NATURAL)
+    assert torch.equal(z, x)
+
+
 # ------------------------------------------------------------------ poly_mul
 def test_poly_mul_c1(mm, O):
     p, g = P30, 3

@@ -28,6 +28,6 @@ for k in k_col_fwd k_col_inv k_row_pmul; do
       > gpurun_out/${R}_sass_${k}.csv 2>/dev/null
 done
 gzip -f gpurun_out/${R}_sass_*.csv
-rm -f gpurun_out/${R}_full_c4.ncu-rep
+rm -f gpurun_out/${R}_full_c4.ncu-rep gpurun_out/${R}_full_c3.ncu-rep
 ls -la gpurun_out | grep ${R}
 du -sh gpurun_out
