@@ -146,6 +146,7 @@ template <class F> struct PmulArgs {
     const W* fs_full;
     int fs_h;
     long long rows_per;   // > 0: truncated transforms of rows_per rows each (TFT), i2 = row mod rows_per
+    void* scratch;        // single-buffer tiles (PmulK::SB): L words per CTA for the first spectrum
 };
 
 // Epilogue selector (compile time): bits 0-1 = step-2 twiddle (0 none, 1 full
@@ -633,9 +634,13 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
 // ---------------------------------------------------------------- fused product rows
 template <class F, int LOGL> struct PmulK {
     typedef typename PmulTile<F, LOGL>::Lay Lay;
-    enum { TWS = TwPlace<F, LOGL, 2 * Lay::ELEMS, 2>::SMEM };
+    // SB: one 2^13-point Goldilocks row in shared memory at a time (66 KiB, three
+    // CTAs per SM instead of one): the first operand's spectrum waits in a
+    // per-CTA L2-resident scratch row while the second is transformed
+    enum { SB = GoldT<F, LOGL>::v && LOGL == 13 };
+    enum { TWS = TwPlace<F, LOGL, (SB ? 1 : 2) * Lay::ELEMS, 2>::SMEM };
     static constexpr size_t smem() {
-        return 2 * (size_t)Lay::ELEMS * sizeof(typename F::T) +
+        return (SB ? 1 : 2) * (size_t)Lay::ELEMS * sizeof(typename F::T) +
                (TWS ? 2 * (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
     }
 };
@@ -660,6 +665,41 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
     const W* twf = K::TWS ? (const W*)twfs : a.lvl_f;
     const W* twi = K::TWS ? (const W*)twis : a.lvl_i;
     const long long ntiles = (a.nrows + C - 1) / C;
+    if constexpr (K::SB) {
+        static_assert(C == 1, "single-buffer product tiles hold one row");
+        // spectrum of a -> scratch row (same thread writes and reads element j:
+        // plain loads, program order, no fence)
+        T* scr = (T*)a.scratch + (size_t)blockIdx.x * L;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const long long r0 = tile;
+            load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false,
+                                         a.in_seg_log, a.in_seg_stride);
+            __syncthreads();
+            run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
+            for (int j = 2 * threadIdx.x; j < L; j += 2 * NT) {
+                const int ix = Lay::addr(0, j);            // j even: j, j + 1 share a 64-block
+                *(ulonglong2*)(scr + j) = make_ulonglong2(sa[ix], sa[ix + 1]);
+            }
+            __syncthreads();
+            load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false,
+                                         a.in_seg_log, a.in_seg_stride);
+            __syncthreads();
+            run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
+            for (int j = 2 * threadIdx.x; j < L; j += 2 * NT) {
+                const int ix = Lay::addr(0, j);
+                const ulonglong2 u = *(const ulonglong2*)(scr + j);
+                sa[ix] = f.mulw(f.mul_redc((T)u.x, sa[ix]), a.sc);
+                sa[ix + 1] = f.mulw(f.mul_redc((T)u.y, sa[ix + 1]), a.sc);
+            }
+            __syncthreads();
+            run_tile<F, Lay, LOGL, true>(f, sa, twi, a.lvl_i);
+            store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false,
+                                                 a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
+                                                 a.out_seg_log, a.out_seg_stride, a.rows_per);
+            __syncthreads();
+        }
+        return;
+    }
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
         load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false, a.in_seg_log,
@@ -768,11 +808,14 @@ static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
     long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
+    const int grid = grid_for(kern, smem, tiles);
+    if (K::SB) MM_CUDA_TRY(cudaMallocAsync(&a.scratch, (size_t)grid * (1u << LOGL) * sizeof(T), st));
     {
         LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+        kern<<<grid, NT, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
+    if (K::SB) MM_CUDA_TRY(cudaFreeAsync(a.scratch, st));
     return MM_OK;
 }
 
