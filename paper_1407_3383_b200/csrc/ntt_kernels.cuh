@@ -46,6 +46,12 @@ template <class T, int LOGL, int C_> struct RowLayoutG {
     __host__ __device__ static constexpr int off(int x) { return x + (x >> 6); }
 };
 
+// threads per CTA of the row kernels: 2^13-point Goldilocks rows fill 66 KiB of
+// shared memory per row, so their CTAs take 512 threads (two per SM, 32 warps)
+template <class F, int LOGL> struct NTr {
+    enum { v = (GoldT<F, LOGL>::v && LOGL == 13) ? 512 : NT };
+};
+
 template <class F> struct Cfg;
 template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, COLC = 32, V = 4 }; };
 template <> struct Cfg<FpG> { enum { RL = 3, BUDGET = 4096, COLC = 16, V = 2 }; };
@@ -219,19 +225,19 @@ template <class F, int LOGL, int ELEMS, int NTAB> struct TwPlace {
 // The tile transform of a pass: Goldilocks tiles take gold.cuh's path when the
 // plan's w_64 is the one it is compiled for (full = gtab + L holds w_L^e), the
 // radix-2^RL groups of ntt_core.cuh otherwise.
-template <class F, class Lay, int LOGL, bool INV>
+template <class F, class Lay, int LOGL, bool INV, int NTH = NT>
 __device__ __forceinline__ void run_tile(const F& f, typename F::T* s, const typename F::W* tw, const typename F::W* gtab) {
     if constexpr (GoldT<F, LOGL>::v) {
         const uint64_t* full = (const uint64_t*)gtab + (1 << LOGL);
         constexpr uint64_t W64 = INV ? gold::Pow2Val<gold::S_INV>::v : gold::Pow2Val<gold::S_FWD>::v;
         if (__ldg(full + ((1 << LOGL) >> 6)) == W64) {
-            if (INV) gold::tile_dit<Lay, LOGL, NT>((uint64_t*)s, full);
-            else gold::tile_dif<Lay, LOGL, NT>((uint64_t*)s, full);
+            if (INV) gold::tile_dit<Lay, LOGL, NTH>((uint64_t*)s, full);
+            else gold::tile_dif<Lay, LOGL, NTH>((uint64_t*)s, full);
             return;
         }
     }
-    if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
-    else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NT>(f, s, tw);
+    if (INV) tile_dit<F, Lay, LOGL, Cfg<F>::RL, NTH>(f, s, tw);
+    else tile_dif<F, Lay, LOGL, Cfg<F>::RL, NTH>(f, s, tw);
 }
 
 // ---------------------------------------------------------------- row-tile I/O
@@ -277,7 +283,7 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // row, zeros beyond) -> padded row tile; consecutive lanes take consecutive
 // 16-byte vectors of a row (fully coalesced).  A thread issues up to 4
 // vector loads before its shared stores.
-template <class F, class Lay, int LOGL, class TIn>
+template <class F, class Lay, int LOGL, class TIn, int NTH = NT>
 __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long long r0, long long nrows, long long rs,
                                           long long len, bool vec, bool perm, int seglog = 0, long long segstride = 0) {
     typedef typename F::T T;
@@ -286,7 +292,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
     const long long rlim = nrows - r0;                        // rows of this tile that exist
     if (L >= V && sizeof(TIn) == sizeof(T) && vec && !perm) {
         constexpr int TOT = C * L / V;
-        constexpr int NV = (TOT + NT - 1) / NT;
+        constexpr int NV = (TOT + NTH - 1) / NTH;
         constexpr int B = NV < 4 ? NV : 4;
         const T* tb = (const T*)in + r0 * rs;
 #pragma unroll
@@ -295,7 +301,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
             int mode[B];                                      // 0 zero, 1 full, 2 partial
 #pragma unroll
             for (int u = 0; u < B; u++) {
-                const int e = threadIdx.x + (u0 + u) * NT;
+                const int e = threadIdx.x + (u0 + u) * NTH;
                 int c, j;
                 RowVecMap<T, Lay, LOGL>::map(e, c, j);
                 const bool rowok = e < TOT && c < rlim;
@@ -305,7 +311,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
-                const int e = threadIdx.x + (u0 + u) * NT;
+                const int e = threadIdx.x + (u0 + u) * NTH;
                 if (e >= TOT) continue;
                 int c, j;
                 RowVecMap<T, Lay, LOGL>::map(e, c, j);
@@ -322,7 +328,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
             }
         }
     } else {
-        for (int e = threadIdx.x; e < C * L; e += NT) {
+        for (int e = threadIdx.x; e < C * L; e += NTH) {
             const int c = e >> LOGL, j = e & (L - 1);
             T v = 0;
             if (c < rlim && j < len) v = ld_conv<TIn, T>(in + (r0 + c) * rs + seg_j(j, seglog, segstride));
@@ -333,7 +339,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
 
 // epilogue + stores of a row tile (step-2 twiddle rows are contiguous in the
 // full table: one or two 16-byte loads per vector)
-template <class F, class Lay, int LOGL, class TOut, int EPIV>
+template <class F, class Lay, int LOGL, class TOut, int EPIV, int NTH = NT>
 __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, TOut* out, long long r0, long long nrows,
                                            long long rs, long long len, bool vec, bool perm, const typename F::W* fs_full,
                                            const typename F::W* fs_lo, const typename F::W* fs_hi, int fs_h,
@@ -353,7 +359,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
     };
     if (L >= V && sizeof(TOut) == sizeof(T) && vec && !perm) {
         constexpr int TOT = C * L / V;
-        constexpr int NV = (TOT + NT - 1) / NT;
+        constexpr int NV = (TOT + NTH - 1) / NTH;
         constexpr int B = NV < 2 ? NV : 2;
         T* ob = (T*)out + r0 * rs;
 #pragma unroll
@@ -362,7 +368,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
             W w[B][V];
 #pragma unroll
             for (int u = 0; u < B; u++) {
-                const int e0 = threadIdx.x + (u0 + u) * NT;
+                const int e0 = threadIdx.x + (u0 + u) * NTH;
                 const int e = e0 < TOT ? e0 : 0;                  // idle lanes read a valid slot
                 int c, j;
                 RowVecMap<T, Lay, LOGL>::map(e, c, j);
@@ -372,7 +378,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
             }
 #pragma unroll
             for (int u = 0; u < B; u++) {
-                const int e = threadIdx.x + (u0 + u) * NT;
+                const int e = threadIdx.x + (u0 + u) * NTH;
                 int c, j;
                 RowVecMap<T, Lay, LOGL>::map(e < TOT ? e : 0, c, j);
                 if (e >= TOT || c >= rlim || j >= len) continue;
@@ -389,7 +395,7 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
             }
         }
     } else {
-        for (int e = threadIdx.x; e < C * L; e += NT) {
+        for (int e = threadIdx.x; e < C * L; e += NTH) {
             const int c = e >> LOGL, j = e & (L - 1);
             if (c >= rlim || j >= len) continue;
             const unsigned i2 = i2_of(c);
@@ -412,7 +418,8 @@ template <class F, int LOGL> struct RowsK {
 };
 
 template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
-__global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
+__global__ void __launch_bounds__(NTr<F, LOGL>::v, 1024 / NTr<F, LOGL>::v) k_rows(F f, RowArgs<F> a) {
+    constexpr int NTH = NTr<F, LOGL>::v;
     typedef typename F::T T;
     typedef typename F::W W;
     typedef RowsK<F, LOGL> K;
@@ -427,11 +434,11 @@ __global__ void __launch_bounds__(NT, 4) k_rows(F f, RowArgs<F> a) {
     const long long ntiles = (a.nrows + C - 1) / C;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
-        load_rows<F, Lay, LOGL, TIn>(s, (const TIn*)a.in, r0, a.nrows, a.in_rs, a.in_len, a.vec_in, INV && a.perm,
+        load_rows<F, Lay, LOGL, TIn, NTH>(s, (const TIn*)a.in, r0, a.nrows, a.in_rs, a.in_len, a.vec_in, INV && a.perm,
                                      a.in_seg_log, a.in_seg_stride);
         __syncthreads();
-        run_tile<F, Lay, LOGL, INV>(f, s, tw, a.lvl);
-        store_rows<F, Lay, LOGL, TOut, EPIV>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
+        run_tile<F, Lay, LOGL, INV, NTH>(f, s, tw, a.lvl);
+        store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(f, s, (TOut*)a.out, r0, a.nrows, a.out_rs, a.out_len, a.vec_out,
                                              !INV && a.perm, a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
                                              a.out_seg_log, a.out_seg_stride, a.rows_per);
         __syncthreads();
@@ -646,7 +653,8 @@ template <class F, int LOGL> struct PmulK {
 };
 
 template <class F, int LOGL, class TIn, class TOut, int EPIV>
-__global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
+__global__ void __launch_bounds__(NTr<F, LOGL>::v, NTr<F, LOGL>::v == 512 ? 2 : 3) k_rows_pmul(F f, PmulArgs<F> a) {
+    constexpr int NTH = NTr<F, LOGL>::v;
     typedef typename F::T T;
     typedef typename F::W W;
     typedef PmulK<F, LOGL> K;
@@ -672,28 +680,28 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
         T* scr = (T*)a.scratch + (size_t)blockIdx.x * L;
         for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const long long r0 = tile;
-            load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false,
+            load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false,
                                          a.in_seg_log, a.in_seg_stride);
             __syncthreads();
-            run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
-            for (int j = 2 * threadIdx.x; j < L; j += 2 * NT) {
+            run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
+            for (int j = 2 * threadIdx.x; j < L; j += 2 * NTH) {
                 const int ix = Lay::addr(0, j);            // j even: j, j + 1 share a 64-block
                 *(ulonglong2*)(scr + j) = make_ulonglong2(sa[ix], sa[ix + 1]);
             }
             __syncthreads();
-            load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false,
+            load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false,
                                          a.in_seg_log, a.in_seg_stride);
             __syncthreads();
-            run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
-            for (int j = 2 * threadIdx.x; j < L; j += 2 * NT) {
+            run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
+            for (int j = 2 * threadIdx.x; j < L; j += 2 * NTH) {
                 const int ix = Lay::addr(0, j);
                 const ulonglong2 u = *(const ulonglong2*)(scr + j);
                 sa[ix] = f.mulw(f.mul_redc((T)u.x, sa[ix]), a.sc);
                 sa[ix + 1] = f.mulw(f.mul_redc((T)u.y, sa[ix + 1]), a.sc);
             }
             __syncthreads();
-            run_tile<F, Lay, LOGL, true>(f, sa, twi, a.lvl_i);
-            store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false,
+            run_tile<F, Lay, LOGL, true, NTH>(f, sa, twi, a.lvl_i);
+            store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false,
                                                  a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
                                                  a.out_seg_log, a.out_seg_stride, a.rows_per);
             __syncthreads();
@@ -702,17 +710,17 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
     }
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
-        load_rows<F, Lay, LOGL, TIn>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false, a.in_seg_log,
+        load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false, a.in_seg_log,
                                      a.in_seg_stride);
-        load_rows<F, Lay, LOGL, TIn>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false, a.in_seg_log,
+        load_rows<F, Lay, LOGL, TIn, NTH>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false, a.in_seg_log,
                                      a.in_seg_stride);
         __syncthreads();
-        run_tile<F, Lay, LOGL, false>(f, sa, twf, a.lvl_f);
-        run_tile<F, Lay, LOGL, false>(f, sb, twf, a.lvl_f);
+        run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
+        run_tile<F, Lay, LOGL, false, NTH>(f, sb, twf, a.lvl_f);
         {
             constexpr int R = L < 16 ? L : 16;
             constexpr int PER = L / R;
-            for (int ch = threadIdx.x; ch < C * PER; ch += NT) {
+            for (int ch = threadIdx.x; ch < C * PER; ch += NTH) {
                 const int c = ch / PER, b = ch % PER;
                 const int base = Lay::chunk_base(c, b * R);
 #pragma unroll
@@ -723,8 +731,8 @@ __global__ void __launch_bounds__(NT, 3) k_rows_pmul(F f, PmulArgs<F> a) {
             }
         }
         __syncthreads();
-        run_tile<F, Lay, LOGL, true>(f, sa, twi, a.lvl_i);
-        store_rows<F, Lay, LOGL, TOut, EPIV>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
+        run_tile<F, Lay, LOGL, true, NTH>(f, sa, twi, a.lvl_i);
+        store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
                                              a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc, a.out_seg_log,
                                              a.out_seg_stride, a.rows_per);
         __syncthreads();
@@ -736,9 +744,9 @@ template <class K> static mm_status set_smem(K kern, size_t bytes) {
     MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     return MM_OK;
 }
-template <class K> static int grid_for(K kern, size_t smem, long long tiles) {
+template <class K> static int grid_for(K kern, size_t smem, long long tiles, int threads = NT) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm < 1) per_sm = 1;
     long long cap = (long long)num_sms() * per_sm;
     return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
@@ -762,7 +770,7 @@ static mm_status launch_rows_e(const F& f, RowArgs<F> a, cudaStream_t st) {
     long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
     {
         LaunchScope ls(INV ? "ntt_rows_inv" : "ntt_rows_fwd", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+        kern<<<grid_for(kern, smem, tiles, NTr<F, LOGL>::v), NTr<F, LOGL>::v, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
     (void)L;
@@ -808,11 +816,11 @@ static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
     long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
-    const int grid = grid_for(kern, smem, tiles);
+    const int grid = grid_for(kern, smem, tiles, NTr<F, LOGL>::v);
     if (K::SB) MM_CUDA_TRY(cudaMallocAsync(&a.scratch, (size_t)grid * (1u << LOGL) * sizeof(T), st));
     {
         LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
-        kern<<<grid, NT, smem, st>>>(f, a);
+        kern<<<grid, NTr<F, LOGL>::v, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
     if (K::SB) MM_CUDA_TRY(cudaFreeAsync(a.scratch, st));
