@@ -52,6 +52,11 @@ template <class F, int LOGL> struct NTr {
     enum { v = (GoldT<F, LOGL>::v && LOGL == 13) ? 512 : NT };
 };
 
+// column kernels: 512 threads for 2^12-point Goldilocks columns (66 KiB tiles)
+template <class F, int LOGL> struct NTc {
+    enum { v = (GoldT<F, LOGL>::v && LOGL == 12) ? 512 : NT };
+};
+
 template <class F> struct Cfg;
 template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, COLC = 32, V = 4 }; };
 template <> struct Cfg<FpG> { enum { RL = 3, BUDGET = 4096, COLC = 16, V = 2 }; };
@@ -471,7 +476,8 @@ __device__ __forceinline__ void col_rows_valid(long long len, long long lin0, lo
 }
 
 template <class F, int LOGL, bool INV, class TIn, class TOut, int EPIV>
-__global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
+__global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_cols(F f, ColArgs<F> a) {
+    constexpr int NTH = NTc<F, LOGL>::v;
     typedef typename F::T T;
     typedef typename F::W W;
     typedef typename Vec<T>::type TV;
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
     constexpr int V = Vec<T>::N;
     constexpr int CV = C / V;        // vectors per tile row
     constexpr int TOT = L * CV;
-    constexpr int NV = (TOT + NT - 1) / NT;
+    constexpr int NV = (TOT + NTH - 1) / NTH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* tws = (W*)smem_raw;
     T* s = (T*)(tws + (K::TWS ? L : 0));
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
         col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
 #pragma unroll
         for (int u = 0; u < NV; u++) {
-            const int e = threadIdx.x + u * NT;
+            const int e = threadIdx.x + u * NTH;
             if (e >= TOT) continue;
             const int t = e / CV, c = (e % CV) * V;
             int nb = 16;
@@ -542,13 +548,13 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 TV buf[B];
 #pragma unroll
                 for (int u = 0; u < B; u++) {
-                    const int e = threadIdx.x + (u0 + u) * NT;
+                    const int e = threadIdx.x + (u0 + u) * NTH;
                     const int t = e / CV, c = (e % CV) * V;
                     buf[u] = __ldg((const TV*)(e < TOT && t < tfull ? tb + (unsigned)t * irs + c : (const T*)a.in));
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
-                    const int e = threadIdx.x + (u0 + u) * NT;
+                    const int e = threadIdx.x + (u0 + u) * NTH;
                     if (e >= TOT) continue;
                     const int t = e / CV, c = (e % CV) * V;
                     T v[V];
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
             }
         } else {
             col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
-            for (int e = threadIdx.x; e < L * C; e += NT) {
+            for (int e = threadIdx.x; e < L * C; e += NTH) {
                 const int t = e / C, c = e % C;
                 T v = 0;
                 if (t < tfull || (t < tzero && (long long)t * a.n1 + lin0 + c < a.in_len))
@@ -578,7 +584,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
             }
         }
         __syncthreads();
-        run_tile<F, Lay, LOGL, INV>(f, cur, tw, a.lvl);
+        run_tile<F, Lay, LOGL, INV, NTH>(f, cur, tw, a.lvl);
         col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
         TOut* outb = (TOut*)a.out + b * a.out_bs + cl0;
         if (a.vec_out && sizeof(TOut) == sizeof(T)) {
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 W w[B][V];
 #pragma unroll
                 for (int u = 0; u < B; u++) {
-                    const int e0 = threadIdx.x + (u0 + u) * NT;
+                    const int e0 = threadIdx.x + (u0 + u) * NTH;
                     const int e = e0 < TOT ? e0 : 0;
                     const int t = e / CV, c = (e % CV) * V;
                     if (Lay::COL) vget<T>(*(const TV*)(cur + Lay::addr(c, t)), v[u]);
@@ -602,7 +608,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
-                    const int e = threadIdx.x + (u0 + u) * NT;
+                    const int e = threadIdx.x + (u0 + u) * NTH;
                     if (e >= TOT) continue;
                     const int t = e / CV, c = (e % CV) * V;
                     if (t >= tzero) continue;
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(NT, 4) k_cols(F f, ColArgs<F> a) {
                 }
             }
         } else {
-            for (int e = threadIdx.x; e < L * C; e += NT) {
+            for (int e = threadIdx.x; e < L * C; e += NTH) {
                 const int t = e / C, c = e % C;
                 if (t >= tzero || (t >= tfull && (long long)t * a.n1 + lin0 + c >= a.out_len)) continue;
                 W wf{};
@@ -796,7 +802,7 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     long long tiles = a.ncols / K::Lay::C * a.nbatch;
     {
         LaunchScope ls(INV ? "ntt_cols_inv" : "ntt_cols_fwd", st);
-        kern<<<grid_for(kern, smem, tiles), NT, smem, st>>>(f, a);
+        kern<<<grid_for(kern, smem, tiles, NTc<F, LOGL>::v), NTc<F, LOGL>::v, smem, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
