@@ -54,7 +54,7 @@ template <class F, int LOGL> struct NTr {
 
 // column kernels: 512 threads for 2^12-point Goldilocks columns (66 KiB tiles)
 template <class F, int LOGL> struct NTc {
-    enum { v = (GoldT<F, LOGL>::v && LOGL == 12) ? 512 : NT };
+    enum { v = (GoldT<F, LOGL>::v && LOGL >= 11) ? 512 : NT };
 };
 
 template <class F> struct Cfg;
@@ -99,7 +99,7 @@ template <class F, int LOGL> struct ColsTile {
     typedef typename F::T T;
     // Goldilocks columns of 2^11 / 2^12 points: two per tile (33 / 66 KiB) so
     // that four / three CTAs share an SM (their passes are latency-bound)
-    enum { C = GoldT<F, LOGL>::v ? 2 : InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
+    enum { C = GoldT<F, LOGL>::v ? (LOGL == 11 ? 4 : 2) : InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
     typedef typename std::conditional<
         InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>,
         typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayoutOdd<T, LOGL, C>>::type>::type Lay;
