@@ -182,7 +182,7 @@ __host__ __device__ constexpr int brev2c(int x) { return ((x & 1) << 1) | ((x >>
 template <int S, int STEP, int D, int R, int T> struct Rot {
     __device__ __forceinline__ static void run(uint64_t v[8]) {
         if constexpr (T < R) {
-            constexpr int r = R == 8 ? brev3c(T) : brev2c(T);
+            constexpr int r = R == 8 ? brev3c(T) : R == 4 ? brev2c(T) : T;
             v[T] = mulpow<S * STEP * D * r>(v[T]);
             Rot<S, STEP, D, R, T + 1>::run(v);
         }
@@ -298,11 +298,33 @@ template <int S> __device__ __forceinline__ void dit4(uint64_t v[4]) {
 __device__ __forceinline__ int brev3(int x) { return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1); }
 __device__ __forceinline__ int brev2(int x) { return ((x & 1) << 1) | ((x >> 1) & 1); }
 
+// 2-point DFT (NA = 16 tiles): (x + y, x - y), the same in both directions
+__device__ __forceinline__ void dft2(uint64_t v[2]) {
+    const uint64_t x = v[0], y = v[1];
+    v[0] = fold(add(x, y));
+    v[1] = fold(subk<2>(x, y));
+}
+
+// chunk q of the stages over the b digits -> (A, the digit d, sub-transform ct):
+// lanes take consecutive A; when NA < 32 they also span sub-transforms so that
+// d stays warp-uniform (rot's switch)
+template <int NA, int CT> __device__ __forceinline__ void decode_a(int q, int& A, int& d, int& ct) {
+    A = q % NA;
+    if constexpr (NA >= 32) {
+        d = (q / NA) & 7;
+        ct = q / (NA * 8);
+    } else {
+        static_assert(NA * CT >= 32 && CT % (32 / NA) == 0, "warp-uniform digit needs 32 / NA sub-transforms");
+        ct = (q / NA) % CT;
+        d = (q / (NA * CT)) & 7;
+    }
+}
+
 // ---------------------------------------------------------------- tile passes
 // One length-LN sub-transform per (c, h): element j of it at Lay::addr(c, h*LN + j);
 // full[TS * e] = w_LN^e (natural powers, e < LN); the 64-th roots w_64^e = 2^(S e)
 // are shifts (rot), the digit they depend on being warp-uniform.
-// LN = NA * 64 with NA in {32, 64}; RA = NA / 8.
+// LN = NA * 64 with NA in {16, 32, 64}; RA = NA / 8.
 template <class Lay, int LN, int H, int NT, int S>
 __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__ full, int TS, int LQ) {
     constexpr int NA = LN / 64, RA = NA / 8, C = Lay::C;
@@ -316,7 +338,8 @@ __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__
 #pragma unroll
         for (int t = 0; t < RA; t++) v[t] = p0[Lay::off(512 * t)];
         if constexpr (RA == 8) dif8<S>(v);
-        else dif4<S>(v);
+        else if constexpr (RA == 4) dif4<S>(v);
+        else dft2(v);
         rot<S, 8 / RA, RA>(v, al);      // w_NA^(al r), al warp-uniform
 #pragma unroll
         for (int t = 0; t < RA; t++) p0[Lay::off(512 * t)] = v[t];
@@ -331,7 +354,7 @@ __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__
 #pragma unroll
         for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(64 * t)];
         dif8<S>(v);
-        const int r = RA == 8 ? brev3(P) : brev2(P);
+        const int r = RA == 8 ? brev3(P) : RA == 4 ? brev2(P) : P;
 #pragma unroll
         for (int t = 0; t < 8; t++) {
             const int ka = r + RA * brev3(t);
@@ -343,7 +366,8 @@ __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__
     __syncthreads();
     // stage C: 8-point DFTs over bh (j = 64 A + 8 bh + bl), then w_64^(bl r)
     for (int q = threadIdx.x; q < CT * NA * 8; q += NT) {
-        const int A = q % NA, bl = (q / NA) & 7, ct = q / (NA * 8);
+        int A, bl, ct;
+        decode_a<NA, CT>(q, A, bl, ct);
         const int c = ct / H, h = ct % H;
         uint64_t* p0 = s + Lay::addr(c, h * LN + 64 * A + bl);
         uint64_t v[8];
@@ -357,7 +381,8 @@ __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__
     __syncthreads();
     // stage D: 8-point DFTs over bl (j = 64 A + 8 P + bl)
     for (int q = threadIdx.x; q < CT * NA * 8; q += NT) {
-        const int A = q % NA, P = (q / NA) & 7, ct = q / (NA * 8);
+        int A, P, ct;
+        decode_a<NA, CT>(q, A, P, ct);
         const int c = ct / H, h = ct % H;
         uint64_t* p0 = s + Lay::addr(c, h * LN + 64 * A + 8 * P);
         uint64_t v[8];
@@ -376,7 +401,8 @@ __device__ __forceinline__ void dit_ln(uint64_t* s, const uint64_t* __restrict__
     constexpr int CT = C * H;
     // stage D': inverse 8-point over the bl digit
     for (int q = threadIdx.x; q < CT * NA * 8; q += NT) {
-        const int A = q % NA, P = (q / NA) & 7, ct = q / (NA * 8);
+        int A, P, ct;
+        decode_a<NA, CT>(q, A, P, ct);
         const int c = ct / H, h = ct % H;
         uint64_t* p0 = s + Lay::addr(c, h * LN + 64 * A + 8 * P);
         uint64_t v[8];
@@ -389,7 +415,8 @@ __device__ __forceinline__ void dit_ln(uint64_t* s, const uint64_t* __restrict__
     __syncthreads();
     // stage C': w_64^-(bl r) then inverse 8-point over bh
     for (int q = threadIdx.x; q < CT * NA * 8; q += NT) {
-        const int A = q % NA, bl = (q / NA) & 7, ct = q / (NA * 8);
+        int A, bl, ct;
+        decode_a<NA, CT>(q, A, bl, ct);
         const int c = ct / H, h = ct % H;
         uint64_t* p0 = s + Lay::addr(c, h * LN + 64 * A + bl);
         uint64_t v[8];
@@ -409,7 +436,7 @@ __device__ __forceinline__ void dit_ln(uint64_t* s, const uint64_t* __restrict__
         uint64_t v[8];
 #pragma unroll
         for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(64 * t)];
-        const int r = RA == 8 ? brev3(P) : brev2(P);
+        const int r = RA == 8 ? brev3(P) : RA == 4 ? brev2(P) : P;
 #pragma unroll
         for (int t = 0; t < 8; t++) {
             const int ka = r + RA * brev3(t);
@@ -430,7 +457,8 @@ __device__ __forceinline__ void dit_ln(uint64_t* s, const uint64_t* __restrict__
         for (int t = 0; t < RA; t++) v[t] = p0[Lay::off(512 * t)];
         rot<S, 8 / RA, RA>(v, al);
         if constexpr (RA == 8) dit8<S>(v);
-        else dit4<S>(v);
+        else if constexpr (RA == 4) dit4<S>(v);
+        else dft2(v);
 #pragma unroll
         for (int t = 0; t < RA; t++) p0[Lay::off(512 * t)] = v[t];
     }

@@ -25,7 +25,7 @@ constexpr size_t SMEM_MAX = 227 * 1024;  // max dynamic shared memory per CTA on
 // Goldilocks tiles of 2^11..2^13 points run gold.cuh's 8-point split with
 // delayed reduction (shared-memory layout: one pad word per 64 elements)
 template <class F, int LOGL> struct GoldT {
-    enum { v = std::is_same<F, FpG>::value && LOGL >= 11 && LOGL <= 13 };
+    enum { v = std::is_same<F, FpG>::value && LOGL >= 10 && LOGL <= 13 };
 };
 template <class T, int LOGL, int C_> struct RowLayoutG {
     static constexpr int L = 1 << LOGL;

@@ -281,7 +281,7 @@ def test_ntt_c4_sampled(mm, O):
     assert torch.equal(z.view(torch.int64), x.view(torch.int64))
 
 
-@pytest.mark.parametrize("k", [11, 12, 22, 23])
+@pytest.mark.parametrize("k", [10, 11, 12, 20, 22, 23])
 @pytest.mark.parametrize("e", [1, 3, 65])
 def test_ntt64_gold_and_generic_tiles(mm, O, k, e):
     # 2^11 / 2^12 / 2^13 Goldilocks tiles run gold.cuh when w^(n/64) = 2^39 (e = 1,
@@ -298,7 +298,7 @@ def test_ntt64_gold_and_generic_tiles(mm, O, k, e):
     assert np.array_equal(host(plan.inverse(yb.clone(), order=mm.BITREV)), x), (k, e)
 
 
-@pytest.mark.parametrize("k", [11, 12, 13, 24])
+@pytest.mark.parametrize("k", [10, 11, 12, 13, 20, 24])
 def test_ntt64_gold_extreme_rows(mm, O, k):
     # closed forms through the Goldilocks tiles: delta_0 -> ones, constant p - 1 ->
     # (n (p-1), 0, ...), zeros -> zeros, delta_1 -> w^i; the all-(p-1) row drives
