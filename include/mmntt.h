@@ -107,7 +107,7 @@ mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, 
  * (32-bit) or 26 (64-bit).
  * `batch` independent transforms, rows contiguous with row stride n elements
  * (uint32 for 32-bit, uint64 for 64-bit).
- * Transforms of length <= 2^12 run as one shared-memory pass per row;
+ * Transforms of length <= 2^12 (2^13 for 64-bit) run as one shared-memory pass per row;
  * longer ones use Algorithm 1 with l = n as a two-pass four-step
  * n = n2 x n1 (column pass + twiddle, row pass).
  * Creating a plan builds the twiddle tables on the device (one sync). */

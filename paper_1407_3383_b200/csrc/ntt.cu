@@ -988,7 +988,8 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
     P->omega = omega;
     P->k = log2n;
     P->batch = batch;
-    if (log2n <= MAX_BLOCK_LOG) {
+    // Goldilocks rows of 2^13 points run in one pass (512-thread CTAs, gold.cuh)
+    if (log2n <= (word_bits == 64 ? MAX_BLOCK_LOG + 1 : MAX_BLOCK_LOG)) {
         P->k1 = log2n;
         P->k2 = 0;
     } else {
@@ -1672,7 +1673,8 @@ extern "C" mm_status mm_ntt_inverse(const mm_ntt_plan* plan, const void* in, voi
 
 static mm_status dist_check(const mm_ntt_plan* P, const void* in, void* out, size_t off, size_t cnt, bool cols) {
     if (!P || !in || !out) return set_err(MM_E_ARG, "null argument");
-    if (P->k2 == 0) return set_err(MM_E_UNSUPPORTED_SIZE, "four-step blocks need log2n > %d", MAX_BLOCK_LOG);
+    if (P->k2 == 0) return set_err(MM_E_UNSUPPORTED_SIZE, "four-step blocks need a two-pass plan (log2n > %d)",
+                                   P->word_bits == 64 ? MAX_BLOCK_LOG + 1 : MAX_BLOCK_LOG);
     if (P->word_bits == 52) return set_err(MM_E_ARG, "four-step blocks are built for 32- and 64-bit plans");
     size_t lim = cols ? (1ull << P->k1) : (1ull << P->k2);
     if (cnt == 0 || off + cnt > lim) return set_err(MM_E_ARG, "block [%zu, %zu) out of range %zu", off, off + cnt, lim);
