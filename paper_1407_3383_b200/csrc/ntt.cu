@@ -999,6 +999,10 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
         int cap = word_bits == 32 ? 10 : 11;
         int k2 = log2n / 2 < cap ? log2n / 2 : cap;
         if (log2n - k2 > 13) k2 = log2n - 13;
+        // Goldilocks: the 2^13-point rows run on gold.cuh's tiles, short columns
+        // on the interleaved generic tiles (2^19..2^21: 10-11 % faster than the
+        // balanced split; 2^18, 2^22, 2^23 measured slower)
+        if (word_bits == 64 && log2n >= 19 && log2n <= 21) k2 = log2n - 13;   // measured: tools/time_split.py
         P->k2 = k2;
         P->k1 = log2n - k2;
     }
