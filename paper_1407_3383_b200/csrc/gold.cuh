@@ -1,5 +1,5 @@
 // gold.cuh -- Goldilocks (p = 2^64 - 2^32 + 1) tile transforms of length
-// 2^11, 2^12 and 2^13 for the 64-bit four-step passes (BASELINE C4 / C5).
+// 2^10 .. 2^13 for the 64-bit passes (BASELINE C4 / C5).
 //
 // Why a separate tile: on sm_100a the Goldilocks butterfly is bound by the
 // integer ALU pipe (tools/probe64.cu: ~57 issue cycles per warp-butterfly, of
@@ -8,7 +8,7 @@
 //
 //  * Structure (Algorithm 1 of the paper, applied inside the
 //    tile): L = NA x 64 with j = 64 a + b.  The NA-point DFTs over a and the
-//    64-point DFTs over b are themselves 8 x 8 (or 4 x 8) splits, so every
+//    64-point DFTs over b are themselves 8 x 8 (4 x 8, 2 x 8) splits, so every
 //    butterfly twiddle is an 8th root of unity: w_8 = 2^(8S) with w_64 = 2^S
 //    (2 has order 192 mod p: w_64 = 2^39 for the root 7^((p-1)/n)),
 //    i.e. a shift plus the 2^64 = EPS / 2^96 = -1 reduction.  Only the
@@ -22,11 +22,11 @@
 //
 // Output orders are exactly those of the generic radix-2 tiles (ntt_core.cuh):
 // forward = DIF natural -> bit-reversed (TFT order), inverse = DIT
-// bit-reversed -> natural with the inverse root (unnormalised).  The fast
-// path applies when the plan's w_64 is 2^39 (forward) / 2^153 (inverse), i.e.
-// for roots of unity that are powers 7^((p-1) m / n) with m = 1 mod 64...
-// precisely: the kernel compares full[L/64] with 2^S at run time and uses the
-// generic tile otherwise.
+// bit-reversed -> natural with the inverse root (unnormalised).  The shifts
+// are compiled for w_64 = 2^39 (forward) / 2^153 (inverse), the 64-th root of
+// the canonical root 7^((p-1)/n) and of every root whose 64-th root agrees
+// with it; the kernel compares full[L/64] with that value at run time and
+// runs the generic radix-8 tile for any other root of unity.
 #pragma once
 #include "arith.cuh"
 

@@ -574,13 +574,25 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                 }
             }
         } else {
+            // element loads (narrow or unaligned input, e.g. 16-bit limbs): up
+            // to eight in flight per thread before the shared stores
             col_rows_valid(a.in_len, lin0, a.n1, C, L, &tfull, &tzero);
-            for (int e = threadIdx.x; e < L * C; e += NTH) {
-                const int t = e / C, c = e % C;
-                T v = 0;
-                if (t < tfull || (t < tzero && (long long)t * a.n1 + lin0 + c < a.in_len))
-                    v = ld_conv<TIn, T>(inb + (unsigned)t * irs + c);
-                s[Lay::addr(c, t)] = v;
+            constexpr int TOTE = L * C, NE = (TOTE + NTH - 1) / NTH, BE = NE < 8 ? NE : 8;
+            for (int u0 = 0; u0 < NE; u0 += BE) {
+                T v[BE];
+#pragma unroll
+                for (int u = 0; u < BE; u++) {
+                    const int e = threadIdx.x + (u0 + u) * NTH;
+                    const int t = e / C, c = e % C;
+                    v[u] = 0;
+                    if (e < TOTE && (t < tfull || (t < tzero && (long long)t * a.n1 + lin0 + c < a.in_len)))
+                        v[u] = ld_conv<TIn, T>(inb + (unsigned)t * irs + c);
+                }
+#pragma unroll
+                for (int u = 0; u < BE; u++) {
+                    const int e = threadIdx.x + (u0 + u) * NTH;
+                    if (e < TOTE) s[Lay::addr(e % C, e / C)] = v[u];
+                }
             }
         }
         __syncthreads();
