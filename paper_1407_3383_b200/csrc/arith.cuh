@@ -95,6 +95,21 @@ __device__ __forceinline__ uint32_t mul_barrett(uint32_t x, uint32_t y, const Ba
     return (uint32_t)d;
 }
 
+// Function 6 with Table 3's FULL profile folded in (m = n = 32: s = 31,
+// t = 32, h = 3): b = a >> 31 has 33 bits (bl, bh), c = (b q) >> 32 =
+// hi(bl q) + bh q exactly, d = a - c p < 4p (Proposition 1, h = 3), and the
+// h corrections become two conditional subtractions (2p, then p).
+__device__ __forceinline__ uint32_t mul_barrett_full(uint32_t x, uint32_t y, uint32_t p, uint32_t q) {
+    const uint64_t a = (uint64_t)x * y;
+    const uint32_t bl = (uint32_t)(a >> 31), bh = (uint32_t)(a >> 63);
+    const uint64_t c = (uint64_t)__umulhi(bl, q) + (bh ? (uint64_t)q : 0ull);
+    uint64_t d = a - c * p;
+    const uint64_t p2 = 2ull * p;
+    d = d >= p2 ? d - p2 : d;
+    d = d >= p ? d - p : d;
+    return (uint32_t)d;
+}
+
 // Field used by the 32-bit NTT kernels (p < 2^30; lazy Harvey butterflies).
 struct Fp32 {
     typedef uint32_t T;

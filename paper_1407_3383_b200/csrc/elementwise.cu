@@ -33,7 +33,7 @@ template <int OP, bool FULL>
 __device__ __forceinline__ uint32_t apply(const ModDev& m, uint32_t x, uint32_t y, uint32_t ys) {
     if (OP == OP_ADD) return FULL ? add_full(x, y, m.p) : add_half(x, y, m.p);
     if (OP == OP_SUB) return FULL ? sub_full(x, y, m.p) : sub_half(x, y, m.p);
-    if (OP == OP_MUL_BARRETT) return mul_barrett(x, y, m.bar);
+    if (OP == OP_MUL_BARRETT) return FULL ? mul_barrett_full(x, y, m.p, m.bar.q) : mul_barrett(x, y, m.bar);
     if (OP == OP_MUL_SHOUP) return FULL ? mul_shoup_full(x, y, ys, m.p) : [&] {
         uint32_t d = mul_shoup_lazy(x, y, ys, m.p);
         return umin32(d, d - m.p);
