@@ -409,16 +409,31 @@ def extras_run(mm, torch, dev, peaks):
                                "note": "same C3 products, c rows packed at 2^16 - 1 words"}
     del a3, b3, c3
 
-    # C4: 8 x 2^24 Goldilocks forward NTT (four-step 2^12 x 2^12)
+    def kern_ms(fn, reps=5):
+        # per-family kernel time per call (library event profiler, launching stream)
+        fn()
+        torch.cuda.synchronize()
+        mm.prof_collect()
+        mm.prof_enable(True)
+        for _ in range(reps):
+            fn()
+        r = mm.prof_collect()
+        mm.prof_enable(False)
+        return {k: round(v[1] / reps, 4) for k, v in r.items()}
+
+    # C4: 8 x 2^24 Goldilocks forward NTT (four-step 2^11 columns x 2^13 rows, gold.cuh tiles)
     w24 = root_of_unity(PG, 7, 24)
     plan4 = mm.NttPlan(64, PG, 24, w24, 8)
     x4 = gen.residues_torch(gen.config_seed(4), 1, 8 << 24, PG, dev).view(torch.uint64)
     y4 = torch.empty_like(x4)
-    ms = tloop(lambda: plan4.forward(x4, out=y4, order=mm.BITREV), 10)
+    f4 = lambda: plan4.forward(x4, out=y4, order=mm.BITREV)
+    ms = tloop(f4, 10)
     bfly = 8 * (1 << 23) * 24
     gbs2 = 8 * (1 << 24) * 32 / (ms * 1e-3) / 1e9
+    inf4 = plan4.info()
     out["C4_8x2^24_goldilocks_fwd"] = {"ms": round(ms, 3), "Gbutterfly_per_s": round(bfly / (ms * 1e-3) / 1e9, 1),
-                                       "GB_per_s_2pass": round(gbs2, 1), "hbm_frac_2pass": round(gbs2 / hbm, 3)}
+                                       "GB_per_s_2pass": round(gbs2, 1), "hbm_frac_2pass": round(gbs2 / hbm, 3),
+                                       "split": f"{inf4['n2']} cols x {inf4['n1']} rows", "kernels_ms": kern_ms(f4)}
     del x4, y4, plan4
 
     # C5: 2^28-bit x 2^28-bit integer product (2^24 16-bit limbs each)
@@ -426,9 +441,11 @@ def extras_run(mm, torch, dev, peaks):
     ia = gen.limbs16_torch(gen.config_seed(5), 1, na, dev).view(torch.uint16)
     ib = gen.limbs16_torch(gen.config_seed(5), 2, na, dev).view(torch.uint16)
     ic = torch.empty(2 * na, dtype=torch.uint16, device=dev)
-    ms = tloop(lambda: mm.int_mul_u16(ia, ib, out=ic), 10)
+    f5 = lambda: mm.int_mul_u16(ia, ib, out=ic)
+    ms = tloop(f5, 10)
     out["C5_int_mul_2^28bit"] = {"ms": round(ms, 3), "Mbit_per_s": round(2 * (1 << 28) / (ms * 1e-3) / 1e6, 1),
-                                 "Gbutterfly_per_s": round(3 * (1 << 24) * 25 / (ms * 1e-3) / 1e9, 1)}
+                                 "Gbutterfly_per_s": round(3 * (1 << 24) * 25 / (ms * 1e-3) / 1e9, 1),
+                                 "kernels_ms": kern_ms(f5)}
     # polynomial matrix product (Table 15: n x n, d < 2^15 over 469762049)
     pm = {}
     for N in (8, 32):
