@@ -290,11 +290,14 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // vector loads before its shared stores.
 template <class F, class Lay, int LOGL, class TIn, int NTH = NT>
 __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long long r0, long long nrows, long long rs,
-                                          long long len, bool vec, bool perm, int seglog = 0, long long segstride = 0) {
+                                          long long len64, bool vec, bool perm, int seglog = 0, long long segstride = 0) {
     typedef typename F::T T;
     typedef typename Vec<T>::type TV;
     constexpr int L = 1 << LOGL, C = Lay::C, V = Vec<T>::N;
-    const long long rlim = nrows - r0;                        // rows of this tile that exist
+    // rows of this tile that exist and the valid prefix, clamped to the tile
+    // (32-bit compares in the per-vector tests below)
+    const int rlim = nrows - r0 < C ? (int)(nrows - r0) : C;
+    const int len = len64 < L ? (int)len64 : L;
     if (L >= V && sizeof(TIn) == sizeof(T) && vec && !perm) {
         constexpr int TOT = C * L / V;
         constexpr int NV = (TOT + NTH - 1) / NTH;
@@ -346,7 +349,7 @@ __device__ __forceinline__ void load_rows(typename F::T* s, const TIn* in, long 
 // full table: one or two 16-byte loads per vector)
 template <class F, class Lay, int LOGL, class TOut, int EPIV, int NTH = NT>
 __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, TOut* out, long long r0, long long nrows,
-                                           long long rs, long long len, bool vec, bool perm, const typename F::W* fs_full,
+                                           long long rs, long long len64, bool vec, bool perm, const typename F::W* fs_full,
                                            const typename F::W* fs_lo, const typename F::W* fs_hi, int fs_h,
                                            long long row0, int k2, const typename F::W& sc, int seglog = 0,
                                            long long segstride = 0, long long rows_per = 0) {
@@ -355,7 +358,8 @@ __device__ __forceinline__ void store_rows(const F& f, const typename F::T* s, T
     typedef typename Vec<T>::type TV;
     typedef Epi<F, EPIV> E;
     constexpr int L = 1 << LOGL, C = Lay::C, V = Vec<T>::N;
-    const long long rlim = nrows - r0;
+    const int rlim = nrows - r0 < C ? (int)(nrows - r0) : C;
+    const int len = len64 < L ? (int)len64 : L;
     const unsigned i2mask = (1u << k2) - 1;
     const unsigned i2b = (unsigned)((row0 + r0) & i2mask);
     // frequency row of tile row c (a truncated transform keeps rows_per rows per transform)
