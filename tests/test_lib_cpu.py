@@ -68,3 +68,24 @@ def test_status_codes_host_side(mm):
     assert L.mm_int_mul_u16(dummy, 1 << 33, dummy2, 1 << 33, dummy3, None) == 6
     # aliasing is rejected
     assert L.mm_int_mul_u16(dummy, 100, dummy2, 100, dummy, None) == 7
+
+
+def test_gold_shift_constants():
+    # gold.cuh compiles its 64-th-root twiddles as shifts: w_64 = 2^S_FWD for the
+    # canonical root 7^((p-1)/n), 2^S_INV for its inverse, and
+    # every 8th / 4th root used by its 8- / 4-point kernels is 2^(8S) / 2^(16S)
+    # with 2^96 = -1 (Pow2's (NEG, C) split); recomputed here with Python integers
+    src = open(os.path.join(ROOT, "paper_1407_3383_b200", "csrc", "gold.cuh")).read()
+    s_fwd = int(re.search(r"S_FWD = (\d+);", src).group(1))
+    s_inv = int(re.search(r"S_INV = (\d+);", src).group(1))
+    p = (1 << 64) - (1 << 32) + 1
+    assert pow(7, (p - 1) // 64, p) == pow(2, s_fwd, p)
+    assert pow(2, s_fwd + s_inv, p) == 1
+    assert pow(2, 96, p) == p - 1 and pow(2, 192, p) == 1 and pow(2, 64, p) == (1 << 32) - 1
+    for S in (s_fwd, s_inv):
+        for k in range(192):   # Pow2<k>: 2^k = (-1)^NEG * C with C = 2^(k mod 96) reduced
+            kr = k % 96
+            c = (1 << kr) if kr < 64 else (1 << (kr - 32)) - (1 << (kr - 64))
+            assert c < p and (c if k < 96 else (p - c) % p) == pow(2, k, p)
+        # the 8-point kernels' roots: w_8 = 2^(8S) has order 8, w_4 = 2^(16S) order 4
+        assert pow(2, 8 * S * 4, p) == p - 1 and pow(2, 16 * S * 2, p) == p - 1
