@@ -58,7 +58,7 @@ template <class F, int LOGL> struct NTc {
 };
 
 template <class F> struct Cfg;
-template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, ROWB = 4096, COLC = 32, V = 4 }; };
+template <> struct Cfg<Fp32> { enum { RL = 4, BUDGET = 8192, ROWB = 2048, COLC = 32, V = 4 }; };
 template <> struct Cfg<FpG> { enum { RL = 3, BUDGET = 4096, ROWB = 4096, COLC = 16, V = 2 }; };
 template <> struct Cfg<FpD> { enum { RL = 3, BUDGET = 4096, ROWB = 4096, COLC = 16, V = 2 }; };
 
@@ -73,7 +73,7 @@ template <class F, int LOGL> struct InterOK {
 // coalesced (the interleaved layout made every warp access touch 32 lines).
 template <class F, int LOGL> struct RowsTile {
     typedef typename F::T T;
-    // ROWB: elements per row tile (32-bit: 16 KiB, so that small batches -- C1's
+    // ROWB: elements per row tile (32-bit: 8 KiB, so that small batches -- C1's
     // 16 rows of 2^10 -- spread over more CTAs; the product tiles keep BUDGET)
     enum { C = (Cfg<F>::ROWB >> LOGL) > 0 ? (Cfg<F>::ROWB >> LOGL) : 1 };
     typedef typename std::conditional<GoldT<F, LOGL>::v, RowLayoutG<T, LOGL, C>, RowLayout<T, LOGL, C>>::type Lay;
