@@ -409,6 +409,107 @@ __global__ void __launch_bounds__(CARRY_T) k_carry16_apply(const uint64_t* __res
     }
 }
 
+// Single-pass carries (decoupled look-back): a CTA takes the next block index
+// from a ticket (so every predecessor is already running), publishes its
+// (G, P) aggregate, walks back over its predecessors' published words until an
+// inclusive prefix, publishes its own inclusive prefix and applies its carry-in
+// -- the coefficients are read once instead of twice.  status[b] = flag << 32 |
+// (G, P), flag 1 = aggregate, 2 = inclusive prefix; one 64-bit word so flag and
+// value travel together (release / acquire at gpu scope).
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__global__ void __launch_bounds__(CARRY_T) k_carry16_fused(const uint64_t* __restrict__ c, long long nc, long long nout,
+                                                           unsigned long long* status, unsigned* ticket,
+                                                           uint16_t* __restrict__ out) {
+    __shared__ uint64_t sc[C16_SM];
+    __shared__ uint32_t sh[64];
+    __shared__ uint32_t s_bid, s_cin;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const long long bid = s_bid;
+    const long long jb = bid * CARRY_B;
+    c16_stage(sc, c, nc, jb);
+    __syncthreads();
+    uint32_t w[16], g[16];
+    c16_wg(sc, w, g);
+    uint32_t acc = 2u;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const long long j = jb + 16 * threadIdx.x + e;
+        acc = gp_comb(acc, j < nout ? (g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) << 1)) : 2u);
+    }
+    {   // block aggregate
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        uint32_t x = acc;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = gp_comb(y, x);
+        }
+        if (lane == 31) sh[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            // warp 0: publish the aggregate, then look back 32 predecessors at a
+            // time (lane l reads block k - l) until an inclusive prefix appears
+            uint32_t agg = 2u;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) agg = gp_comb(agg, sh[q]);
+            if (bid == 0) {
+                if (lane == 0) {
+                    st_release64(status, (2ull << 32) | agg);
+                    s_cin = 0;
+                }
+            } else {
+                if (lane == 0) st_release64(status + bid, (1ull << 32) | agg);
+                uint32_t run = 2u;                         // identity: G = 0, P = 1
+                for (long long k = bid - 1;; k -= 32) {
+                    const long long kk = k - lane;
+                    unsigned long long v = (2ull << 32) | 2u;   // before block 0: identity, inclusive
+                    if (kk >= 0)
+                        do { v = ld_acquire64(status + kk); } while ((v >> 32) == 0);
+                    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 32) == 2);
+                    const int stop = inc ? __ffs(inc) - 1 : 31;    // nearest inclusive prefix
+                    uint32_t x2 = lane <= stop ? (uint32_t)v : 2u;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {          // far (higher lane) before near
+                        const uint32_t y = __shfl_down_sync(0xffffffffu, x2, o);
+                        if (lane + o < 32) x2 = gp_comb(y, x2);
+                    }
+                    run = gp_comb(__shfl_sync(0xffffffffu, x2, 0), run);
+                    if (inc) break;
+                }
+                if (lane == 0) {
+                    st_release64(status + bid, (2ull << 32) | gp_comb(run, agg));
+                    s_cin = run & 1u;                      // carry into the block (G of the prefix)
+                }
+            }
+        }
+        __syncthreads();
+    }
+    uint32_t C = block_carry_in(acc, s_cin, sh);
+    const long long j0 = jb + 16 * threadIdx.x;
+    uint32_t o[8];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const uint32_t limb = (w[e] + C) & 0xFFFFu;
+        C = g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) & C);
+        if (e & 1) o[e >> 1] |= limb << 16; else o[e >> 1] = limb;
+    }
+    if (j0 + 16 <= nout && ((((uintptr_t)(out + j0)) & 15) == 0)) {
+        uint4* d = (uint4*)(out + j0);
+        d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; e++)
+            if (j0 + e < nout) out[j0 + e] = (uint16_t)(o[e >> 1] >> (16 * (e & 1)));
+    }
+}
+
 // ---------------------------------------------------------------- carries over column blocks (sharded int_mul)
 // A rank of the sharded product holds coefficients c_j, j = r n1 + col0 + i
 // (row r < nrows, i < c1): one chunk of c1 consecutive j per row.  The digit
@@ -1893,20 +1994,14 @@ template <class D>
 static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D::Out* out, cudaStream_t st) {
     // digit-sum lookbehind at position j: j - 1 (carry_gp) -- every policy handles j = 0
     const long long nblk = (nout + CARRY_B - 1) / CARRY_B;
-    if constexpr (std::is_same<D, Dig16>::value) {   // shared-memory staged 16-bit limb path
+    if constexpr (std::is_same<D, Dig16>::value) {   // shared-memory staged 16-bit limb path, one pass
+        // agg holds 2 nblk + 2 words here: the look-back status words and the ticket
+        unsigned long long* status = (unsigned long long*)agg;
+        unsigned* ticket = (unsigned*)(status + nblk);
+        MM_CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)nblk * 8 + 8, st));
         {
-            LaunchScope ls("carry_reduce", st);
-            k_carry16_reduce<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg);
-        }
-        MM_LAUNCH_CHECK();
-        {
-            LaunchScope ls("carry_scan", st);
-            k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
-        }
-        MM_LAUNCH_CHECK();
-        {
-            LaunchScope ls("carry_apply", st);
-            k_carry16_apply<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg, out);
+            LaunchScope ls("carry_fused", st);
+            k_carry16_fused<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, status, ticket, out);
         }
         MM_LAUNCH_CHECK();
         return MM_OK;
@@ -1951,13 +2046,14 @@ extern "C" mm_status mm_int_mul_u16(const uint16_t* a, size_t na, const uint16_t
     // coefficient buffer (lc u64) lives after the 2 n transform buffers of the workspace
     size_t n = 1ull << k;
     void* ws = nullptr;
-    if ((s = stream_ws(st, (2 * n + lc) * 8 + 16 * 1024 * 8, &ws)) != MM_OK) return s;
+    if ((s = stream_ws(st, (2 * n + lc) * 8 + 17 * 1024 * 8, &ws)) != MM_OK) return s;
     uint64_t* coef = (uint64_t*)ws + 2 * n;
     if ((s = product_impl<FpG, uint16_t, uint64_t>(P, a, (long long)na, b, (long long)nb, coef, (long long)lc, 1, st)) !=
         MM_OK)
         return s;
     // carry propagation (evaluation at 2^16)
-    if ((long long)(nout + CARRY_B - 1) / CARRY_B > 16 * 1024 * 2) return set_err(MM_E_SIZE_OVERFLOW, "too many carry blocks");
+    if ((long long)(nout + CARRY_B - 1) / CARRY_B > 17 * 1024 - 1) return set_err(MM_E_SIZE_OVERFLOW, "too many carry blocks");
+    // coef + lc: 8-byte aligned status words of the single-pass carry (carry_run)
     return carry_run(Dig16{coef, (long long)lc}, (long long)nout, (uint32_t*)(coef + lc), c, st);
 }
 
