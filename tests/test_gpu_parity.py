@@ -560,7 +560,7 @@ def test_int_mul_random(mm, O, na, nb):
         assert np.array_equal(c, O.int_mul_schoolbook_u16(a, b))
 
 
-@pytest.mark.parametrize("N", [1, 2, 4095, 4097, 1 << 16])
+@pytest.mark.parametrize("N", [1, 2, 4095, 4097, 1 << 16, 1 << 20, 3 << 20])
 def test_int_mul_all_ffff(mm, O, N):
     # (2^(16N) - 1)^2 = [1, 0 x (N-1), 0xFFFE, 0xFFFF x (N-1)]: max carries & coefficients
     a = np.full(N, 0xFFFF, dtype=np.uint16)
