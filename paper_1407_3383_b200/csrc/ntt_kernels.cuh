@@ -52,7 +52,7 @@ template <class F, int LOGL> struct NTr {
     enum { v = (GoldT<F, LOGL>::v && LOGL == 13) ? 512 : NT };
 };
 
-// column kernels: 512 threads for 2^12-point Goldilocks columns (66 KiB tiles)
+// column kernels: 512 threads for 2^11- and 2^12-point Goldilocks columns (66 KiB tiles)
 template <class F, int LOGL> struct NTc {
     enum { v = (GoldT<F, LOGL>::v && LOGL >= 11) ? 512 : NT };
 };
@@ -99,8 +99,9 @@ template <class T, int LOGL, int C_> struct RowLayoutOdd : RowLayout<T, LOGL, C_
 };
 template <class F, int LOGL> struct ColsTile {
     typedef typename F::T T;
-    // Goldilocks columns of 2^11 / 2^12 points: two per tile (33 / 66 KiB) so
-    // that four / three CTAs share an SM (their passes are latency-bound)
+    // Goldilocks columns (latency-bound passes, sized for resident warps):
+    // four of 2^11 points (66 KiB, full 32-byte row segments) and two of 2^12
+    // (66 KiB) with 512-thread CTAs (NTc); two of 2^10 (16 KiB, 256 threads)
     enum { C = GoldT<F, LOGL>::v ? (LOGL == 11 ? 4 : 2) : InterOK<F, LOGL>::v ? Cfg<F>::COLC : 32 / (int)sizeof(T) };
     typedef typename std::conditional<
         InterOK<F, LOGL>::v, ColLayout<T, LOGL, C>,
