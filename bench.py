@@ -292,6 +292,7 @@ def extras_run(mm, torch, dev, peaks):
     # ALU probe (register-only butterflies) and per-class instruction issue rates
     b32 = mm.probe_butterfly(32, 4000)
     b64 = mm.probe_butterfly(64, 1000)
+    bg8 = mm.probe_butterfly(65, 1000)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
     issue = {}
@@ -299,6 +300,7 @@ def extras_run(mm, torch, dev, peaks):
         r = mm.probe_issue(kind, 4000)
         issue[nm] = round(r / (nsm * clk), 3)
     out["alu_probe"] = {"bfly32_G_per_s": round(b32 / 1e9, 1), "bfly64_G_per_s": round(b64 / 1e9, 1),
+                        "gold8_G_per_s": round(bg8 / 1e9, 1),
                         "warp_inst_per_clk_per_SM": issue,
                         "note": "register-resident butterflies / single-class instruction chains, full grid, "
                                 "no memory traffic; per-clk rates at the max SM clock"}
@@ -433,7 +435,10 @@ def extras_run(mm, torch, dev, peaks):
     inf4 = plan4.info()
     out["C4_8x2^24_goldilocks_fwd"] = {"ms": round(ms, 3), "Gbutterfly_per_s": round(bfly / (ms * 1e-3) / 1e9, 1),
                                        "GB_per_s_2pass": round(gbs2, 1), "hbm_frac_2pass": round(gbs2 / hbm, 3),
-                                       "split": f"{inf4['n2']} cols x {inf4['n1']} rows", "kernels_ms": kern_ms(f4)}
+                                       "split": f"{inf4['n2']} cols x {inf4['n1']} rows", "kernels_ms": kern_ms(f4),
+                                       "alu_frac_vs_gold8_probe": round(bfly / (ms * 1e-3) / bg8, 3),
+                                       "alu_note": "achieved butterflies / register-resident gold.cuh 8-point rate "
+                                                   "(the passes also carry the w_L and step-2 table products)"}
     del x4, y4, plan4
 
     # C5: 2^28-bit x 2^28-bit integer product (2^24 16-bit limbs each)

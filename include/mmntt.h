@@ -272,7 +272,8 @@ mm_status mm_ntt_inv_cols(const mm_ntt_plan *plan, const void *in, void *out, si
 unsigned long long mm_launch_count(void);
 /* Integer-issue probe (ALU roofline of the butterfly): runs the library's own
  * 32-bit (word_bits = 32, radix-16 Shoup/Harvey DIF) or Goldilocks (64,
- * radix-8) butterfly on register-resident data, `iters` rounds per thread over
+ * radix-8 FpG::dif; 65: gold.cuh's 8-point split with shift twiddles and
+ * delayed reduction) butterfly on register-resident data, `iters` rounds per thread over
  * a full grid, with no memory traffic.  Returns the kernel time (*ms, CUDA
  * events on `stream`, synchronises) and the butterfly count (*bfly). */
 mm_status mm_probe_butterfly(int word_bits, int iters, double *ms, double *bfly, void *stream);

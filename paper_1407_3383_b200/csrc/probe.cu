@@ -8,6 +8,7 @@
 // mm_probe_butterfly64: the same for the Goldilocks butterfly (radix 8).
 #include "common.h"
 #include "arith.cuh"
+#include "gold.cuh"
 
 namespace mm {
 
@@ -57,6 +58,20 @@ __global__ void __launch_bounds__(256) k_probe_bfly64(int iters, uint64_t* sink)
     uint64_t acc = 0;
 #pragma unroll
     for (int t = 0; t < R; t++) acc ^= v[t];
+    if (acc == 0x12345678ull) sink[0] = acc;
+}
+
+// gold.cuh's 8-point Goldilocks DIF (shift twiddles, 3-word delayed
+// reduction) on register-resident values: the ALU ceiling of C4 / C5's tiles
+// (12 butterflies per call; no memory traffic, no table products)
+__global__ void __launch_bounds__(256) k_probe_gold8(int iters, uint64_t* sink) {
+    uint64_t v[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) v[t] = (uint64_t)(threadIdx.x * 2654435761u + t + blockIdx.x) * 0x9E3779B97F4A7C15ull;
+    for (int it = 0; it < iters; it++) gold::dif8<gold::S_FWD>(v);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++) acc ^= v[t];
     if (acc == 0x12345678ull) sink[0] = acc;
 }
 
@@ -174,6 +189,9 @@ extern "C" mm_status mm_probe_butterfly(int word_bits, int iters, double* ms, do
             f.pinv = inv_mod_2_32(f.p);
             k_probe_bfly32<16><<<blocks, threads, 0, st>>>(f, make_uint2(12345u, 67890u), iters, (uint32_t*)sink);
             per_iter = 32.0;
+        } else if (word_bits == 65) {      // Goldilocks 8-point split (gold.cuh)
+            k_probe_gold8<<<blocks, threads, 0, st>>>(iters, (uint64_t*)sink);
+            per_iter = 12.0;
         } else {
             k_probe_bfly64<8><<<blocks, threads, 0, st>>>(iters, (uint64_t*)sink);
             per_iter = 12.0;
