@@ -11,7 +11,10 @@
  *    duration of the stream-ordered work it enqueues.
  *  - Every compute call is asynchronous on `stream` (a cudaStream_t, passed as
  *    void* so this header needs no CUDA include; NULL = legacy default
- *    stream).  Only the *_create calls synchronise the device.
+ *    stream).  Only the *_create / *_destroy / setup calls synchronise the
+ *    device (and, under MMNTT_DEBUG=1, the range checks the stream).
+ *    Temporaries and per-stream workspaces are stream-ordered allocations
+ *    (cudaMallocAsync), so calls on different streams never share scratch.
  *  - Residues are canonical: inputs must lie in [0, p) ("stored as
  *    their representative in {0, ..., p-1}"), outputs always do.  Inputs are
  *    trusted unless the environment variable MMNTT_DEBUG=1 is set, in which
@@ -49,6 +52,7 @@ typedef enum { MM_MUL_BARRETT = 0, MM_MUL_SHOUP = 1, MM_MUL_MONTGOMERY = 2 } mm_
 typedef enum { MM_ORDER_NATURAL = 0, MM_ORDER_BITREV = 1 } mm_order;
 
 typedef struct mm_mod32 mm_mod32;
+typedef struct mm_mod64 mm_mod64;
 typedef struct mm_modf64 mm_modf64;
 typedef struct mm_ntt_plan mm_ntt_plan;
 
@@ -98,6 +102,24 @@ mm_status mm_to_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, si
 mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, size_t n, void *stream);
 
 /* ------------------------------------------------------------------------
+ * 64-bit modulus context (SURVEY §8(b) mm_mod64_create; BASELINE C4 / C5's
+ * p = 2^64 - 2^32 + 1, the only 64-bit modulus of this build, else
+ * MM_E_INVALID_MODULUS).  The paper's 64-bit reductions are the generic
+ * Barrett / Montgomery forms at m = n = 64; this modulus has the
+ * special reduction 2^64 = 2^32 - 1, 2^96 = -1 (mod p) (R11).
+ *   mm_modadd_u64 / mm_modsub_u64 / mm_modmul_u64 : z_i = (x_i op y_i) rem p
+ * over n uint64 residues in [0, p) (canonical outputs), device pointers,
+ * async on stream, in place allowed, MMNTT_DEBUG=1 range-checks the inputs. */
+mm_status mm_mod64_create(uint64_t p, mm_mod64 **ctx);
+void mm_mod64_destroy(mm_mod64 *ctx);
+mm_status mm_modadd_u64(const mm_mod64 *ctx, const uint64_t *x, const uint64_t *y, uint64_t *z, size_t n,
+                        void *stream);
+mm_status mm_modsub_u64(const mm_mod64 *ctx, const uint64_t *x, const uint64_t *y, uint64_t *z, size_t n,
+                        void *stream);
+mm_status mm_modmul_u64(const mm_mod64 *ctx, const uint64_t *x, const uint64_t *y, uint64_t *z, size_t n,
+                        void *stream);
+
+/* ------------------------------------------------------------------------
  * Batched NTT plans.
  * FFT_w of length n = 2^log2n: out_i = sum_j w^(i j) in_j.
  *   word_bits = 32: p an odd prime < 2^30 (lazy butterflies in [0, 4p));
@@ -118,8 +140,10 @@ mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, 
 mm_status mm_ntt_plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch,
                              mm_ntt_plan **plan);
 void mm_ntt_plan_destroy(mm_ntt_plan *plan);
-/* out[0..3] = {n1 (row length), n2 (column length), passes, workspace bytes} */
-mm_status mm_ntt_plan_info(const mm_ntt_plan *plan, uint64_t out[4]);
+/* out[0..5] = {n1 (row length), n2 (column length), passes, 0 (plans hold no
+ * workspace: NATURAL-order four-step calls permute through a stream-ordered
+ * temporary), word_bits, batch} */
+mm_status mm_ntt_plan_info(const mm_ntt_plan *plan, uint64_t out[6]);
 
 /* Forward: in (natural order) -> out in `order`:
  *   MM_ORDER_NATURAL: out[i] = ahat_i;  MM_ORDER_BITREV: out[i] = ahat_{[i]_k},
@@ -177,6 +201,55 @@ void mm_modf64_destroy(mm_modf64 *ctx);
 mm_status mm_modadd_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
 mm_status mm_modsub_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
 mm_status mm_modmul_f64(const mm_modf64 *ctx, const double *x, const double *y, double *z, size_t n, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Numeric reductions in float / double (paper §3.2-3.3; SURVEY
+ * §8(f) item 3): residues of an odd p held as integral floats (fbits = 32,
+ * trailing field l = 23) or doubles (fbits = 64, l = 52); m = bit size of p
+ * (p < 2^m); u = 1.0 / p rounded to nearest, u-bar = 1.0 / p rounded
+ * toward +inf.  The GPU rounds per instruction, so "the current
+ * rounding mode" of the paper is the mode of every operation of the variant.
+ *   MM_NUM_F14      Function 14, u, to nearest, both corrections;
+ *                   m <= l/2 (double 26, float 11), inputs a < 2^(l/2) p.
+ *   MM_NUM_F14_UP   Function 14 with u-bar, every operation toward +inf,
+ *                   line 4 dropped (Proposition 10).
+ *   MM_NUM_F15_UP   Function 15: u-bar, toward +inf, no correction
+ *                   (Proposition 11); m <= (l-1)/2 (double 25, float 11),
+ *                   inputs a < 2^floor((l-1)/2) p.
+ *   MM_NUM_F15_NEAR Function 15 in round-to-nearest (Remark 12): only
+ *                   for p prime and a = x y with x, y residues (mulmod only).
+ *   MM_NUM_F16      Function 16, u, to nearest; m <= l - 2
+ *                   (double 50, float 21) -- the product of mm_modmul_f64.
+ *   MM_NUM_F16_UP   Function 16 with u-bar, toward +inf, line 7 dropped
+ *                   (Proposition 13).
+ * mm_modnum_create : p odd >= 3 with m <= l - 2 (else MM_E_INVALID_MODULUS /
+ *     MM_E_PROFILE); a variant whose bound m exceeds returns MM_E_PROFILE at
+ *     the call.  *ctx owned by the library.
+ * mm_modnum_info   : out[0..5] = {p, u, u-bar, l, m, fbits}.
+ * mm_mulmod_num    : z_i = (x_i y_i) rem p for residues x_i, y_i in [0, p)
+ *     (F14 / F15 on the exact product a = x y, 2m <= l; F16 on the factors).
+ * mm_reduce_num    : z_i = a_i rem p for integral a_i in [0, alpha p)
+ *     (F14 / F14_UP / F15_UP only; MM_E_ARG for F16, MM_E_INVALID_MODULUS
+ *     for F15_NEAR).
+ * Device vectors of float (fbits 32) or double (64), n elements, async on
+ * stream, in place allowed; 16-byte aligned vectors take 128-bit accesses.
+ * Inputs are trusted unless MMNTT_DEBUG=1 (then out-of-domain inputs return
+ * MM_E_RANGE; that check synchronises the stream). */
+typedef enum {
+    MM_NUM_F14 = 0,
+    MM_NUM_F14_UP = 1,
+    MM_NUM_F15_UP = 2,
+    MM_NUM_F15_NEAR = 3,
+    MM_NUM_F16 = 4,
+    MM_NUM_F16_UP = 5
+} mm_num_variant;
+typedef struct mm_modnum mm_modnum;
+mm_status mm_modnum_create(int fbits, uint64_t p, mm_modnum **ctx);
+void mm_modnum_destroy(mm_modnum *ctx);
+mm_status mm_modnum_info(const mm_modnum *ctx, double out[6]);
+mm_status mm_mulmod_num(const mm_modnum *ctx, mm_num_variant v, const void *x, const void *y, void *z, size_t n,
+                        void *stream);
+mm_status mm_reduce_num(const mm_modnum *ctx, mm_num_variant v, const void *a, void *z, size_t n, void *stream);
 
 /* Truncated product (Algorithm 1 with l < n):
  * the same c = a b mod p as mm_poly_mul (32-bit p < 2^30, packed rows),
@@ -310,10 +383,12 @@ mm_status mm_ntt_inv_rows_seg(const mm_ntt_plan *plan, const void *in, void *out
  * orders all ranks' writes before the row pass. */
 mm_status mm_ntt_fwd_cols_p2p(const mm_ntt_plan *plan, const void *in, void *const *peer_recv, int G, int rank,
                               size_t col0, size_t ncols, void *stream);
-/* CUDA IPC plumbing for it: a 64-byte handle of a device allocation, opened
- * in another process of the same node as a peer pointer (lazy peer access),
- * closed when done. */
-mm_status mm_ipc_get_handle(const void *dev_ptr, void *handle_out);
+/* CUDA IPC plumbing for it: mm_ipc_get_handle writes the 64-byte handle of
+ * the cudaMalloc allocation that contains dev_ptr and dev_ptr's byte offset
+ * inside it (caching allocators place buffers at offsets); another process
+ * of the same node opens the handle (lazy peer access, the allocation base)
+ * and adds the offset; mm_ipc_close takes the opened base. */
+mm_status mm_ipc_get_handle(const void *dev_ptr, void *handle_out, uint64_t *offset_out);
 mm_status mm_ipc_open_handle(const void *handle, void **dev_ptr);
 mm_status mm_ipc_close(void *dev_ptr);
 
@@ -351,6 +426,57 @@ mm_status mm_carry_chunks_apply(const uint64_t *coef, const uint64_t *halo_in, s
                                 size_t col0, size_t nc, size_t nout, int shift, const uint32_t *cin, uint16_t *out,
                                 void *stream);
 
+
+/* ------------------------------------------------------------------------
+ * Distributed transform and integer product (Algorithm 1
+ * split across the GPUs of one node: "a critical point in large
+ * sizes becomes the matrix transposition", P:925 -- here an all-to-all).
+ * One process per GPU.  NCCL is not linked: libnccl.so.2 is dlopen'ed (the
+ * copy torch already loaded), MM_E_NCCL if it cannot be.
+ *   mm_dist_unique_id : 128-byte NCCL unique id (rank 0; the caller
+ *       broadcasts it, e.g. over torch.distributed).
+ *   mm_dist_create    : communicator of `world` <= 8 ranks on the current
+ *       device; *d owned by the library (mm_dist_destroy).  Collective.
+ *   mm_dist_info      : out = {rank, world, p2p receive-buffer bytes (0 = NCCL
+ *       transport), NCCL version code}.
+ *   mm_dist_p2p_enable: setup (collective, synchronises): two receive buffers
+ *       of `bytes` and a flag page in one cudaMalloc, IPC handles all-gathered,
+ *       peers opened.  Afterwards mm_ntt_forward_dist uses the fused transpose
+ *       (mm_ntt_fwd_cols_p2p stores rows into the peers' receive buffers over
+ *       NVLink) ordered by device-side flags (release / acquire at system
+ *       scope), no all-to-all and no host barrier, whenever a column block
+ *       fits `bytes`.
+ *   mm_dist_p2p_status: 0, or 1 + the flag slot of a device-side wait that
+ *       timed out (~20 s: a peer stopped); synchronises the device.
+ * Plans: four-step (log2n > 12, 32-bit; > 13, 64-bit), batch 1, with n1 and
+ * n2 divisible by world.  Rank g of G, c1 = n1 / G, r2 = n2 / G:
+ *   mm_ntt_forward_dist : local_in = [n2][c1] column block (natural input
+ *       element j2 n1 + j1, j1 in [g c1, (g+1) c1)); local_out = [r2][n1] row
+ *       block = positions [g r2 n1, (g+1) r2 n1) of the TFT-order output
+ *       (position i holds ahat_{[i]_k}).
+ *   mm_ntt_inverse_dist : the reverse (row block in, column block out, n^-1).
+ *   mm_int_mul_u16_dist : a (na limbs), b (nb limbs) whole on every rank (2 B
+ *       per limb); the product of mm_int_mul_u16 with one all-to-all per
+ *       operand and one back, carries by a ring halo exchange and an
+ *       all-gather of per-chunk (generate, propagate) pairs; local_c =
+ *       [n2][c1] limbs, element (r, i) = limb r n1 + g c1 + i of a b (0 beyond
+ *       na + nb).  mm_int_mul_u16_dist_layout gives {n1, n2, c1, log2 n}.
+ * Workspaces are stream-ordered allocations; all calls are asynchronous on
+ * `stream` and collective (every rank calls them in the same order). */
+typedef struct mm_dist mm_dist;
+mm_status mm_dist_unique_id(void *id_out);
+mm_status mm_dist_create(const void *nccl_unique_id, int rank, int world, mm_dist **d);
+void mm_dist_destroy(mm_dist *d);
+mm_status mm_dist_info(const mm_dist *d, int64_t out[4]);
+mm_status mm_dist_p2p_enable(mm_dist *d, size_t bytes);
+mm_status mm_dist_p2p_status(mm_dist *d, uint64_t *slot);
+mm_status mm_ntt_forward_dist(mm_dist *d, const mm_ntt_plan *plan, const void *local_in, void *local_out,
+                              void *stream);
+mm_status mm_ntt_inverse_dist(mm_dist *d, const mm_ntt_plan *plan, const void *local_in, void *local_out,
+                              void *stream);
+mm_status mm_int_mul_u16_dist(mm_dist *d, const uint16_t *a, size_t na, const uint16_t *b, size_t nb,
+                              uint16_t *local_c, void *stream);
+mm_status mm_int_mul_u16_dist_layout(mm_dist *d, size_t na, size_t nb, uint64_t out[4]);
 
 #ifdef __cplusplus
 }

@@ -18,12 +18,13 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "ModF64", "NttPlan", "poly_mul", "poly_mul_tft", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "Mod64", "ModF64", "ModNum", "Dist", "NttPlan", "poly_mul", "poly_mul_tft", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
 MUL_BARRETT, MUL_SHOUP, MUL_MONTGOMERY = 0, 1, 2
 NATURAL, BITREV = 0, 1
+NUM_F14, NUM_F14_UP, NUM_F15_UP, NUM_F15_NEAR, NUM_F16, NUM_F16_UP = range(6)
 
 _P = ctypes.c_void_p
 _u32, _u64, _i32, _sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_size_t
@@ -64,7 +65,7 @@ EXPORTS = {
     "mm_ntt_fwd_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_rows": (_ST, [_P, _P, _P, _sz, _sz, _P]),
     "mm_ntt_inv_cols": (_ST, [_P, _P, _P, _sz, _sz, _P]),
-    "mm_ipc_get_handle": (_ST, [_P, _P]),
+    "mm_ipc_get_handle": (_ST, [_P, _P, ctypes.POINTER(_u64)]),
     "mm_ipc_open_handle": (_ST, [_P, ctypes.POINTER(_P)]),
     "mm_ipc_close": (_ST, [_P]),
     "mm_ntt_fwd_cols_p2p": (_ST, [_P, _P, _P, _i32, _i32, _sz, _sz, _P]),
@@ -77,6 +78,26 @@ EXPORTS = {
     "mm_ntt_fwd_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_ntt_inv_rows_seg": (_ST, [_P, _P, _P, _sz, _sz, _sz, _sz, _P]),
     "mm_launch_count": (ctypes.c_ulonglong, []),
+    "mm_modnum_create": (_ST, [_i32, _u64, ctypes.POINTER(_P)]),
+    "mm_modnum_destroy": (None, [_P]),
+    "mm_modnum_info": (_ST, [_P, ctypes.POINTER(ctypes.c_double)]),
+    "mm_mulmod_num": (_ST, [_P, _i32, _P, _P, _P, _sz, _P]),
+    "mm_reduce_num": (_ST, [_P, _i32, _P, _P, _sz, _P]),
+    "mm_mod64_create": (_ST, [_u64, ctypes.POINTER(_P)]),
+    "mm_mod64_destroy": (None, [_P]),
+    "mm_modadd_u64": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modsub_u64": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_modmul_u64": (_ST, [_P, _P, _P, _P, _sz, _P]),
+    "mm_dist_unique_id": (_ST, [_P]),
+    "mm_dist_create": (_ST, [_P, _i32, _i32, ctypes.POINTER(_P)]),
+    "mm_dist_destroy": (None, [_P]),
+    "mm_dist_info": (_ST, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "mm_dist_p2p_enable": (_ST, [_P, _sz]),
+    "mm_dist_p2p_status": (_ST, [_P, ctypes.POINTER(_u64)]),
+    "mm_ntt_forward_dist": (_ST, [_P, _P, _P, _P, _P]),
+    "mm_ntt_inverse_dist": (_ST, [_P, _P, _P, _P, _P]),
+    "mm_int_mul_u16_dist": (_ST, [_P, _P, _sz, _P, _sz, _P, _P]),
+    "mm_int_mul_u16_dist_layout": (_ST, [_P, _sz, _sz, ctypes.POINTER(_u64)]),
     "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_probe_issue": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_prof_enable": (None, [_i32]),
@@ -145,6 +166,25 @@ def _esz(t: torch.Tensor) -> int:
     return t.element_size()
 
 
+def _need(t: torch.Tensor | None, numel: int, esize: int, name: str, like: torch.Tensor | None = None):
+    """Argument check before a C call (the C ABI cannot see buffer lengths):
+    a contiguous CUDA tensor of `numel` elements of `esize` bytes on the same
+    device as `like`; raises ValueError otherwise."""
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must live on a CUDA device (no CPU fallback)")
+    if like is not None and t.device != like.device:
+        raise ValueError(f"{name} is on {t.device}, expected {like.device}")
+    if t.element_size() != esize:
+        raise ValueError(f"{name} must have {esize}-byte elements, got {t.element_size()}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
 # ------------------------------------------------------------------ modulus context
 class ModF64:
     """Modulus context for residues held as IEEE doubles (mm_modf64_create,
@@ -166,6 +206,8 @@ class ModF64:
         if x.dtype != torch.float64 or y.dtype != torch.float64:
             raise ValueError("float64 residues expected")
         z = torch.empty_like(x) if out is None else out
+        _need(y, x.numel(), 8, "y", x)
+        _need(z, x.numel(), 8, "out", x)
         _check(getattr(lib(), name)(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
         return z
 
@@ -177,6 +219,85 @@ class ModF64:
 
     def mul(self, x, y, out=None):
         return self._run("mm_modmul_f64", x, y, out)
+
+
+class ModNum:
+    """Numeric reductions (mm_modnum_create, paper §3.2-3.3, Functions 14-16):
+    residues of an odd p held as integral float32 (fbits 32) or float64 (64)
+    values; `variant` one of NUM_F14, NUM_F14_UP, NUM_F15_UP, NUM_F15_NEAR,
+    NUM_F16, NUM_F16_UP (include/mmntt.h)."""
+
+    def __init__(self, fbits: int, p: int):
+        self.fbits, self.p = int(fbits), int(p)
+        self.dtype = torch.float64 if fbits == 64 else torch.float32
+        h = ctypes.c_void_p()
+        _check(lib().mm_modnum_create(self.fbits, self.p, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_modnum_destroy(h)
+            self._h = None
+
+    def info(self) -> dict:
+        out = (ctypes.c_double * 6)()
+        _check(lib().mm_modnum_info(self._h, out))
+        return dict(zip(["p", "u", "ubar", "l", "m", "fbits"], list(out)))
+
+    def _chk(self, x, name):
+        if x.dtype != self.dtype:
+            raise ValueError(f"{name} must be {self.dtype}")
+
+    def mul(self, x, y, variant=NUM_F16, out=None):
+        self._chk(x, "x")
+        self._chk(y, "y")
+        z = torch.empty_like(x) if out is None else out
+        _need(y, x.numel(), x.element_size(), "y", x)
+        _need(z, x.numel(), x.element_size(), "out", x)
+        _check(lib().mm_mulmod_num(self._h, int(variant), _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def reduce(self, a, variant=NUM_F14, out=None):
+        self._chk(a, "a")
+        z = torch.empty_like(a) if out is None else out
+        _need(z, a.numel(), a.element_size(), "out", a)
+        _check(lib().mm_reduce_num(self._h, int(variant), _ptr(a), _ptr(z), a.numel(), _stream(a)))
+        return z
+
+
+class Mod64:
+    """64-bit modulus context (mm_mod64_create): p = 2^64 - 2^32 + 1 only."""
+
+    def __init__(self, p: int = GOLDILOCKS):
+        self.p = int(p)
+        h = ctypes.c_void_p()
+        _check(lib().mm_mod64_create(self.p, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_mod64_destroy(h)
+            self._h = None
+
+    def _run(self, name, x, y, out):
+        if x.element_size() != 8:
+            raise ValueError("64-bit residues expected")
+        z = torch.empty_like(x) if out is None else out
+        _need(y, x.numel(), 8, "y", x)
+        _need(z, x.numel(), 8, "out", x)
+        _check(getattr(lib(), name)(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
+        return z
+
+    def add(self, x, y, out=None):
+        return self._run("mm_modadd_u64", x, y, out)
+
+    def sub(self, x, y, out=None):
+        return self._run("mm_modsub_u64", x, y, out)
+
+    def mul(self, x, y, out=None):
+        return self._run("mm_modmul_u64", x, y, out)
 
 
 class Mod32:
@@ -201,21 +322,27 @@ class Mod32:
         keys = ["p", "r", "s", "t", "h", "q", "pinv", "r2"]
         return dict(zip(keys, [int(v) for v in out]))
 
-    def _out(self, x, out):
-        return torch.empty_like(x) if out is None else out
+    def _out(self, x, out, *others):
+        if x.element_size() != 4:
+            raise ValueError("32-bit residues expected")
+        z = torch.empty_like(x) if out is None else out
+        _need(z, x.numel(), 4, "out", x)
+        for nm, t in others:
+            _need(t, x.numel(), 4, nm, x)
+        return z
 
     def add(self, x, y, out=None):
-        z = self._out(x, out)
+        z = self._out(x, out, ("y", y))
         _check(lib().mm_modadd_u32(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
         return z
 
     def sub(self, x, y, out=None):
-        z = self._out(x, out)
+        z = self._out(x, out, ("y", y))
         _check(lib().mm_modsub_u32(self._h, _ptr(x), _ptr(y), _ptr(z), x.numel(), _stream(x)))
         return z
 
     def mul(self, x, y, variant=MUL_MONTGOMERY, y_shoup=None, out=None):
-        z = self._out(x, out)
+        z = self._out(x, out, ("y", y), *((("y_shoup", y_shoup),) if variant == MUL_SHOUP else ()))
         _check(lib().mm_modmul_u32(self._h, variant, _ptr(x), _ptr(y), _ptr(y_shoup), _ptr(z), x.numel(),
                                    _stream(x)))
         return z
@@ -256,9 +383,10 @@ class NttPlan:
             self._h = None
 
     def info(self) -> dict:
-        out = (ctypes.c_uint64 * 4)()
+        out = (ctypes.c_uint64 * 6)()
         _check(lib().mm_ntt_plan_info(self._h, out))
-        return dict(n1=int(out[0]), n2=int(out[1]), passes=int(out[2]), ws_bytes=int(out[3]))
+        return dict(n1=int(out[0]), n2=int(out[1]), passes=int(out[2]), ws_bytes=int(out[3]),
+                    word_bits=int(out[4]), batch=int(out[5]))
 
     def _chk(self, x):
         if x.numel() != self.n * self.batch or _esz(x) * 8 != (32 if self.word_bits == 32 else 64):
@@ -267,12 +395,14 @@ class NttPlan:
     def forward(self, x, out=None, order=BITREV):
         self._chk(x)
         out = x if out is None else out
+        _need(out, x.numel(), x.element_size(), "out", x)
         _check(lib().mm_ntt_forward(self._h, _ptr(x), _ptr(out), order, _stream(x)))
         return out
 
     def inverse(self, x, out=None, order=BITREV):
         self._chk(x)
         out = x if out is None else out
+        _need(out, x.numel(), x.element_size(), "out", x)
         _check(lib().mm_ntt_inverse(self._h, _ptr(x), _ptr(out), order, _stream(x)))
         return out
 
@@ -385,6 +515,10 @@ def poly_mul(a: torch.Tensor, b: torch.Tensor, p: int, g: int, word_bits: int | 
         raise ValueError("batch mismatch")
     lb = b2.shape[1]
     lc = la + lb - 1
+    esz = 4 if word_bits == 32 else 8
+    for nm, t in (("a", a), ("b", b)) + ((("out", out),) if out is not None else ()):
+        if not t.is_cuda or t.device != a.device or t.element_size() != esz:
+            raise ValueError(f"{nm} must be a CUDA tensor of {esz}-byte residues on {a.device}")
     if out is None:
         out = torch.empty((batch, lc), dtype=a.dtype, device=a.device)
     o2 = out if out.dim() == 2 else out.reshape(batch, lc)
@@ -405,8 +539,12 @@ def poly_mul_tft(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.Te
     b2 = b.reshape(-1, b.shape[-1]) if b.dim() > 1 else b.reshape(1, -1)
     batch, la = a2.shape
     lb = b2.shape[1]
+    if b2.shape[0] != batch or a.element_size() != 4:
+        raise ValueError("a, b: [batch, la], [batch, lb] uint32")
+    _need(b2, batch * lb, 4, "b", a)
     if out is None:
         out = torch.empty((batch, la + lb - 1), dtype=a.dtype, device=a.device)
+    _need(out, batch * (la + lb - 1), 4, "out", a)
     _check(lib().mm_poly_mul_tft(int(p), int(g), _ptr(a2), la, _ptr(b2), lb, _ptr(out), batch, _stream(a)))
     return out if a.dim() > 1 else out.reshape(-1)
 
@@ -418,8 +556,12 @@ def poly_matmul(A: torch.Tensor, B: torch.Tensor, p: int, g: int, out: torch.Ten
         raise ValueError("expected A [m, kk, da] and B [kk, n, db]")
     m, kk, da = A.shape
     n, db = B.shape[1], B.shape[2]
+    if A.element_size() != 4:
+        raise ValueError("uint32 residues expected")
+    _need(B, kk * n * db, 4, "B", A)
     if out is None:
         out = torch.empty((m, n, da + db - 1), dtype=A.dtype, device=A.device)
+    _need(out, m * n * (da + db - 1), 4, "out", A)
     _check(lib().mm_poly_matmul(int(p), int(g), _ptr(A), _ptr(B), _ptr(out), m, kk, n, da, db, _stream(A)))
     return out
 
@@ -450,14 +592,17 @@ def poly_mul_host(a: torch.Tensor, b: torch.Tensor, p: int, g: int, out: torch.T
 
 
 # ------------------------------------------------------------------ CUDA IPC (peer-scatter path)
-def ipc_handle(t: torch.Tensor) -> bytes:
-    """64-byte CUDA IPC handle of the allocation holding t (t at its start)."""
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t
+    inside that allocation): the opener adds the offset to the opened base."""
     buf = ctypes.create_string_buffer(64)
-    _check(lib().mm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), buf))
-    return buf.raw
+    off = ctypes.c_uint64()
+    _check(lib().mm_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), buf, ctypes.byref(off)))
+    return buf.raw, int(off.value)
 
 
 def ipc_open(handle: bytes) -> int:
+    """Open a peer allocation; returns its base address in this process."""
     ptr = ctypes.c_void_p()
     _check(lib().mm_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(ptr)))
     return int(ptr.value)
@@ -498,8 +643,12 @@ def int_matmul_u32(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = 
         raise ValueError("expected A [m, kk, na] and B [kk, n, nb]")
     m, kk, na = A.shape
     n, nb = B.shape[1], B.shape[2]
+    if A.element_size() != 4:
+        raise ValueError("32-bit limbs expected")
+    _need(B, kk * n * nb, 4, "B", A)
     if out is None:
         out = torch.empty((m, n, na + nb + 1), dtype=A.dtype, device=A.device)
+    _need(out, m * n * (na + nb + 1), 4, "out", A)
     _check(lib().mm_int_matmul_u32(_ptr(A), _ptr(B), _ptr(out), m, kk, n, na, nb, _stream(A)))
     return out
 
@@ -509,15 +658,117 @@ def int_mul_u32(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = Non
     FFT (mm_int_mul_u32); na + nb limbs."""
     if a.element_size() != 4 or b.element_size() != 4:
         raise ValueError("32-bit limbs expected")
+    _need(b, b.numel(), 4, "b", a)
     if out is None:
         out = torch.empty(a.numel() + b.numel(), dtype=a.dtype, device=a.device)
+    _need(out, a.numel() + b.numel(), 4, "out", a)
     _check(lib().mm_int_mul_u32(_ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(out), _stream(a)))
     return out
 
 
 def int_mul_u16(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Exact product of little-endian 16-bit limb arrays (mm_int_mul_u16); na + nb limbs."""
+    if a.element_size() != 2:
+        raise ValueError("16-bit limbs expected")
+    _need(b, b.numel(), 2, "b", a)
     if out is None:
         out = torch.empty(a.numel() + b.numel(), dtype=a.dtype, device=a.device)
+    _need(out, a.numel() + b.numel(), 2, "out", a)
     _check(lib().mm_int_mul_u16(_ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(out), _stream(a)))
     return out
+
+
+# ------------------------------------------------------------------ distributed (C ABI, NCCL inside the library)
+class Dist:
+    """Communicator of the library's distributed calls (mm_dist_create): rank 0
+    draws an NCCL unique id (mm_dist_unique_id), torch.distributed broadcasts
+    it, every rank builds the communicator on its current device."""
+
+    def __init__(self, group=None):
+        import torch.distributed as tdist
+        self.rank = tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        idbuf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(lib().mm_dist_unique_id(idbuf))
+        obj = [idbuf.raw if self.rank == 0 else None]
+        src = tdist.get_global_rank(group, 0) if group is not None else 0
+        tdist.broadcast_object_list(obj, src=src, group=group)
+        h = ctypes.c_void_p()
+        _check(lib().mm_dist_create(ctypes.create_string_buffer(obj[0], 128), self.rank, self.world, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def single(cls):
+        """A one-rank communicator without a process group (tests, G = 1)."""
+        self = cls.__new__(cls)
+        self.rank, self.world = 0, 1
+        idbuf = ctypes.create_string_buffer(128)
+        _check(lib().mm_dist_unique_id(idbuf))
+        h = ctypes.c_void_p()
+        _check(lib().mm_dist_create(idbuf, 0, 1, ctypes.byref(h)))
+        self._h = h
+        return self
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mm_dist_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def info(self) -> dict:
+        out = (ctypes.c_int64 * 4)()
+        _check(lib().mm_dist_info(self._h, out))
+        return dict(rank=int(out[0]), world=int(out[1]), p2p_bytes=int(out[2]), nccl_version=int(out[3]))
+
+    def enable_p2p(self, nbytes: int):
+        _check(lib().mm_dist_p2p_enable(self._h, int(nbytes)))
+
+    def p2p_status(self) -> int:
+        v = ctypes.c_uint64()
+        _check(lib().mm_dist_p2p_status(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def ntt_forward(self, plan: "NttPlan", x_cols: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Column block [n2, n1/G] (natural input) -> row block [n2/G, n1] of the TFT-order output."""
+        inf = plan.info()
+        n1, n2 = inf["n1"], inf["n2"]
+        esz = 4 if plan.word_bits == 32 else 8
+        _need(x_cols, n2 * (n1 // self.world), esz, "x_cols")
+        if out is None:
+            out = torch.empty((n2 // self.world, n1), dtype=x_cols.dtype, device=x_cols.device)
+        _need(out, (n2 // self.world) * n1, esz, "out", x_cols)
+        _check(lib().mm_ntt_forward_dist(self._h, plan._h, _ptr(x_cols), _ptr(out), _stream(x_cols)))
+        return out
+
+    def ntt_inverse(self, plan: "NttPlan", y_rows: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        inf = plan.info()
+        n1, n2 = inf["n1"], inf["n2"]
+        esz = 4 if plan.word_bits == 32 else 8
+        _need(y_rows, (n2 // self.world) * n1, esz, "y_rows")
+        if out is None:
+            out = torch.empty((n2, n1 // self.world), dtype=y_rows.dtype, device=y_rows.device)
+        _need(out, n2 * (n1 // self.world), esz, "out", y_rows)
+        _check(lib().mm_ntt_inverse_dist(self._h, plan._h, _ptr(y_rows), _ptr(out), _stream(y_rows)))
+        return out
+
+    def int_mul_layout(self, na: int, nb: int) -> dict:
+        out = (ctypes.c_uint64 * 4)()
+        _check(lib().mm_int_mul_u16_dist_layout(self._h, na, nb, out))
+        return dict(n1=int(out[0]), n2=int(out[1]), c1=int(out[2]), log2n=int(out[3]))
+
+    def int_mul_u16(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Sharded a b (16-bit limbs, whole on every rank) -> this rank's [n2, c1]
+        limb block (limb r n1 + rank c1 + i at (r, i))."""
+        if a.element_size() != 2:
+            raise ValueError("16-bit limbs expected")
+        _need(b, b.numel(), 2, "b", a)
+        L = self.int_mul_layout(a.numel(), b.numel())
+        if out is None:
+            out = torch.empty((L["n2"], L["c1"]), dtype=a.dtype, device=a.device)
+        _need(out, L["n2"] * L["c1"], 2, "out", a)
+        _check(lib().mm_int_mul_u16_dist(self._h, _ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(out), _stream(a)))
+        return out

@@ -11,6 +11,7 @@
 //   Proposition 15), i.e. the TFT order with no transposition at all.
 //   The inverse runs the steps backwards with w^-1.
 #include "common.h"
+#include <cuda.h>
 #include "ntt_kernels.cuh"
 #include "fast32.h"
 #include "tft.h"
@@ -885,9 +886,6 @@ struct mm_ntt_plan {
     void* fs_pm_i = nullptr;   // inverse step-2 table times n^-1 2^32
     void* fs_ni_i = nullptr;   // inverse step-2 table times n^-1 (standalone inverse)
     mm::f32::Tw15 tw_f1, tw_i1, tw_f2, tw_i2;   // level-table entries 1..15 (host copies)
-    void* ws = nullptr;      // lazily allocated workspace (bit-mirror permutations)
-    size_t ws_bytes = 0;
-    std::mutex mu;
 };
 
 namespace mm {
@@ -1049,7 +1047,7 @@ static mm_status build_tables(mm_ntt_plan* P) {
 static void free_plan(mm_ntt_plan* P) {
     if (!P) return;
     void* bufs[] = {P->lvl_f1,  P->lvl_i1,  P->lvl_f2,    P->lvl_i2,    P->fs_lo_f, P->fs_hi_f,
-                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->fs_pm_i, P->fs_ni_i, P->ws};
+                    P->fs_lo_i, P->fs_hi_i, P->fs_full_f, P->fs_full_i, P->fs_pm_i, P->fs_ni_i};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -1121,17 +1119,18 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
     return MM_OK;
 }
 
-static mm_status ensure_ws(mm_ntt_plan* P, size_t bytes) {
-    std::lock_guard<std::mutex> g(P->mu);
-    if (P->ws_bytes >= bytes) return MM_OK;
-    if (P->ws) {
-        cudaDeviceSynchronize();
-        cudaFree(P->ws);
-        P->ws = nullptr;
-        P->ws_bytes = 0;
+// NATURAL-order transforms on the four-step path go through a bit-mirror
+// permutation of a temporary: a stream-ordered allocation
+// (cudaMallocAsync / cudaFreeAsync from the device's default pool), so the
+// plan holds no mutable workspace and calls on different streams sharing a
+// plan never touch the same buffer, and nothing here synchronises.
+template <class T>
+static mm_status bitrev_rows(const void* in, void* out, int k, long long batch, cudaStream_t st) {
+    {
+        LaunchScope ls("bitrev_permute", st);
+        k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)out, k, batch);
     }
-    MM_CUDA_TRY(cudaMalloc(&P->ws, bytes));
-    P->ws_bytes = bytes;
+    MM_LAUNCH_CHECK();
     return MM_OK;
 }
 
@@ -1154,6 +1153,14 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         a.lvl = (const W*)P->lvl_f1;
         return launch_rows<F, false, T, T>(f, a, st);
     }
+    if (order == MM_ORDER_NATURAL) {   // Algorithm 1's TFT order into a temporary, then the permutation
+        void* tmp = nullptr;
+        MM_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * P->batch * sizeof(T), st));
+        mm_status s = fwd_impl<F>(P, in, tmp, MM_ORDER_BITREV, st);
+        if (s == MM_OK) s = bitrev_rows<T>(tmp, out, P->k, (long long)P->batch, st);
+        cudaFreeAsync(tmp, st);
+        return s;
+    }
     if constexpr (sizeof(T) == 4) {
         if (P->fast16 && ((uintptr_t)out & 15) == 0) {
             // 2^16 = 256 x 256: the specialised column and row passes (ntt_fast32.cu)
@@ -1174,18 +1181,7 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
             ra.lvl = (const uint2*)P->lvl_f1;
             ra.tc = P->tw_f1;
             ra.f = ff;
-            if ((s = f32::launch_row_fwd(ra, st)) != MM_OK) return s;
-            if (order == MM_ORDER_NATURAL) {
-                size_t bytes = (size_t)n * P->batch * sizeof(T);
-                if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
-                {
-                    LaunchScope ls("bitrev_permute", st);
-                    k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)out, (T*)P->ws, P->k, (long long)P->batch);
-                }
-                MM_LAUNCH_CHECK();
-                MM_CUDA_TRY(cudaMemcpyAsync(out, P->ws, bytes, cudaMemcpyDeviceToDevice, st));
-            }
-            return MM_OK;
+            return f32::launch_row_fwd(ra, st);
         }
     }
     // column pass: in -> out, then row pass: out -> out (bit-mirrored result)
@@ -1215,18 +1211,7 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     a.k = P->k1;
     a.canon = 1;
     a.lvl = (const W*)P->lvl_f1;
-    if ((s = launch_rows<F, false, T, T>(f, a, st)) != MM_OK) return s;
-    if (order == MM_ORDER_NATURAL) {
-        size_t bytes = (size_t)n * P->batch * sizeof(T);
-        if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
-        {
-            LaunchScope ls("bitrev_permute", st);
-            k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)out, (T*)P->ws, P->k, (long long)P->batch);
-        }
-        MM_LAUNCH_CHECK();
-        MM_CUDA_TRY(cudaMemcpyAsync(out, P->ws, bytes, cudaMemcpyDeviceToDevice, st));
-    }
-    return MM_OK;
+    return launch_rows<F, false, T, T>(f, a, st);
 }
 
 template <class F>
@@ -1251,15 +1236,13 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     }
     mm_status s;
     const void* src = in;
-    if (order == MM_ORDER_NATURAL) {
-        size_t bytes = (size_t)n * P->batch * sizeof(T);
-        if ((s = ensure_ws(P, bytes)) != MM_OK) return s;
-        {
-            LaunchScope ls("bitrev_permute", st);
-            k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)P->ws, P->k, (long long)P->batch);
-        }
-        MM_LAUNCH_CHECK();
-        src = P->ws;
+    if (order == MM_ORDER_NATURAL) {   // permute into a temporary, then the TFT-order inverse
+        void* tmp = nullptr;
+        MM_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * P->batch * sizeof(T), st));
+        s = bitrev_rows<T>(in, tmp, P->k, (long long)P->batch, st);
+        if (s == MM_OK) s = inv_impl<F>(P, tmp, out, MM_ORDER_BITREV, st);
+        cudaFreeAsync(tmp, st);
+        return s;
     }
     if constexpr (sizeof(T) == 4) {
         if (P->fast16 && ((uintptr_t)src & 15) == 0 && ((uintptr_t)out & 15) == 0) {
@@ -1558,14 +1541,13 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(g_cache_mu);
     auto& e = g_ws[WsKey{dev, st}];
-    if (e.second < bytes) {
+    if (e.second < bytes) {   // grow in stream order: the old buffer is freed after the work queued on it
         if (e.first) {
-            MM_CUDA_TRY(cudaStreamSynchronize(st));
-            cudaFree(e.first);
+            cudaFreeAsync(e.first, st);
             e.first = nullptr;
             e.second = 0;
         }
-        MM_CUDA_TRY(cudaMalloc(&e.first, bytes));
+        MM_CUDA_TRY(cudaMallocAsync(&e.first, bytes, st));
         e.second = bytes;
     }
     *out = e.first;
@@ -1591,12 +1573,11 @@ static mm_status stream_ws_slot(cudaStream_t st, int slot, size_t bytes, void** 
     auto& e = g_ws_slots[WsSlotKey{dev, slot, st}];
     if (e.second < bytes) {
         if (e.first) {
-            MM_CUDA_TRY(cudaStreamSynchronize(st));
-            cudaFree(e.first);
+            cudaFreeAsync(e.first, st);
             e.first = nullptr;
             e.second = 0;
         }
-        MM_CUDA_TRY(cudaMalloc(&e.first, bytes));
+        MM_CUDA_TRY(cudaMallocAsync(&e.first, bytes, st));
         e.second = bytes;
     }
     *out = e.first;
@@ -1749,12 +1730,14 @@ extern "C" void mm_ntt_plan_destroy(mm_ntt_plan* plan) {
     free_plan(plan);
 }
 
-extern "C" mm_status mm_ntt_plan_info(const mm_ntt_plan* P, uint64_t out[4]) {
+extern "C" mm_status mm_ntt_plan_info(const mm_ntt_plan* P, uint64_t out[6]) {
     if (!P || !out) return set_err(MM_E_ARG, "null argument");
     out[0] = 1ull << P->k1;
     out[1] = 1ull << P->k2;
     out[2] = P->k2 ? 2 : 1;
-    out[3] = P->ws_bytes;
+    out[3] = 0;                 // workspaces are stream-ordered allocations (none held by the plan)
+    out[4] = (uint64_t)P->word_bits;
+    out[5] = (uint64_t)P->batch;
     return MM_OK;
 }
 
@@ -2443,12 +2426,35 @@ extern "C" mm_status mm_ntt_fwd_cols_p2p(const mm_ntt_plan* plan, const void* in
     return P->word_bits == 32 ? run(Fp32{}) : run(FpG{});
 }
 
-// CUDA IPC plumbing for the peer-scatter path (one node, one process per GPU)
-extern "C" mm_status mm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */) {
-    if (!dev_ptr || !handle_out) return set_err(MM_E_ARG, "null argument");
+// CUDA IPC plumbing for the peer-scatter path (one node, one process per GPU).
+// An IPC handle names a whole cudaMalloc allocation; a caching allocator
+// (torch) places tensors at offsets inside its blocks, so the handle travels
+// with the pointer's offset from the allocation base (cuMemGetAddressRange)
+// and the opener adds it back.
+typedef CUresult (*PFN_addr_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_addr_range addr_range_fn() {
+    static PFN_addr_range fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (PFN_addr_range)p;
+    }();
+    return fn;
+}
+extern "C" mm_status mm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 bytes */, uint64_t* offset_out) {
+    if (!dev_ptr || !handle_out || !offset_out) return set_err(MM_E_ARG, "null argument");
+    auto rng = addr_range_fn();
+    if (!rng) return set_err(MM_E_CUDA, "cuMemGetAddressRange is not available");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (rng(&base, &size, (CUdeviceptr)(uintptr_t)dev_ptr) != CUDA_SUCCESS)
+        return set_err(MM_E_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
     cudaIpcMemHandle_t h;
-    MM_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+    MM_CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
     memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
     return MM_OK;
 }
 extern "C" mm_status mm_ipc_open_handle(const void* handle /* 64 bytes */, void** dev_ptr) {

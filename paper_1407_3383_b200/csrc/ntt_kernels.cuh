@@ -661,6 +661,9 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
         }
         __syncthreads();
     }
+    // fused transpose: order this thread's peer stores system-wide before the
+    // stream's next kernel raises the ready flags (dist.cu k_dist_signal)
+    if (a.npeers) __threadfence_system();
 }
 
 // ---------------------------------------------------------------- fused product rows

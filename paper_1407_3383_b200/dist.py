@@ -117,15 +117,30 @@ class ShardedNtt:
         return range(self.rank * self.r2 * self.n1, (self.rank + 1) * self.r2 * self.n1)
 
 
-def peer_pointers(buf: torch.Tensor, group=None) -> list:
+def peer_pointers(buf: torch.Tensor, group=None) -> tuple[list, list]:
     """Device addresses of every rank's `buf` as seen from this process (one
-    node): CUDA IPC handles all-gathered and opened (own rank: local).  The
-    tensor must start its allocation (fresh torch.empty)."""
+    node): (CUDA IPC handle, offset of buf inside its allocation) all-gathered,
+    peers' allocations opened and the offsets added back (own rank: local).
+    Returns (pointers, opened bases to pass to close_peer_pointers)."""
     import paper_1407_3383_b200 as mm
     G, g = dist.get_world_size(group), dist.get_rank(group)
     handles = [None] * G
     dist.all_gather_object(handles, mm.ipc_handle(buf), group=group)
-    return [buf.data_ptr() if h == g else mm.ipc_open(handles[h]) for h in range(G)]
+    ptrs, bases = [], []
+    for h in range(G):
+        if h == g:
+            ptrs.append(buf.data_ptr())
+            continue
+        base = mm.ipc_open(handles[h][0])
+        bases.append(base)
+        ptrs.append(base + handles[h][1])
+    return ptrs, bases
+
+
+def close_peer_pointers(bases) -> None:
+    import paper_1407_3383_b200 as mm
+    for b in bases:
+        mm.ipc_close(b)
 
 
 class ShardedIntMul:

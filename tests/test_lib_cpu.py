@@ -89,3 +89,32 @@ def test_gold_shift_constants():
             assert c < p and (c if k < 96 else (p - c) % p) == pow(2, k, p)
         # the 8-point kernels' roots: w_8 = 2^(8S) has order 8, w_4 = 2^(16S) order 4
         assert pow(2, 8 * S * 4, p) == p - 1 and pow(2, 16 * S * 2, p) == p - 1
+
+
+def test_modnum_constants_host_side(mm):
+    # mm_modnum_create is host-only: u = 1/p to nearest and u-bar = the
+    # least float / double >= 1/p, checked with exact rationals
+    from fractions import Fraction
+    import numpy as np
+    L = mm.lib()
+    h = ctypes.c_void_p()
+    out = (ctypes.c_double * 6)()
+    for fbits in (32, 64):
+        l = 52 if fbits == 64 else 23
+        ftype = np.float64 if fbits == 64 else np.float32
+        for p in (3, 7, 2039, 65537, 2097143, 33554393, 67108859, 1125899906842597, 1108307720798209):
+            st = L.mm_modnum_create(fbits, p, ctypes.byref(h))
+            if p.bit_length() > l - 2:
+                assert st == 2                       # MM_E_PROFILE: m > l - 2 (Function 16's bound)
+                continue
+            assert st == 0
+            assert L.mm_modnum_info(h, out) == 0
+            u, ub = Fraction(out[1]), Fraction(out[2])
+            assert out[1] == float(ftype(1) / ftype(p))          # nearest
+            assert ub >= Fraction(1, p)
+            below = Fraction(float(np.nextafter(ftype(out[2]), ftype(0))))
+            assert below < Fraction(1, p)                          # least such value
+            assert (out[3], out[4], out[5]) == (l, p.bit_length(), fbits)
+            L.mm_modnum_destroy(h)
+    assert L.mm_modnum_create(64, 4, ctypes.byref(h)) == 1         # even
+    assert L.mm_modnum_create(16, 7, ctypes.byref(h)) == 10        # bad fbits

@@ -468,3 +468,64 @@ def test_poly_matmul_naive_pins(O):
     Z = rng.integers(0, p, size=(2, 2, 2), dtype=np.uint64)
     assert np.array_equal(O.poly_matmul_naive(O.poly_matmul_naive(X, Y, p), Z, p),
                           O.poly_matmul_naive(X, O.poly_matmul_naive(Y, Z, p), p))
+
+
+# ---------------------------------------------------------------- order_pow2: negative pins
+def test_order_pow2_negatives(O):
+    # or_order_pow2 must return the exact order, not just 2^k: w^2 has order
+    # 2^(k-1), w^(2^j) order 2^(k-j), -1 order 2, 1 order 1; w has no order
+    # dividing 2^(k-1) (w^(2^(k-1)) = -1), and a generator of (Z/pZ)^* (order
+    # p - 1, which 2^k does not reach) has none dividing 2^k.  Python pow is
+    # the library check of each claim.
+    for p, g, kmax in ((P30, 3, 23), (P32, 5, 30), (PG, 7, 32), (P29, 3, 26)):
+        for k in (1, 2, 5, kmax - 1, kmax):
+            w = O.root_of_unity(g, k, p)
+            for j in range(0, k + 1):
+                wj = O.powmod(w, 1 << j, p)
+                assert O.order_pow2(wj, k, p) == 1 << (k - j), (p, k, j)
+            if k >= 1:
+                assert pow(w, 1 << (k - 1), p) == p - 1
+                assert O.order_pow2(w, k - 1, p) == 0, (p, k)     # order 2^k does not divide 2^(k-1)
+            assert O.order_pow2(g, k, p) == 0                     # generator: order p - 1
+        assert O.order_pow2(1, 0, p) == 1
+        assert O.order_pow2(p - 1, 1, p) == 2
+        assert O.order_pow2(p - 1, 0, p) == 0
+    # a non-root whose order is odd (> 1): 3^(2^23 * 119... ) -- take g^(2^l) with l the 2-adicity
+    for p, g in ((P30, 3), (PG, 7)):
+        l = O.two_adicity(p)
+        odd = O.powmod(g, 1 << l, p)                              # order (p-1)/2^l, odd and > 1
+        assert odd != 1 and O.order_pow2(odd, l, p) == 0
+
+
+# ---------------------------------------------------------------- definition pins
+def _def_pins():
+    rows = []
+    with open(os.path.join(HERE, "golden", "definition_pins.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            lhs, rhs = line.split("->")
+            p, w, a = lhs.split()
+            rows.append((int(p), int(w), [int(x) for x in a.split(",")], [int(x) for x in rhs.split(",")]))
+    return rows
+
+
+@pytest.mark.parametrize("row", _def_pins())
+def test_definition_pins(O, row):
+    # P:889 FFT_w(a) on SURVEY App. A's (and SPEC S:327's) worked values: the
+    # O(n^2) definition, the textbook radix-2 NTT, the BITREV order,
+    # Algorithm 1 and the inverse all reproduce them
+    p, w, a, ahat = row
+    n = len(a)
+    k = n.bit_length() - 1
+    assert [sum(pow(w, i * j, p) * a[j] for j in range(n)) % p for i in range(n)] == ahat   # library re-derivation
+    assert O.order_pow2(w, k, p) == n
+    av = np.array(a, dtype=np.uint64)
+    assert [int(v) for v in O.dft(av, w, p)] == ahat
+    assert [int(v) for v in O.ntt(av, w, p)] == ahat
+    bit = [ahat[O.bitrev(i, k)] for i in range(n)]
+    assert [int(v) for v in O.to_bitrev(np.array(ahat, dtype=np.uint64))] == bit
+    for k1 in range(1, k):
+        assert [int(v) for v in O.algorithm1(av, k1, w, p)] == bit
+    assert [int(v) for v in O.intt(np.array(ahat, dtype=np.uint64), w, p)] == a
