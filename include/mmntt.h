@@ -258,7 +258,8 @@ mm_status mm_reduce_num(const mm_modnum *ctx, mm_num_variant v, const void *a, v
  * operand and for the inverse, and an inverse column TFT (van der Hoeven)
  * that rebuilds each column's lambda coefficients.  For lc just above a
  * power of two this skips about half of the padded transform's row work.
- * Products that fit one pass (lc <= 2^12) go to mm_poly_mul. */
+ * Products that fit one pass (lc <= 2^12), and those whose four-step split has
+ * columns longer than 2^10 (n = 2^24), go to mm_poly_mul: the same c. */
 mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t *a, size_t la, const uint32_t *b, size_t lb,
                           uint32_t *c, size_t batch, void *stream);
 
@@ -331,6 +332,14 @@ mm_status mm_ntt_inv_rows(const mm_ntt_plan *plan, const void *in, void *out, si
                           void *stream);
 mm_status mm_ntt_inv_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
                           void *stream);
+
+/* Free the plans, per-stream workspaces and host-pipeline buffers that
+ * mm_poly_mul*, mm_int_mul*, mm_poly_matmul and mm_int_matmul_u32 cache
+ * between calls (a cached Goldilocks plan of 2^24 holds 256 MiB of step-2
+ * tables, 1 GiB at 2^26) and trim the device's default memory pool.
+ * Synchronises the device; no call may be in flight on another host thread.
+ * Later calls rebuild what they need. */
+mm_status mm_release_cached(void);
 
 /* ------------------------------------------------------------------------
  * Instrumentation (measurement only; not part of the method).

@@ -56,6 +56,52 @@ bool hprime(uint64_t n) {
     return true;
 }
 
+// ---- MMNTT_DEBUG input range checks (header conventions): residues of rows
+// [rows][len] at row stride ld must be canonical -- u32 / u64 below p, FP64
+// (word_bits 52) integral in [0, p).  One counting kernel, then a stream sync.
+template <class T>
+__global__ void k_rows_range(const T* __restrict__ x, long long rows, long long len, long long ld, uint64_t p,
+                             unsigned long long* bad) {
+    unsigned long long local = 0;
+    const long long n = rows * len;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / len, j = i - r * len;
+        const T v = x[r * ld + j];
+        if constexpr (sizeof(T) == 8 && T(0.5) != T(0)) {
+            local += !(v >= 0.0 && v < (double)p && floor(v) == v);
+        } else {
+            local += (uint64_t)v >= p;
+        }
+    }
+    if (local) atomicAdd(bad, local);
+}
+
+mm_status check_rows(const void *x, int word_bits, size_t rows, size_t len, size_t ld, uint64_t p, cudaStream_t st) {
+    if (!x || !rows || !len) return MM_OK;
+    unsigned long long *d = nullptr, h = 0;
+    MM_CUDA_TRY(cudaMallocAsync((void **)&d, sizeof(*d), st));
+    MM_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(*d), st));
+    {
+        LaunchScope ls("debug_range_check", st);
+        const int grid = num_sms() * 4;
+        if (word_bits == 32)
+            k_rows_range<uint32_t><<<grid, 256, 0, st>>>((const uint32_t *)x, (long long)rows, (long long)len,
+                                                         (long long)ld, p, d);
+        else if (word_bits == 64)
+            k_rows_range<uint64_t><<<grid, 256, 0, st>>>((const uint64_t *)x, (long long)rows, (long long)len,
+                                                         (long long)ld, p, d);
+        else
+            k_rows_range<double><<<grid, 256, 0, st>>>((const double *)x, (long long)rows, (long long)len,
+                                                       (long long)ld, p, d);
+    }
+    MM_LAUNCH_CHECK();
+    MM_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MM_CUDA_TRY(cudaFreeAsync(d, st));
+    MM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h) return set_err(MM_E_RANGE, "%llu input residues outside [0, p)", h);
+    return MM_OK;
+}
+
 static std::atomic<unsigned long long> g_launches{0};
 static std::atomic<int> g_prof{0};
 static std::mutex g_prof_mu;

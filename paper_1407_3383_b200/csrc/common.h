@@ -13,6 +13,9 @@ namespace mm {
 mm_status set_err(mm_status s, const char *fmt, ...);
 int num_sms();
 bool debug_checks();
+// MMNTT_DEBUG=1 range check of [rows][len] residues at row stride ld (word_bits
+// 32 / 64: integers < p; 52: integral doubles in [0, p)); synchronises st
+mm_status check_rows(const void *x, int word_bits, size_t rows, size_t len, size_t ld, uint64_t p, cudaStream_t st);
 
 typedef unsigned __int128 u128;
 static inline uint64_t hmulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)(((u128)a * b) % p); }

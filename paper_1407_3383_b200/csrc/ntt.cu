@@ -1746,6 +1746,10 @@ extern "C" mm_status mm_ntt_forward(const mm_ntt_plan* plan, const void* in, voi
     if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
     mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
     cudaStream_t st = (cudaStream_t)stream;
+    if (debug_checks()) {
+        mm_status s = check_rows(in, P->word_bits, P->batch, 1ull << P->k, 1ull << P->k, P->p, st);
+        if (s != MM_OK) return s;
+    }
     if (P->word_bits == 52) return fwd_impl<FpD>(P, in, out, order, st);
     return P->word_bits == 32 ? fwd_impl<Fp32>(P, in, out, order, st) : fwd_impl<FpG>(P, in, out, order, st);
 }
@@ -1755,6 +1759,10 @@ extern "C" mm_status mm_ntt_inverse(const mm_ntt_plan* plan, const void* in, voi
     if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
     mm_ntt_plan* P = const_cast<mm_ntt_plan*>(plan);
     cudaStream_t st = (cudaStream_t)stream;
+    if (debug_checks()) {
+        mm_status s = check_rows(in, P->word_bits, P->batch, 1ull << P->k, 1ull << P->k, P->p, st);
+        if (s != MM_OK) return s;
+    }
     if (P->word_bits == 52) return inv_impl<FpD>(P, in, out, order, st);
     return P->word_bits == 32 ? inv_impl<Fp32>(P, in, out, order, st) : inv_impl<FpG>(P, in, out, order, st);
 }
@@ -1863,6 +1871,10 @@ extern "C" mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const
     mm_ntt_plan* P = nullptr;
     if ((s = cached_plan(word_bits, p, k, omega, &P)) != MM_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
+    if (debug_checks()) {
+        if ((s = check_rows(a, word_bits, batch, la, lda, p, st)) != MM_OK) return s;
+        if ((s = check_rows(b, word_bits, batch, lb, ldb, p, st)) != MM_OK) return s;
+    }
     if (word_bits == 32)
         return product_impl<Fp32, uint32_t, uint32_t>(P, (const uint32_t*)a, (long long)la, (const uint32_t*)b,
                                                       (long long)lb, (uint32_t*)c, (long long)lc, (long long)batch, st,
@@ -1969,6 +1981,43 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     }
     // the caller's stream is ordered after the last download
     MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
+    return MM_OK;
+}
+
+// Release everything the library caches between calls: the poly_mul / int_mul
+// plans (Goldilocks plans hold 2 n-word step-2 tables: 256 MiB at 2^24, 1 GiB
+// at 2^26), the per-stream workspaces and the host-pipeline slots; then trim
+// the device's default memory pool.  Synchronises the device; later calls
+// rebuild what they need.
+extern "C" mm_status mm_release_cached(void) {
+    MM_CUDA_TRY(cudaDeviceSynchronize());
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        for (auto& kv : g_plans) free_plan(kv.second);
+        g_plans.clear();
+        for (auto& kv : g_ws)
+            if (kv.second.first) cudaFreeAsync(kv.second.first, 0);
+        g_ws.clear();
+        for (auto& kv : g_ws_slots)
+            if (kv.second.first) cudaFreeAsync(kv.second.first, 0);
+        g_ws_slots.clear();
+    }
+    {
+        std::lock_guard<std::mutex> g(g_pipe_mu);
+        for (auto& kv : g_pipes) {
+            HostPipe* h = kv.second;
+            std::lock_guard<std::mutex> lk(h->mu);
+            if (h->buf) cudaFree(h->buf);
+            h->buf = nullptr;
+            h->bytes = 0;
+            for (int i = 0; i < 3; i++) h->used[i] = false;
+        }
+    }
+    MM_CUDA_TRY(cudaDeviceSynchronize());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     return MM_OK;
 }
 
@@ -2257,6 +2306,10 @@ extern "C" mm_status mm_poly_matmul(uint64_t p, uint64_t g, const uint32_t* A, c
     mm_ntt_plan* P = nullptr;
     if ((s = cached_plan(32, p, k, omega, &P)) != MM_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
+    if (debug_checks()) {
+        if ((s = check_rows(A, 32, m * kk, da, da, p, st)) != MM_OK) return s;
+        if ((s = check_rows(B, 32, kk * n, db, db, p, st)) != MM_OK) return s;
+    }
     void* ws = nullptr;
     if ((s = stream_ws2(st, (size_t)(m * kk + kk * n + m * n) * L * 4, &ws)) != MM_OK) return s;
     uint32_t* Ah = (uint32_t*)ws;
@@ -2490,8 +2543,16 @@ extern "C" mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t* a, 
     uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
     mm_ntt_plan* P = nullptr;
     if ((s = cached_plan(32, p, k, omega, &P)) != MM_OK) return s;
+    // the inverse column TFT takes columns of <= 2^10 points; the 2^11-point
+    // columns of a 2^24 plan (R9) go through the padded product, which returns
+    // the same c (checked before any launch)
+    if (P->k2 > 10) return mm_poly_mul(32, p, g, a, la, b, lb, c, batch, stream);
     const long long n1 = 1ll << P->k1, lam = ((long long)lc + n1 - 1) / n1;
     cudaStream_t st = (cudaStream_t)stream;
+    if (debug_checks()) {
+        if ((s = check_rows(a, 32, batch, la, la, p, st)) != MM_OK) return s;
+        if ((s = check_rows(b, 32, batch, lb, lb, p, st)) != MM_OK) return s;
+    }
     void* ws = nullptr;
     if ((s = stream_ws(st, (size_t)(2 * lam * n1 * (long long)batch) * 4, &ws)) != MM_OK) return s;
     uint32_t* WA = (uint32_t*)ws;

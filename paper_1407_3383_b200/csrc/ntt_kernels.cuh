@@ -508,9 +508,12 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
     constexpr bool PIPE = K::PIPE && sizeof(TIn) == sizeof(T);
     const bool pipe = PIPE && a.vec_in;
     // cp.async the whole column tile `tile` into dst (zero-fill beyond in_len)
+    // tiles run column-group-major (tile = cg nbatch + b): the nbatch tiles of one
+    // column group are in flight together and share their step-2 table segment
+    // (w^(j1 [i2]) does not depend on the batch row) through L2
     auto issue = [&](long long tile, T* dst) {
-        const long long b = tile / cgroups;
-        const long long cl0 = (tile - b * cgroups) * C;
+        const long long b = tile % a.nbatch;
+        const long long cl0 = (tile / a.nbatch) * C;
         const long long lin0 = a.col0 + cl0;
         const T* tb = (const T*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;
@@ -534,8 +537,8 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
         cp_async_commit();
     }
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-        const long long b = tile / cgroups;
-        const long long cl0 = (tile - b * cgroups) * C;
+        const long long b = tile % a.nbatch;
+        const long long cl0 = (tile / a.nbatch) * C;
         const long long lin0 = a.col0 + cl0;        // logical column of c = 0
         const TIn* inb = (const TIn*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;

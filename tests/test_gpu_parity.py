@@ -161,6 +161,23 @@ def test_modf64_rejects_wide_prime(mm):
         mm.ModF64((1 << 61) - 1)
 
 
+def test_mod64_goldilocks(mm, O):
+    # mm_mod64_create + vector add / sub / mul over p = 2^64 - 2^32 + 1 vs u128 %
+    n = (1 << 19) + 3
+    x = residues(config_seed(4), 11, n, PG)
+    y = residues(config_seed(4), 12, n, PG)
+    B = sorted({0, 1, 2, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, 1 << 63, (PG - 1) // 2, PG - (1 << 32), PG - 2, PG - 1})
+    x = np.concatenate([x, np.array([a for a in B for _ in B], dtype=np.uint64)])
+    y = np.concatenate([y, np.array([b for _ in B for b in B], dtype=np.uint64)])
+    M = mm.Mod64()
+    xt, yt = dev(x), dev(y)
+    for op, ref in [(M.add, O.vec_addmod(x, y, PG)), (M.sub, O.vec_submod(x, y, PG)), (M.mul, O.vec_mulmod(x, y, PG))]:
+        assert np.array_equal(host(op(xt, yt)), ref)
+        assert np.array_equal(host(op(xt[1:], yt[1:])), ref[1:])      # unaligned: scalar tail kernel
+    with pytest.raises(mm.MMError):
+        mm.Mod64(P30)
+
+
 # ------------------------------------------------------------------ numeric reductions (paper §3.2-3.3)
 # (fbits, p, variants): primes at the bit bounds of Table 10 (float m = 11, 21;
 # double m = 25, 26, 50) and small ones; each variant only where its bound allows
@@ -826,6 +843,47 @@ def test_sharded_int_mul_c5_loopback(mm, O, c5_ref):
         assert np.array_equal(got, c5_ref[2]), G
 
 
+@pytest.mark.parametrize("bits,p,g,k", [(32, P30, 3, 16), (64, PG, 7, 20), (64, PG, 7, 24)])
+def test_dist_c_abi_single_rank(mm, O, bits, p, g, k):
+    # mm_dist_create / mm_ntt_forward_dist / mm_ntt_inverse_dist through the C ABI
+    # with a one-rank NCCL communicator, then the peer-memory transport (device
+    # flags, alternating receive buffers: epochs 1-3 cover the free-flag wait)
+    w = O.root_of_unity(g, k, p)
+    plan = mm.NttPlan(bits, p, k, w, 1)
+    inf = plan.info()
+    assert (inf["word_bits"], inf["batch"], inf["passes"]) == (bits, 1, 2)
+    x = residues(21, k, 1 << k, p)
+    xt = dev(x).reshape(inf["n2"], inf["n1"])
+    ref = host(plan.forward(xt.reshape(-1), out=torch.empty_like(xt.reshape(-1)), order=mm.BITREV))
+    if k <= 20:
+        assert np.array_equal(u64(ref), O.to_bitrev(O.ntt(x, w, p)))
+    D = mm.Dist.single()
+    assert D.info()["world"] == 1 and D.info()["nccl_version"] > 0
+    y = D.ntt_forward(plan, xt)
+    assert np.array_equal(host(y).reshape(-1), ref)
+    assert np.array_equal(host(D.ntt_inverse(plan, y)).reshape(-1), x)
+    D.enable_p2p(xt.numel() * xt.element_size())
+    assert D.info()["p2p_bytes"] >= xt.numel() * xt.element_size()
+    for e in range(3):
+        y = D.ntt_forward(plan, xt)
+        assert np.array_equal(host(y).reshape(-1), ref), e
+    assert D.p2p_status() == 0
+    D.close()
+
+
+@pytest.mark.parametrize("na,nb", [(3000, 5000), (1 << 15, 1 << 15), (1 << 16, 100)])
+def test_dist_int_mul_c_abi_single_rank(mm, O, na, nb):
+    # mm_int_mul_u16_dist with one rank: the [n2][c1] block is the whole product
+    D = mm.Dist.single()
+    a, b = limbs16(na + 5, 1, na), limbs16(nb + 5, 2, nb)
+    L = D.int_mul_layout(na, nb)
+    assert L["c1"] == L["n1"] and L["n1"] * L["n2"] == 1 << L["log2n"]
+    got = host(D.int_mul_u16(dev(a), dev(b))).reshape(-1)
+    assert np.array_equal(got[:na + nb], O.int_mul_ntt_u16(a, b))
+    assert not got[na + nb:].any()
+    D.close()
+
+
 def _ipc_worker(rank, world, port):
     import os
     import torch.distributed as dist
@@ -833,15 +891,19 @@ def _ipc_worker(rank, world, port):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import ctypes
         import paper_1407_3383_b200 as m
-        from paper_1407_3383_b200.dist import peer_pointers
+        from paper_1407_3383_b200.dist import close_peer_pointers, peer_pointers
         torch.cuda.set_device(0)
-        buf = torch.zeros(1024, dtype=torch.int32, device="cuda")
-        ptrs = peer_pointers(buf)
+        big = torch.zeros(4096 + 1024, dtype=torch.int32, device="cuda")
+        # buffers at nonzero offsets inside their allocations (a caching
+        # allocator's usual placement): 16 KiB + 4 KiB per rank in
+        buf = big[4096 + 1024 * 0:][:1024] if rank == 0 else big[4096 - 1024:][:1024]
+        assert m.ipc_handle(buf)[1] > 0
+        ptrs, bases = peer_pointers(buf)
         # each rank writes its id into its slot of every peer's buffer through the opened pointers
         for h, q in enumerate(ptrs):
             src = torch.full((4,), rank + 1, dtype=torch.int32, device="cuda")
-            import ctypes
             torch.cuda.synchronize()
             ctypes.CDLL("libcudart.so").cudaMemcpy(ctypes.c_void_p(q + 16 * rank), ctypes.c_void_p(src.data_ptr()),
                                                    ctypes.c_size_t(16), 3)
@@ -850,9 +912,7 @@ def _ipc_worker(rank, world, port):
         got = buf[:4 * world].view(world, 4).cpu()
         assert all((got[r] == r + 1).all() for r in range(world)), got
         dist.barrier()
-        for h, q in enumerate(ptrs):
-            if h != rank:
-                m.ipc_close(q)
+        close_peer_pointers(bases)
     finally:
         dist.destroy_process_group()
 
@@ -867,3 +927,48 @@ def test_ipc_peer_pointers(mm):
     port = s.getsockname()[1]
     s.close()
     mp.spawn(_ipc_worker, args=(2, port), nprocs=2, join=True)
+
+
+def test_debug_range_checks(mm, O, monkeypatch):
+    # MMNTT_DEBUG=1: non-canonical residues are refused with MM_E_RANGE (header
+    # conventions) by the NTT, product and numeric entry points; canonical ones pass
+    monkeypatch.setenv("MMNTT_DEBUG", "1")
+    for bits, p, g, k in [(32, P30, 3, 10), (32, P30, 3, 16), (64, PG, 7, 12), (64, PG, 7, 20)]:
+        w = O.root_of_unity(g, k, p)
+        plan = mm.NttPlan(bits, p, k, w, 2)
+        x = residues(3, k, 2 << k, p)
+        xt = dev(x)
+        plan.forward(xt.clone(), order=mm.BITREV)                       # in range: fine
+        bad = xt.clone()
+        bad.view(torch.int64 if bits == 64 else torch.int32)[(1 << k) + 5] = -1   # 2^32 - 1 / 2^64 - 1 >= p
+        for fn in (plan.forward, plan.inverse):
+            with pytest.raises(mm.MMError) as e:
+                fn(bad.clone(), order=mm.BITREV)
+            assert e.value.status == 5
+    a = dev(residues(4, 1, 3 * 700, P30).reshape(3, 700))
+    b = dev(residues(4, 2, 3 * 900, P30).reshape(3, 900))
+    mm.poly_mul(a, b, P30, 3)
+    a.view(torch.int32)[2, 699] = P30
+    with pytest.raises(mm.MMError):
+        mm.poly_mul(a, b, P30, 3)
+    with pytest.raises(mm.MMError):
+        mm.poly_mul_tft(a.repeat(1, 30), b.repeat(1, 30), P30, 3)
+    M = mm.ModNum(64, 65537)
+    xf = torch.tensor([1.0, 2.5, 3.0, 4.0], dtype=torch.float64, device=DEV)   # 2.5 is not an integer
+    with pytest.raises(mm.MMError):
+        M.mul(xf, xf)
+    monkeypatch.delenv("MMNTT_DEBUG")
+    mm.poly_mul(a, b, P30, 3)                                             # trusted again
+
+
+def test_release_cached(mm, O):
+    # mm_release_cached frees the cached plans / workspaces; later calls rebuild them
+    a = residues(8, 1, 2 * 5000, P30).reshape(2, 5000)
+    b = residues(8, 2, 2 * 3000, P30).reshape(2, 3000)
+    c1 = host(mm.poly_mul(dev(a), dev(b), P30, 3))
+    ia, ib = limbs16(8, 3, 20000), limbs16(8, 4, 30000)
+    i1 = host(mm.int_mul_u16(dev(ia), dev(ib)))
+    mm.release_cached()
+    assert np.array_equal(host(mm.poly_mul(dev(a), dev(b), P30, 3)), c1)
+    assert np.array_equal(host(mm.int_mul_u16(dev(ia), dev(ib))), i1)
+    assert np.array_equal(u64(c1[1]), O.poly_mul_ntt(a[1], b[1], P30, 3))
