@@ -857,6 +857,177 @@ __global__ void k_crt3(const uint32_t* __restrict__ c, long long stride, long lo
     }
 }
 
+// ---------------------------------------------------------------- fused Garner CRT + carries (three-prime path)
+// One pass from the three residue products to 32-bit limbs: a CTA of the
+// single-pass look-back carry (k_carry16_fused's scheme) stages the
+// coefficients its 4096 limbs need, rebuilding each from c mod p1, p2, p3 by
+// Garner (c = x1 + p1 t2 + p1 p2 x3 < p1 p2 p3, three 32-bit words) with
+// Shoup products instead of 64-bit divisions, then forms digit sums
+// s_j = w0(c_j) + w1(c_{j-1}) + w2(c_{j-2}) and the (generate, propagate) chain.
+// Limb positions: entry e = j / nout, local jl = j - e nout; coefficient jl of
+// entry e (residue q at Cp[q stride + e nc + jl]) exists for jl < nc, the
+// positions jl in [nc, nout) are zero (nout - nc >= 1 keeps entries apart:
+// a limb's digit sum reaches 2 positions back, and positions of the previous
+// entry that close are its zero tail when nout - nc = 2, or absent when E = 1).
+struct Crt3S {
+    uint32_t p1, p2, p3;
+    uint32_t i12, i12s, i13, i13s, i23, i23s;   // inverses and their Shoup companions
+    uint64_t p12;
+};
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t ws, uint32_t p) {
+    const uint32_t q = __umulhi(x, ws);
+    const uint32_t r = x * w - q * p;        // in [0, 2p)
+    return r >= p ? r - p : r;
+}
+__device__ __forceinline__ void garner3(uint32_t r1, uint32_t r2, uint32_t r3, const Crt3S& K, uint32_t* w) {
+    const uint32_t x1 = r1;
+    const uint32_t x1m2 = x1 >= K.p2 ? x1 - K.p2 : x1;                 // x1 < p1 < 2 p2
+    const uint32_t d2 = r2 >= x1m2 ? r2 - x1m2 : r2 + K.p2 - x1m2;
+    const uint32_t t2 = shoup_mul(d2, K.i12, K.i12s, K.p2);           // (r2 - x1) / p1 mod p2
+    const uint32_t x1m3 = x1 >= K.p3 ? x1 - K.p3 : x1;                 // x1 < 2 p3
+    const uint32_t d3 = r3 >= x1m3 ? r3 - x1m3 : r3 + K.p3 - x1m3;
+    const uint32_t t3 = shoup_mul(d3, K.i13, K.i13s, K.p3);           // (r3 - x1) / p1 mod p3
+    const uint32_t t2m3 = t2 >= K.p3 ? t2 - K.p3 : t2;                 // t2 < p2 < 2 p3
+    const uint32_t e3 = t3 >= t2m3 ? t3 - t2m3 : t3 + K.p3 - t2m3;
+    const uint32_t x3 = shoup_mul(e3, K.i23, K.i23s, K.p3);           // (t3 - t2) / p2 mod p3
+    const uint64_t lo = (uint64_t)x1 + (uint64_t)K.p1 * t2;            // < 2^60
+    const uint64_t ml = K.p12 * x3, mh = __umul64hi(K.p12, (uint64_t)x3);
+    const uint64_t sum = lo + ml;
+    w[0] = (uint32_t)sum;
+    w[1] = (uint32_t)(sum >> 32);
+    w[2] = (uint32_t)(mh + (sum < lo ? 1 : 0));
+}
+constexpr int CC_HALO = 3;                                  // positions before a block: s_{jb-1} reaches jb - 3
+__global__ void __launch_bounds__(CARRY_T) k_crt_carry32(const uint32_t* __restrict__ Cp, long long stride,
+                                                         long long nc, long long nout, long long nall, Crt3S K,
+                                                         unsigned long long* status, unsigned* ticket,
+                                                         uint32_t* __restrict__ out) {
+    extern __shared__ uint32_t sw_dyn[];                    // the three words of every staged position
+    uint32_t (*sw)[CARRY_B + CC_HALO + 1] = (uint32_t (*)[CARRY_B + CC_HALO + 1])sw_dyn;
+    __shared__ uint32_t sh[64];
+    __shared__ uint32_t s_bid, s_cin;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const long long bid = s_bid;
+    const long long jb = bid * CARRY_B;
+    // stage: 4 positions per thread per round, loads of a round issued together
+    constexpr int NPOS = CARRY_B + CC_HALO, ROUNDS = (NPOS + 4 * CARRY_T - 1) / (4 * CARRY_T);
+#pragma unroll 1
+    for (int rd = 0; rd < ROUNDS; rd++) {
+        uint32_t r1[4], r2[4], r3[4];
+        bool live[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int r = threadIdx.x + (rd * 4 + u) * CARRY_T;
+            const long long q = jb - CC_HALO + r;
+            long long at = 0;
+            live[u] = false;
+            if (r < NPOS && q >= 0 && q < nall) {
+                const long long e = q / nout, jl = q - e * nout;
+                live[u] = jl < nc;
+                at = e * nc + jl;
+            }
+            r1[u] = live[u] ? __ldg(Cp + at) : 0u;
+            r2[u] = live[u] ? __ldg(Cp + stride + at) : 0u;
+            r3[u] = live[u] ? __ldg(Cp + 2 * stride + at) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int r = threadIdx.x + (rd * 4 + u) * CARRY_T;
+            if (r >= NPOS) continue;
+            uint32_t w[3] = {0u, 0u, 0u};
+            if (live[u]) garner3(r1[u], r2[u], r3[u], K, w);
+            sw[0][r] = w[0];
+            sw[1][r] = w[1];
+            sw[2][r] = w[2];
+        }
+    }
+    __syncthreads();
+    // limbs j = jb + 16 t + e: s_j = w0(c_j) + w1(c_{j-1}) + w2(c_{j-2}); u_j = (s_j mod 2^32) + (s_{j-1} >> 32)
+    uint32_t w[16], g[16];
+    {
+        const int base = CC_HALO + 16 * (int)threadIdx.x;    // staged index of limb j0
+        // s_{j0 - 1}; positions before 0 are staged as zeros, so s_{-1} = 0
+        uint64_t sprev = (uint64_t)sw[0][base - 1] + sw[1][base - 2] + sw[2][base - 3];
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+            const int i = base + e;
+            const uint64_t sj = (uint64_t)sw[0][i] + sw[1][i - 1] + sw[2][i - 2];
+            const uint64_t u = (sj & 0xFFFFFFFFull) + (sprev >> 32);
+            w[e] = (uint32_t)u;
+            g[e] = (uint32_t)(u >> 32);
+            sprev = sj;
+        }
+    }
+    uint32_t acc = 2u;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const long long j = jb + 16 * threadIdx.x + e;
+        acc = gp_comb(acc, j < nall ? (g[e] | ((w[e] == 0xFFFFFFFFu ? 1u : 0u) << 1)) : 2u);
+    }
+    {   // block aggregate, publication and decoupled look-back (as k_carry16_fused)
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        uint32_t x = acc;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = gp_comb(y, x);
+        }
+        if (lane == 31) sh[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t agg = 2u;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) agg = gp_comb(agg, sh[q]);
+            if (bid == 0) {
+                if (lane == 0) {
+                    st_release64(status, (2ull << 32) | agg);
+                    s_cin = 0;
+                }
+            } else {
+                if (lane == 0) st_release64(status + bid, (1ull << 32) | agg);
+                uint32_t run = 2u;
+                for (long long k = bid - 1;; k -= 32) {
+                    const long long kk = k - lane;
+                    unsigned long long v = (2ull << 32) | 2u;
+                    if (kk >= 0)
+                        do { v = ld_acquire64(status + kk); } while ((v >> 32) == 0);
+                    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 32) == 2);
+                    const int stop = inc ? __ffs(inc) - 1 : 31;
+                    uint32_t x2 = lane <= stop ? (uint32_t)v : 2u;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_down_sync(0xffffffffu, x2, o);
+                        if (lane + o < 32) x2 = gp_comb(y, x2);
+                    }
+                    run = gp_comb(__shfl_sync(0xffffffffu, x2, 0), run);
+                    if (inc) break;
+                }
+                if (lane == 0) {
+                    st_release64(status + bid, (2ull << 32) | gp_comb(run, agg));
+                    s_cin = run & 1u;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    uint32_t C = block_carry_in(acc, s_cin, sh);
+    const long long j0 = jb + 16 * threadIdx.x;
+    uint32_t o[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        o[e] = w[e] + C;
+        C = g[e] | ((w[e] == 0xFFFFFFFFu ? 1u : 0u) & C);
+    }
+    if (j0 + 16 <= nall && ((((uintptr_t)(out + j0)) & 15) == 0)) {
+        uint4* d = (uint4*)(out + j0);
+#pragma unroll
+        for (int i = 0; i < 4; i++) d[i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 16; e++)
+            if (j0 + e < nall) out[j0 + e] = o[e];
+    }
+}
+
 }  // namespace mm
 
 using namespace mm;
@@ -1714,6 +1885,106 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     return launch_cols<F, true, T, TOut>(f, ci, st);
 }
 
+// Remark 6: the three products of the three-prime method in one
+// launch per pass -- row q of every batched operand is reduced mod p_q, with
+// p_q's field constants and tables selected per tile.  R = residues [3][rs]
+// (a at offset 0, b at offset na), Cp = products [3][lc]; the three plans
+// share k (hence the split and the table geometry).
+static mm_status product3_impl(mm_ntt_plan* const PL[3], const uint32_t* R, long long rs, long long na, long long nb,
+                               uint32_t* Cp, long long lc, cudaStream_t st) {
+    typedef uint2 W;
+    mm_ntt_plan* P = PL[0];
+    Fp32 f = make_field<Fp32>(P);
+    if (P->k2 == 0) {
+        // one-pass products: a product tile holds several rows, which would mix
+        // moduli -- one launch per prime (these sizes are launch-latency bound)
+        for (int q = 0; q < 3; q++) {
+            mm_status s = product_impl<Fp32, uint32_t, uint32_t>(PL[q], R + q * rs, na, R + q * rs + na, nb, Cp + q * lc,
+                                                                 lc, 1, st);
+            if (s != MM_OK) return s;
+        }
+        return MM_OK;
+    }
+    const long long n = 1ll << P->k, n1 = 1ll << P->k1;
+    void* ws = nullptr;
+    mm_status s = stream_ws(st, (size_t)(6 * n) * sizeof(uint32_t), &ws);
+    if (s != MM_OK) return s;
+    uint32_t* WA = (uint32_t*)ws;
+    uint32_t* WB = WA + 3 * n;
+    for (int op = 0; op < 2; op++) {
+        ColArgs<Fp32> cc{};
+        cc.in = op == 0 ? R : R + na;
+        cc.out = op == 0 ? WA : WB;
+        cc.ncols = n1;
+        cc.nbatch = 3;
+        cc.in_rs = n1; cc.out_rs = n1;
+        cc.in_bs = rs; cc.out_bs = n;
+        cc.in_len = op == 0 ? na : nb; cc.out_len = n;
+        cc.n1 = n1;
+        cc.k = P->k2;
+        cc.fs = 1;
+        cc.lvl = (const W*)P->lvl_f2;
+        cc.fs_lo = (const W*)P->fs_lo_f;
+        cc.fs_hi = (const W*)P->fs_hi_f;
+        cc.fs_full = (const W*)P->fs_full_f;
+        cc.fs_h = P->fs_h;
+        cc.nmod = 3;
+        cc.mod_span = 1;
+        for (int q = 0; q < 3; q++) {
+            cc.fm[q] = make_field<Fp32>(PL[q]);
+            cc.lvlm[q] = (const W*)PL[q]->lvl_f2;
+            cc.fslom[q] = (const W*)PL[q]->fs_lo_f;
+            cc.fshim[q] = (const W*)PL[q]->fs_hi_f;
+            cc.fsfullm[q] = (const W*)PL[q]->fs_full_f;
+        }
+        if ((s = launch_cols<Fp32, false, uint32_t, uint32_t>(f, cc, st)) != MM_OK) return s;
+    }
+    PmulArgs<Fp32> m{};
+    m.a = WA; m.b = WB; m.c = WA;
+    m.nrows = 3ll << P->k2;
+    m.a_rs = m.b_rs = m.c_rs = n1;
+    m.la = m.lb = m.lc = n1;
+    m.k = P->k1;
+    m.fs = 1; m.k2 = P->k2; m.row0 = 0;
+    m.sc = host_w<W>(P->ninv_r, P->p);
+    m.lvl_f = (const W*)P->lvl_f1;
+    m.lvl_i = (const W*)P->lvl_i1;
+    m.fs_lo = (const W*)P->fs_lo_i;
+    m.fs_hi = (const W*)P->fs_hi_i;
+    m.fs_full = (const W*)P->fs_full_i;
+    m.fs_h = P->fs_h;
+    m.nmod = 3;
+    m.mod_span = 1ll << P->k2;
+    for (int q = 0; q < 3; q++) {
+        m.fm[q] = make_field<Fp32>(PL[q]);
+        m.scm[q] = host_w<W>(PL[q]->ninv_r, PL[q]->p);
+        m.lvlfm[q] = (const W*)PL[q]->lvl_f1;
+        m.lvlim[q] = (const W*)PL[q]->lvl_i1;
+        m.fslom[q] = (const W*)PL[q]->fs_lo_i;
+        m.fshim[q] = (const W*)PL[q]->fs_hi_i;
+        m.fsfullm[q] = (const W*)PL[q]->fs_full_i;
+    }
+    if ((s = launch_pmul<Fp32, uint32_t, uint32_t>(f, m, st)) != MM_OK) return s;
+    ColArgs<Fp32> ci{};
+    ci.in = WA; ci.out = Cp;
+    ci.ncols = n1;
+    ci.nbatch = 3;
+    ci.in_rs = n1; ci.out_rs = n1;
+    ci.in_bs = n; ci.out_bs = lc;
+    ci.in_len = n; ci.out_len = lc;
+    ci.n1 = n1;
+    ci.k = P->k2;
+    ci.canon = 1;
+    ci.lvl = (const W*)P->lvl_i2;
+    ci.nmod = 3;
+    ci.mod_span = 1;
+    for (int q = 0; q < 3; q++) {
+        ci.fm[q] = make_field<Fp32>(PL[q]);
+        ci.lvlm[q] = (const W*)PL[q]->lvl_i2;
+    }
+    return launch_cols<Fp32, true, uint32_t, uint32_t>(f, ci, st);
+}
+
 }  // namespace mm
 
 // ====================================================================== C ABI
@@ -2021,6 +2292,37 @@ extern "C" mm_status mm_release_cached(void) {
     return MM_OK;
 }
 
+static Crt3S crt3s_consts() {
+    static const uint32_t PR[3] = {998244353u, 985661441u, 943718401u};
+    Crt3S K;
+    K.p1 = PR[0]; K.p2 = PR[1]; K.p3 = PR[2];
+    K.i12 = (uint32_t)hpowmod(PR[0] % PR[1], PR[1] - 2, PR[1]);
+    K.i13 = (uint32_t)hpowmod(PR[0] % PR[2], PR[2] - 2, PR[2]);
+    K.i23 = (uint32_t)hpowmod(PR[1] % PR[2], PR[2] - 2, PR[2]);
+    K.i12s = (uint32_t)(((uint64_t)K.i12 << 32) / K.p2);
+    K.i13s = (uint32_t)(((uint64_t)K.i13 << 32) / K.p3);
+    K.i23s = (uint32_t)(((uint64_t)K.i23 << 32) / K.p3);
+    K.p12 = (uint64_t)PR[0] * PR[1];
+    return K;
+}
+// Garner + carries in one launch: residue products Cp[3][stride] (entry e's
+// coefficient k at e nc + k) -> nall = E nout 32-bit limbs; `scratch` holds
+// the look-back status words and the ticket (nblk + 1 words of 8 bytes)
+static mm_status crt_carry32(const uint32_t* Cp, long long stride, long long nc, long long nout, long long nall,
+                             unsigned long long* scratch, uint32_t* out, cudaStream_t st) {
+    const long long nblk = (nall + CARRY_B - 1) / CARRY_B;
+    MM_CUDA_TRY(cudaMemsetAsync(scratch, 0, (size_t)nblk * 8 + 8, st));
+    const size_t smem = 3 * (CARRY_B + CC_HALO + 1) * sizeof(uint32_t);   // 48 KiB + a little: opt in
+    MM_CUDA_TRY(cudaFuncSetAttribute(k_crt_carry32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {
+        LaunchScope ls("crt_carry_fused", st);
+        k_crt_carry32<<<(int)nblk, CARRY_T, smem, st>>>(Cp, stride, nc, nout, nall, crt3s_consts(), scratch,
+                                                         (unsigned*)(scratch + nblk), out);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
 // reduce -> scan -> apply over nout output digits; agg: one word per CARRY_B digits
 template <class D>
 static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D::Out* out, cudaStream_t st) {
@@ -2129,20 +2431,18 @@ extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t
         k_residues3<<<grid, 256, 0, st>>>(b, (long long)nb, R + na, (long long)rs, K);
     }
     MM_LAUNCH_CHECK();
+    mm_ntt_plan* PL[3];
     for (int i = 0; i < 3; i++) {
         uint64_t omega = hpowmod(GEN[i], (PR[i] - 1) >> k, PR[i]);
-        mm_ntt_plan* P = nullptr;
-        if ((s = cached_plan(32, PR[i], k, omega, &P)) != MM_OK) return s;
-        if ((s = product_impl<Fp32, uint32_t, uint32_t>(P, R + i * rs, (long long)na, R + i * rs + na, (long long)nb,
-                                                        Cp + i * lc, (long long)lc, 1, st)) != MM_OK)
-            return s;
+        if ((s = cached_plan(32, PR[i], k, omega, &PL[i])) != MM_OK) return s;
     }
-    {
-        LaunchScope ls("crt_garner", st);
-        k_crt3<<<grid, 256, 0, st>>>(Cp, (long long)lc, (long long)lc, Wd, K);
-    }
-    MM_LAUNCH_CHECK();
-    return carry_run(Dig32x3{Wd, (long long)lc}, (long long)nout, agg, c, st);
+    // the three products modulo p1, p2, p3 in one launch per pass (Remark 6)
+    if ((s = product3_impl(PL, R, (long long)rs, (long long)na, (long long)nb, Cp, (long long)lc, st)) != MM_OK)
+        return s;
+    // Garner CRT and carries in one pass (crt_carry32); Wd is its look-back scratch
+    (void)agg;
+    return crt_carry32(Cp, (long long)lc, (long long)lc, (long long)nout, (long long)nout,
+                       (unsigned long long*)(((uintptr_t)Wd + 7) & ~(uintptr_t)7), c, st);
 }
 
 // ---- sharded integer product building blocks (dist.py ShardedIntMul) ----------------
@@ -2418,12 +2718,9 @@ extern "C" mm_status mm_int_matmul_u32(const uint32_t* A, const uint32_t* B, uin
     for (int i = 0; i < 3; i++)
         if ((s = mm_poly_matmul(PR[i], GEN[i], RA + i * sa, RB + i * sb, RC + i * sc, m, kk, n, na, nb, stream)) != MM_OK)
             return s;
-    {
-        LaunchScope ls("crt_garner", st);
-        k_crt3<<<grid, 256, 0, st>>>(RC, (long long)sc, (long long)sc, Wd, K);
-    }
-    MM_LAUNCH_CHECK();
-    return carry_run(Dig32x3Batch{Wd, (long long)lc, (long long)nout}, (long long)nall, agg, C, st);
+    (void)agg;
+    return crt_carry32(RC, (long long)sc, (long long)lc, (long long)nout, (long long)nall,
+                       (unsigned long long*)(((uintptr_t)Wd + 7) & ~(uintptr_t)7), C, st);
 }
 
 // ---- fused column pass + transpose over peer memory ---------------------------------

@@ -142,6 +142,16 @@ template <class F> struct ColArgs {
     // buffers of the other ranks written in place (npeers = 0: plain out)
     int npeers, peer_shift;
     void* peer_out[8];
+    // Remark 6: nmod > 1 moduli in one launch -- batch rows
+    // [q mod_span, (q+1) mod_span) run over field fm[q] with plan q's tables
+    int nmod;
+    long long mod_span;
+    F fm[3];
+    W scm[3];
+    const W* lvlm[3];
+    const W* fslom[3];
+    const W* fshim[3];
+    const W* fsfullm[3];
 };
 template <class F> struct PmulArgs {
     typedef typename F::W W;
@@ -161,6 +171,17 @@ template <class F> struct PmulArgs {
     int fs_h;
     long long rows_per;   // > 0: truncated transforms of rows_per rows each (TFT), i2 = row mod rows_per
     void* scratch;        // single-buffer tiles (PmulK::SB): L words per CTA for the first spectrum
+    // Remark 6: nmod > 1 moduli in one launch -- rows [q mod_span,
+    // (q+1) mod_span) run over field fm[q] with plan q's tables and scale
+    int nmod;
+    long long mod_span;
+    F fm[3];
+    W scm[3];
+    const W* lvlfm[3];
+    const W* lvlim[3];
+    const W* fslom[3];
+    const W* fshim[3];
+    const W* fsfullm[3];
 };
 
 // Epilogue selector (compile time): bits 0-1 = step-2 twiddle (0 none, 1 full
@@ -504,16 +525,27 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
     const W* tw = K::TWS ? (const W*)tws : a.lvl;
     const long long cgroups = a.ncols / C;                 // host guarantees ncols % C == 0
     const long long ntiles = cgroups * a.nbatch;
+    // the modulus of the current tile (Remark 6): field, tables, scale
+    F ff = f;
+    const W* lvl = a.lvl;
+    const W* fsf = a.fs_full;
+    const W* fslo = a.fs_lo;
+    const W* fshi = a.fs_hi;
+    W sc = a.sc;
+    int curq = 0;
     const unsigned irs = (unsigned)a.in_rs, ors = (unsigned)a.out_rs, n1 = (unsigned)a.n1;
     constexpr bool PIPE = K::PIPE && sizeof(TIn) == sizeof(T);
     const bool pipe = PIPE && a.vec_in;
     // cp.async the whole column tile `tile` into dst (zero-fill beyond in_len)
     // tiles run column-group-major (tile = cg nbatch + b): the nbatch tiles of one
     // column group are in flight together and share their step-2 table segment
-    // (w^(j1 [i2]) does not depend on the batch row) through L2
+    // (w^(j1 [i2]) does not depend on the batch row) through L2.  Several
+    // moduli (different tables per batch row): batch-major, so a CTA restages
+    // its twiddles only when its tiles cross into the next modulus.
+    const bool bmajor = a.nmod > 1;
     auto issue = [&](long long tile, T* dst) {
-        const long long b = tile % a.nbatch;
-        const long long cl0 = (tile / a.nbatch) * C;
+        const long long b = bmajor ? tile / cgroups : tile % a.nbatch;
+        const long long cl0 = (bmajor ? tile % cgroups : tile / a.nbatch) * C;
         const long long lin0 = a.col0 + cl0;
         const T* tb = (const T*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;
@@ -537,9 +569,28 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
         cp_async_commit();
     }
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-        const long long b = tile % a.nbatch;
-        const long long cl0 = (tile / a.nbatch) * C;
+        const long long b = bmajor ? tile / cgroups : tile % a.nbatch;
+        const long long cl0 = (bmajor ? tile % cgroups : tile / a.nbatch) * C;
         const long long lin0 = a.col0 + cl0;        // logical column of c = 0
+        if (bmajor) {
+            const int q = (int)(b / a.mod_span);
+            if (q != curq || tile == blockIdx.x) {
+                curq = q;
+                ff = a.fm[q];
+                lvl = a.lvlm[q];
+                fsf = a.fsfullm[q];
+                fslo = a.fslom[q];
+                fshi = a.fshim[q];
+                sc = a.scm[q];
+                if (K::TWS) {
+                    __syncthreads();
+                    stage_twiddles(tws, lvl, L);
+                    __syncthreads();
+                } else {
+                    tw = lvl;
+                }
+            }
+        }
         const TIn* inb = (const TIn*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;
         T* cur = s;
@@ -606,7 +657,7 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
             }
         }
         __syncthreads();
-        run_tile<F, Lay, LOGL, INV, NTH>(f, cur, tw, a.lvl);
+        run_tile<F, Lay, LOGL, INV, NTH>(ff, cur, tw, lvl);
         col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
         TOut* outb = (TOut*)a.out + b * a.out_bs + cl0;
         if (a.vec_out && sizeof(TOut) == sizeof(T)) {
@@ -626,7 +677,7 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
 #pragma unroll
                         for (int i = 0; i < V; i++) v[u][i] = cur[Lay::addr(c + i, t)];
                     }
-                    if (E::FS == 1) ld_wvec<W, V>(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
+                    if (E::FS == 1) ld_wvec<W, V>(fsf + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
@@ -637,8 +688,8 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                     const unsigned bt = (unsigned)brev(t, LOGL);
 #pragma unroll
                     for (int i = 0; i < V; i++)
-                        v[u][i] = E::apply(f, v[u][i], w[u][i], a.fs_lo, a.fs_hi, a.fs_h,
-                                           ((unsigned)lin0 + c + i) * bt, a.sc);
+                        v[u][i] = E::apply(ff, v[u][i], w[u][i], fslo, fshi, a.fs_h,
+                                           ((unsigned)lin0 + c + i) * bt, sc);
                     if (a.npeers) {         // fused transpose: store into the owning rank's receive buffer
                         T* pb = (T*)a.peer_out[t >> a.peer_shift] + cl0;
                         *(TV*)(pb + (unsigned)t * ors + c) = vmake<T>(v[u]);
@@ -656,9 +707,9 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                 const int t = e / C, c = e % C;
                 if (t >= tzero || (t >= tfull && (long long)t * a.n1 + lin0 + c >= a.out_len)) continue;
                 W wf{};
-                if (E::FS == 1) wf = __ldg(a.fs_full + (unsigned)t * n1 + (unsigned)lin0 + c);
-                T x = E::apply(f, cur[Lay::addr(c, t)], wf, a.fs_lo, a.fs_hi, a.fs_h,
-                               ((unsigned)lin0 + c) * (unsigned)brev(t, LOGL), a.sc);
+                if (E::FS == 1) wf = __ldg(fsf + (unsigned)t * n1 + (unsigned)lin0 + c);
+                T x = E::apply(ff, cur[Lay::addr(c, t)], wf, fslo, fshi, a.fs_h,
+                               ((unsigned)lin0 + c) * (unsigned)brev(t, LOGL), sc);
                 outb[(unsigned)t * ors + c] = (TOut)x;
             }
         }
@@ -703,6 +754,7 @@ __global__ void __launch_bounds__(NTr<F, LOGL>::v, NTr<F, LOGL>::v == 512 ? 2 : 
     }
     const W* twf = K::TWS ? (const W*)twfs : a.lvl_f;
     const W* twi = K::TWS ? (const W*)twis : a.lvl_i;
+    if (K::SB && a.nmod > 1) return;   // host never combines them (Goldilocks 2^13 rows: one modulus)
     const long long ntiles = (a.nrows + C - 1) / C;
     if constexpr (K::SB) {
         static_assert(C == 1, "single-buffer product tiles hold one row");
@@ -739,15 +791,47 @@ __global__ void __launch_bounds__(NTr<F, LOGL>::v, NTr<F, LOGL>::v == 512 ? 2 : 
         }
         return;
     }
+    // the modulus of the current tile (Remark 6): rows of one tile never
+    // straddle two moduli (host: mod_span % C == 0)
+    F ff = f;
+    const W* lvlf = a.lvl_f;
+    const W* lvli = a.lvl_i;
+    const W* fsf = a.fs_full;
+    const W* fslo = a.fs_lo;
+    const W* fshi = a.fs_hi;
+    W sc = a.sc;
+    int curq = -1;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long r0 = tile * C;
+        if (a.nmod > 1) {
+            const int q = (int)(r0 / a.mod_span);
+            if (q != curq) {
+                curq = q;
+                ff = a.fm[q];
+                lvlf = a.lvlfm[q];
+                lvli = a.lvlim[q];
+                fsf = a.fsfullm[q];
+                fslo = a.fslom[q];
+                fshi = a.fshim[q];
+                sc = a.scm[q];
+                if (K::TWS) {
+                    __syncthreads();
+                    stage_twiddles(twfs, lvlf, L);
+                    stage_twiddles(twis, lvli, L);
+                    __syncthreads();
+                } else {
+                    twf = lvlf;
+                    twi = lvli;
+                }
+            }
+        }
         load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false, a.in_seg_log,
                                      a.in_seg_stride);
         load_rows<F, Lay, LOGL, TIn, NTH>(sb, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false, a.in_seg_log,
                                      a.in_seg_stride);
         __syncthreads();
-        run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
-        run_tile<F, Lay, LOGL, false, NTH>(f, sb, twf, a.lvl_f);
+        run_tile<F, Lay, LOGL, false, NTH>(ff, sa, twf, lvlf);
+        run_tile<F, Lay, LOGL, false, NTH>(ff, sb, twf, lvlf);
         {
             constexpr int R = L < 16 ? L : 16;
             constexpr int PER = L / R;
@@ -757,14 +841,14 @@ __global__ void __launch_bounds__(NTr<F, LOGL>::v, NTr<F, LOGL>::v == 512 ? 2 : 
 #pragma unroll
                 for (int t = 0; t < R; t++) {
                     const int ix = base + t;          // R consecutive elements never cross a pad
-                    sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
+                    sa[ix] = ff.mulw(ff.mul_redc(sa[ix], sb[ix]), sc);
                 }
             }
         }
         __syncthreads();
-        run_tile<F, Lay, LOGL, true, NTH>(f, sa, twi, a.lvl_i);
-        store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, a.fs_full,
-                                             a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc, a.out_seg_log,
+        run_tile<F, Lay, LOGL, true, NTH>(ff, sa, twi, lvli);
+        store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(ff, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false, fsf,
+                                             fslo, fshi, a.fs_h, a.row0, a.k2, sc, a.out_seg_log,
                                              a.out_seg_stride, a.rows_per);
         __syncthreads();
     }
