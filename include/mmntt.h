@@ -333,6 +333,16 @@ mm_status mm_ntt_inv_rows(const mm_ntt_plan *plan, const void *in, void *out, si
 mm_status mm_ntt_inv_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
                           void *stream);
 
+/* Sub-batch concurrency of the batched products (default 2): mm_poly_mul /
+ * mm_poly_mul_ld with the 2^16-point kernels (C3 shape) split batches of at
+ * least 128 n rows into n sub-batches on the library's own streams, forked
+ * from and joined back into the caller's stream by events (stream-ordered,
+ * no host synchronisation; CUDA-graph capturable), so that one sub-batch's
+ * HBM-bound column passes overlap another's ALU-bound product rows.  n = 1
+ * runs every kernel on the caller's stream (per-kernel timing).  1 <= n <= 4,
+ * else MM_E_ARG.  Process-wide setting. */
+mm_status mm_set_product_streams(int n);
+
 /* Free the plans, per-stream workspaces and host-pipeline buffers that
  * mm_poly_mul*, mm_int_mul*, mm_poly_matmul and mm_int_matmul_u32 cache
  * between calls (a cached Goldilocks plan of 2^24 holds 256 MiB of step-2

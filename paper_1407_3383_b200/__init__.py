@@ -99,6 +99,7 @@ EXPORTS = {
     "mm_int_mul_u16_dist": (_ST, [_P, _P, _sz, _P, _sz, _P, _P]),
     "mm_int_mul_u16_dist_layout": (_ST, [_P, _sz, _sz, ctypes.POINTER(_u64)]),
     "mm_release_cached": (_ST, []),
+    "mm_set_product_streams": (_ST, [_i32]),
     "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_probe_issue": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_prof_enable": (None, [_i32]),
@@ -454,6 +455,11 @@ class NttPlan:
     def inv_cols(self, x, out, col0, ncols):
         _check(lib().mm_ntt_inv_cols(self._h, _ptr(x), _ptr(out), col0, ncols, _stream(x)))
         return out
+
+
+def set_product_streams(n: int):
+    """Sub-batch concurrency of the batched products (mm_set_product_streams)."""
+    _check(lib().mm_set_product_streams(int(n)))
 
 
 def release_cached():

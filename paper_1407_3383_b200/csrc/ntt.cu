@@ -1756,6 +1756,36 @@ static mm_status stream_ws_slot(cudaStream_t st, int slot, size_t bytes, void** 
 }
 static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) { return stream_ws_slot(st, 1, bytes, out); }
 
+// ---- fork streams for sub-batch concurrency (product_impl) ----------------------
+constexpr int MAX_FORK = 4;
+struct Fork {
+    cudaStream_t s[MAX_FORK];
+    cudaEvent_t fork, join[MAX_FORK];
+    std::mutex mu;
+};
+static std::mutex g_fork_mu;
+static std::map<int, Fork*> g_forks;
+static int g_product_streams = 2;
+static int product_streams() { return g_product_streams; }
+static mm_status fork_streams(Fork** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_fork_mu);
+    Fork*& F = g_forks[dev];
+    if (!F) {
+        Fork* f = new (std::nothrow) Fork;
+        if (!f) return set_err(MM_E_ARG, "out of host memory");
+        for (int i = 0; i < MAX_FORK; i++) {
+            MM_CUDA_TRY(cudaStreamCreateWithFlags(&f->s[i], cudaStreamNonBlocking));
+            MM_CUDA_TRY(cudaEventCreateWithFlags(&f->join[i], cudaEventDisableTiming));
+        }
+        MM_CUDA_TRY(cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming));
+        F = f;
+    }
+    *out = F;
+    return MM_OK;
+}
+
 // n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
 static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, long long lda, const uint32_t* b,
                                 long long lb, long long ldb, uint32_t* c, long long lc, long long ldc, long long batch,
@@ -1825,15 +1855,48 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         return launch_pmul<F, TIn, TOut>(f, m, st);
     }
     const long long n = 1ll << P->k, n1 = 1ll << P->k1;
+    if constexpr (sizeof(T) == 4 && sizeof(TIn) == 4 && sizeof(TOut) == 4) {
+        if (P->fast16) {
+            // Large batches run as sub-batches on the library's fork streams
+            // (forked from and joined back into `st` by events): one
+            // sub-batch's HBM-heavy column passes overlap another's ALU-bound
+            // product rows, and each kernel's tail overlaps the other stream's
+            // work (C3: 2.21 -> 2.08 ms on B200, tools/exp_streams.py)
+            const int ns = product_streams();
+            if (ns > 1 && batch >= 128 * ns) {
+                Fork* FK = nullptr;
+                mm_status s = fork_streams(&FK);
+                if (s != MM_OK) return s;
+                std::lock_guard<std::mutex> lk(FK->mu);
+                MM_CUDA_TRY(cudaEventRecord(FK->fork, st));
+                long long r0 = 0;
+                for (int h = 0; h < ns; h++) {
+                    const long long rows = batch / ns + (h < batch % ns ? 1 : 0);
+                    MM_CUDA_TRY(cudaStreamWaitEvent(FK->s[h], FK->fork, 0));
+                    void* wsh = nullptr;
+                    if ((s = stream_ws(FK->s[h], (size_t)(2 * n * rows) * sizeof(T), &wsh)) != MM_OK) return s;
+                    if ((s = fast16_product(P, (const uint32_t*)a + r0 * lda, la, lda, (const uint32_t*)b + r0 * ldb, lb,
+                                            ldb, (uint32_t*)c + r0 * ldc, lc, ldc, rows, (uint32_t*)wsh,
+                                            (uint32_t*)wsh + n * rows, FK->s[h])) != MM_OK)
+                        return s;
+                    MM_CUDA_TRY(cudaEventRecord(FK->join[h], FK->s[h]));
+                    MM_CUDA_TRY(cudaStreamWaitEvent(st, FK->join[h], 0));
+                    r0 += rows;
+                }
+                return MM_OK;
+            }
+            void* ws = nullptr;
+            mm_status s = stream_ws(st, (size_t)(2 * n * batch) * sizeof(T), &ws);
+            if (s != MM_OK) return s;
+            return fast16_product(P, (const uint32_t*)a, la, lda, (const uint32_t*)b, lb, ldb, (uint32_t*)c, lc, ldc,
+                                  batch, (uint32_t*)ws, (uint32_t*)ws + n * batch, st);
+        }
+    }
     void* ws = nullptr;
     mm_status s = stream_ws(st, (size_t)(2 * n * batch) * sizeof(T), &ws);
     if (s != MM_OK) return s;
     T* WA = (T*)ws;
     T* WB = WA + n * batch;
-    if constexpr (sizeof(T) == 4 && sizeof(TIn) == 4 && sizeof(TOut) == 4) {
-        if (P->fast16) return fast16_product(P, (const uint32_t*)a, la, lda, (const uint32_t*)b, lb, ldb, (uint32_t*)c,
-                                             lc, ldc, batch, (uint32_t*)WA, (uint32_t*)WB, st);
-    }
     // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb
     for (int op = 0; op < 2; op++) {
         ColArgs<F> cc{};
@@ -2252,6 +2315,12 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     }
     // the caller's stream is ordered after the last download
     MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
+    return MM_OK;
+}
+
+extern "C" mm_status mm_set_product_streams(int n) {
+    if (n < 1 || n > MAX_FORK) return set_err(MM_E_ARG, "product streams must be in [1, %d]", MAX_FORK);
+    g_product_streams = n;
     return MM_OK;
 }
 

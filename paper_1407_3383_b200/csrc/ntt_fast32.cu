@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <string.h>
+#include <stdlib.h>
 #include "common.h"
 #include "arith.cuh"
 #include "fast32.h"
@@ -522,6 +523,11 @@ __global__ void __launch_bounds__(NT, 4) k_row_inv(RowArgs32 a) {
 template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    static const int cap_env = [] {
+        const char* e = getenv("MMNTT_CTAS_PER_SM");   // experiment knob: cap resident CTAs per SM
+        return e ? atoi(e) : 0;
+    }();
+    if (cap_env > 0 && per_sm > cap_env) per_sm = cap_env;
     if (per_sm < 1) per_sm = 1;
     long long cap = (long long)num_sms() * per_sm;
     return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);

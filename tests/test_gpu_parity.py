@@ -972,3 +972,38 @@ def test_release_cached(mm, O):
     assert np.array_equal(host(mm.poly_mul(dev(a), dev(b), P30, 3)), c1)
     assert np.array_equal(host(mm.int_mul_u16(dev(ia), dev(ib))), i1)
     assert np.array_equal(u64(c1[1]), O.poly_mul_ntt(a[1], b[1], P30, 3))
+
+
+def test_poly_mul_fork_streams(mm, O):
+    # C3 shape, 512 products: the sub-batch fork (mm_set_product_streams 2 and 3)
+    # equals the one-stream result and the oracle, also inside a CUDA graph
+    p, g, B, d = P30, 3, 512, 1 << 15
+    a = gen.residues_torch(config_seed(3), 7, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    b = gen.residues_torch(config_seed(3), 8, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    mm.set_product_streams(1)
+    ref = mm.poly_mul(a, b, p, g)
+    try:
+        for ns in (2, 3):
+            mm.set_product_streams(ns)
+            c = mm.poly_mul(a, b, p, g)
+            assert torch.equal(c.view(torch.int32), ref.view(torch.int32)), ns
+        mm.set_product_streams(2)
+        c = torch.zeros_like(ref)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            mm.poly_mul(a, b, p, g, out=c)                       # warm (plans, workspaces)
+            with torch.cuda.graph(graph, stream=s):
+                mm.poly_mul(a, b, p, g, out=c)
+        torch.cuda.synchronize()
+        c.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(c.view(torch.int32), ref.view(torch.int32))
+        for r in (0, 255, 256, 511):                              # both halves of the fork
+            assert np.array_equal(u64(host(ref[r])), O.poly_mul_ntt(host(a[r]), host(b[r]), p, g)), r
+        with pytest.raises(mm.MMError):
+            mm.set_product_streams(0)
+    finally:
+        mm.set_product_streams(2)
