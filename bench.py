@@ -516,7 +516,9 @@ def extras_run(mm, torch, dev, peaks):
     del a3, b3, c3
 
     def kern_ms(fn, reps=5):
-        # per-family kernel time per call (library event profiler, launching stream)
+        # per-family kernel time per call (library event profiler, launching
+        # stream), kernels serialised on one stream so their times add up
+        mm.set_product_streams(1)
         fn()
         torch.cuda.synchronize()
         mm.prof_collect()
@@ -525,6 +527,7 @@ def extras_run(mm, torch, dev, peaks):
             fn()
         r = mm.prof_collect()
         mm.prof_enable(False)
+        mm.set_product_streams(2)
         return {k: round(v[1] / reps, 4) for k, v in r.items()}
 
     # C4: 8 x 2^24 Goldilocks forward NTT (four-step 2^11 columns x 2^13 rows, gold.cuh tiles)

@@ -1305,6 +1305,60 @@ static mm_status bitrev_rows(const void* in, void* out, int k, long long batch, 
     return MM_OK;
 }
 
+// ---- fork streams for sub-batch concurrency (product_impl) ----------------------
+constexpr int MAX_FORK = 4;
+struct Fork {
+    cudaStream_t s[MAX_FORK];
+    cudaEvent_t fork, join[MAX_FORK];
+    std::mutex mu;
+};
+static std::mutex g_fork_mu;
+static std::map<int, Fork*> g_forks;
+static int g_product_streams = 2;
+static int product_streams() { return g_product_streams; }
+static mm_status fork_streams(Fork** out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_fork_mu);
+    Fork*& F = g_forks[dev];
+    if (!F) {
+        Fork* f = new (std::nothrow) Fork;
+        if (!f) return set_err(MM_E_ARG, "out of host memory");
+        for (int i = 0; i < MAX_FORK; i++) {
+            MM_CUDA_TRY(cudaStreamCreateWithFlags(&f->s[i], cudaStreamNonBlocking));
+            MM_CUDA_TRY(cudaEventCreateWithFlags(&f->join[i], cudaEventDisableTiming));
+        }
+        MM_CUDA_TRY(cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming));
+        F = f;
+    }
+    *out = F;
+    return MM_OK;
+}
+
+// fn(in + r0 n, out + r0 n, rows, stream) over the fork streams, sub-batches of
+// the batch forked from and joined back into st (one call on st when the
+// concurrency is 1 or the batch is a single transform)
+template <class T, class Fn>
+static mm_status forked(const T* in, T* out, long long batch, long long n, cudaStream_t st, Fn fn) {
+    const int ns = (int)(product_streams() < batch ? product_streams() : batch);
+    if (ns < 2) return fn(in, out, batch, st);
+    Fork* FK = nullptr;
+    mm_status s = fork_streams(&FK);
+    if (s != MM_OK) return s;
+    std::lock_guard<std::mutex> lk(FK->mu);
+    MM_CUDA_TRY(cudaEventRecord(FK->fork, st));
+    long long r0 = 0;
+    for (int h = 0; h < ns; h++) {
+        const long long rows = batch / ns + (h < batch % ns ? 1 : 0);
+        MM_CUDA_TRY(cudaStreamWaitEvent(FK->s[h], FK->fork, 0));
+        if ((s = fn(in + r0 * n, out + r0 * n, rows, FK->s[h])) != MM_OK) return s;
+        MM_CUDA_TRY(cudaEventRecord(FK->join[h], FK->s[h]));
+        MM_CUDA_TRY(cudaStreamWaitEvent(st, FK->join[h], 0));
+        r0 += rows;
+    }
+    return MM_OK;
+}
+
 // ---- forward / inverse drivers ------------------------------------------------------
 template <class F>
 static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order order, cudaStream_t st) {
@@ -1355,34 +1409,42 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
             return f32::launch_row_fwd(ra, st);
         }
     }
-    // column pass: in -> out, then row pass: out -> out (bit-mirrored result)
-    ColArgs<F> c{};
-    c.in = in; c.out = out;
-    c.ncols = 1ll << P->k1;
-    c.nbatch = (long long)P->batch;
-    c.in_rs = c.out_rs = 1ll << P->k1;
-    c.in_bs = c.out_bs = n;
-    c.in_len = c.out_len = n;
-    c.col0 = 0;
-    c.n1 = 1ll << P->k1;
-    c.k = P->k2;
-    c.fs = 1;
-    c.lvl = (const W*)P->lvl_f2;
-    c.fs_lo = (const W*)P->fs_lo_f;
-    c.fs_hi = (const W*)P->fs_hi_f;
-    c.fs_full = (const W*)P->fs_full_f;
-    c.fs_h = P->fs_h;
-    mm_status s = launch_cols<F, false, T, T>(f, c, st);
-    if (s != MM_OK) return s;
-    RowArgs<F> a{};
-    a.in = out; a.out = out;
-    a.nrows = (long long)P->batch << P->k2;
-    a.in_rs = a.out_rs = 1ll << P->k1;
-    a.in_len = a.out_len = 1ll << P->k1;
-    a.k = P->k1;
-    a.canon = 1;
-    a.lvl = (const W*)P->lvl_f1;
-    return launch_rows<F, false, T, T>(f, a, st);
+    // column pass: in -> out, then row pass: out -> out (bit-mirrored result),
+    // for nb transforms from gin to gout on stream gs
+    auto four_step = [&](const void* gin, void* gout, long long nb, cudaStream_t gs) -> mm_status {
+        ColArgs<F> c{};
+        c.in = gin; c.out = gout;
+        c.ncols = 1ll << P->k1;
+        c.nbatch = nb;
+        c.in_rs = c.out_rs = 1ll << P->k1;
+        c.in_bs = c.out_bs = n;
+        c.in_len = c.out_len = n;
+        c.col0 = 0;
+        c.n1 = 1ll << P->k1;
+        c.k = P->k2;
+        c.fs = 1;
+        c.lvl = (const W*)P->lvl_f2;
+        c.fs_lo = (const W*)P->fs_lo_f;
+        c.fs_hi = (const W*)P->fs_hi_f;
+        c.fs_full = (const W*)P->fs_full_f;
+        c.fs_h = P->fs_h;
+        mm_status s = launch_cols<F, false, T, T>(f, c, gs);
+        if (s != MM_OK) return s;
+        RowArgs<F> a{};
+        a.in = gout; a.out = gout;
+        a.nrows = nb << P->k2;
+        a.in_rs = a.out_rs = 1ll << P->k1;
+        a.in_len = a.out_len = 1ll << P->k1;
+        a.k = P->k1;
+        a.canon = 1;
+        a.lvl = (const W*)P->lvl_f1;
+        return launch_rows<F, false, T, T>(f, a, gs);
+    };
+    // 64-bit four-step batches run as sub-batches on the fork streams (the
+    // latency-bound column pass of one overlaps the row pass of the other:
+    // C4 3.25 -> 3.04 ms on B200, tools/exp_streams2.py)
+    if (sizeof(T) == 8) return forked((const T*)in, (T*)out, (long long)P->batch, n, st, four_step);
+    return four_step(in, out, (long long)P->batch, st);
 }
 
 template <class F>
@@ -1437,33 +1499,39 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
             return f32::launch_col_inv(ci, st);
         }
     }
-    // inverse row pass (DIT over j1 + twiddle w^-(j1 [i2])): src -> out
-    RowArgs<F> a{};
-    a.in = src; a.out = out;
-    a.nrows = (long long)P->batch << P->k2;
-    a.in_rs = a.out_rs = 1ll << P->k1;
-    a.in_len = a.out_len = 1ll << P->k1;
-    a.k = P->k1;
-    a.fs = 1; a.k2 = P->k2; a.row0 = 0;
-    a.lvl = (const W*)P->lvl_i1;
-    a.fs_lo = (const W*)P->fs_lo_i;
-    a.fs_hi = (const W*)P->fs_hi_i;
-    a.fs_full = (const W*)P->fs_full_i;
-    a.fs_h = P->fs_h;
-    if ((s = launch_rows<F, true, T, T>(f, a, st)) != MM_OK) return s;
-    // inverse column pass (DIT over i2, n^-1, canonical): out -> out
-    ColArgs<F> c{};
-    c.in = out; c.out = out;
-    c.ncols = 1ll << P->k1;
-    c.nbatch = (long long)P->batch;
-    c.in_rs = c.out_rs = 1ll << P->k1;
-    c.in_bs = c.out_bs = n;
-    c.in_len = c.out_len = n;
-    c.n1 = 1ll << P->k1;
-    c.k = P->k2;
-    c.scale = 1; c.sc = sc; c.canon = 1;
-    c.lvl = (const W*)P->lvl_i2;
-    return launch_cols<F, true, T, T>(f, c, st);
+    auto four_step = [&](const void* gin, void* gout, long long nb, cudaStream_t gs) -> mm_status {
+        // inverse row pass (DIT over j1 + twiddle w^-(j1 [i2])): gin -> gout
+        RowArgs<F> a{};
+        a.in = gin; a.out = gout;
+        a.nrows = nb << P->k2;
+        a.in_rs = a.out_rs = 1ll << P->k1;
+        a.in_len = a.out_len = 1ll << P->k1;
+        a.k = P->k1;
+        a.fs = 1; a.k2 = P->k2; a.row0 = 0;
+        a.lvl = (const W*)P->lvl_i1;
+        a.fs_lo = (const W*)P->fs_lo_i;
+        a.fs_hi = (const W*)P->fs_hi_i;
+        a.fs_full = (const W*)P->fs_full_i;
+        a.fs_h = P->fs_h;
+        mm_status s2 = launch_rows<F, true, T, T>(f, a, gs);
+        if (s2 != MM_OK) return s2;
+        // inverse column pass (DIT over i2, n^-1, canonical): gout -> gout
+        ColArgs<F> c{};
+        c.in = gout; c.out = gout;
+        c.ncols = 1ll << P->k1;
+        c.nbatch = nb;
+        c.in_rs = c.out_rs = 1ll << P->k1;
+        c.in_bs = c.out_bs = n;
+        c.in_len = c.out_len = n;
+        c.n1 = 1ll << P->k1;
+        c.k = P->k2;
+        c.scale = 1; c.sc = sc; c.canon = 1;
+        c.lvl = (const W*)P->lvl_i2;
+        return launch_cols<F, true, T, T>(f, c, gs);
+    };
+    (void)s;
+    if (sizeof(T) == 8) return forked((const T*)src, (T*)out, (long long)P->batch, n, st, four_step);
+    return four_step(src, out, (long long)P->batch, st);
 }
 
 // ---- forward with zero-padded input rows / inverse with truncated output rows ----------
@@ -1756,36 +1824,6 @@ static mm_status stream_ws_slot(cudaStream_t st, int slot, size_t bytes, void** 
 }
 static mm_status stream_ws2(cudaStream_t st, size_t bytes, void** out) { return stream_ws_slot(st, 1, bytes, out); }
 
-// ---- fork streams for sub-batch concurrency (product_impl) ----------------------
-constexpr int MAX_FORK = 4;
-struct Fork {
-    cudaStream_t s[MAX_FORK];
-    cudaEvent_t fork, join[MAX_FORK];
-    std::mutex mu;
-};
-static std::mutex g_fork_mu;
-static std::map<int, Fork*> g_forks;
-static int g_product_streams = 2;
-static int product_streams() { return g_product_streams; }
-static mm_status fork_streams(Fork** out) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> g(g_fork_mu);
-    Fork*& F = g_forks[dev];
-    if (!F) {
-        Fork* f = new (std::nothrow) Fork;
-        if (!f) return set_err(MM_E_ARG, "out of host memory");
-        for (int i = 0; i < MAX_FORK; i++) {
-            MM_CUDA_TRY(cudaStreamCreateWithFlags(&f->s[i], cudaStreamNonBlocking));
-            MM_CUDA_TRY(cudaEventCreateWithFlags(&f->join[i], cudaEventDisableTiming));
-        }
-        MM_CUDA_TRY(cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming));
-        F = f;
-    }
-    *out = F;
-    return MM_OK;
-}
-
 // n = 2^16 = 256 x 256, p < 2^30: the specialised passes of ntt_fast32.cu
 static mm_status fast16_product(mm_ntt_plan* P, const uint32_t* a, long long la, long long lda, const uint32_t* b,
                                 long long lb, long long ldb, uint32_t* c, long long lc, long long ldc, long long batch,
@@ -1897,8 +1935,22 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
     if (s != MM_OK) return s;
     T* WA = (T*)ws;
     T* WB = WA + n * batch;
-    // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb
+    // forward column passes (steps 1-2) for a and b, zero padding beyond la / lb;
+    // 64-bit products: a's and b's passes on the two fork streams (concurrent)
+    const bool fork2 = sizeof(T) == 8 && product_streams() > 1;
+    Fork* FK = nullptr;
+    std::unique_lock<std::mutex> flk;
+    if (fork2) {
+        if ((s = fork_streams(&FK)) != MM_OK) return s;
+        flk = std::unique_lock<std::mutex>(FK->mu);
+        MM_CUDA_TRY(cudaEventRecord(FK->fork, st));
+    }
     for (int op = 0; op < 2; op++) {
+        cudaStream_t cs = st;
+        if (fork2) {
+            cs = FK->s[op];
+            MM_CUDA_TRY(cudaStreamWaitEvent(cs, FK->fork, 0));
+        }
         ColArgs<F> cc{};
         cc.in = op == 0 ? (const void*)a : (const void*)b;
         cc.out = op == 0 ? WA : WB;
@@ -1915,8 +1967,13 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
         cc.fs_hi = (const W*)P->fs_hi_f;
         cc.fs_full = (const W*)P->fs_full_f;
         cc.fs_h = P->fs_h;
-        if ((s = launch_cols<F, false, TIn, T>(f, cc, st)) != MM_OK) return s;
+        if ((s = launch_cols<F, false, TIn, T>(f, cc, cs)) != MM_OK) return s;
+        if (fork2) {
+            MM_CUDA_TRY(cudaEventRecord(FK->join[op], cs));
+            MM_CUDA_TRY(cudaStreamWaitEvent(st, FK->join[op], 0));
+        }
     }
+    if (fork2) flk.unlock();
     // fused row pass: steps 3-4 for both, pointwise product * n^-1, inverse step 4-3, inverse twiddle
     PmulArgs<F> m{};
     m.a = WA; m.b = WB; m.c = WA;
