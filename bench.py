@@ -471,6 +471,26 @@ def extras_run(mm, torch, dev, peaks):
     out["f64_elementwise_2^27_p63x2^44+1"] = c3f
     del xf, yf, zf
 
+    # paper §3.2-3.3: Functions 14 / 15 / 16 and their toward-+inf forms (mm_mulmod_num),
+    # doubles (2^27) and floats (2^28) at Table 10's bit sizes (context: P:748-755)
+    num = {}
+    for fbits, pn, nn, variants in ((64, 33554393, 1 << 27, (0, 1, 2, 3, 4, 5)), (64, 1125899906842597, 1 << 27, (4, 5)),
+                                    (32, 2039, 1 << 28, (0, 1, 2, 3, 4, 5)), (32, 2097143, 1 << 28, (4, 5))):
+        dt = torch.float64 if fbits == 64 else torch.float32
+        xn = gen.residues_torch(11, 1, nn, pn, dev).view(torch.int64).to(dt)
+        yn = gen.residues_torch(11, 2, nn, pn, dev).view(torch.int64).to(dt)
+        zn = torch.empty_like(xn)
+        MN = mm.ModNum(fbits, pn)
+        names = ["F14", "F14_up", "F15_up", "F15_near", "F16", "F16_up"]
+        for v in variants:
+            msn = tloop(lambda: MN.mul(xn, yn, variant=v, out=zn), 10)
+            by = 3 * nn * (fbits // 8)
+            num[f"{'f64' if fbits == 64 else 'f32'}_m{pn.bit_length()}_{names[v]}"] = {
+                "Gelem_per_s": round(nn / (msn * 1e-3) / 1e9, 1), "ms": round(msn, 4),
+                "hbm_frac": round(by / (msn * 1e-3) / 1e9 / hbm, 3)}
+        del xn, yn, zn
+    out["numeric_mulmod_functions_14_16"] = num
+
     # C3-fwd: 4096 forward NTTs of length 2^16 (TFT order), and the inverse
     pl16 = mm.NttPlan(32, P30, 16, root_of_unity(P30, G30, 16), 4096)
     x16 = gen.residues_torch(gen.config_seed(3), 3, 4096 << 16, P30, dev).view(torch.uint32)
@@ -802,7 +822,7 @@ def run_ours(args, world, rank, local):
     alu_bfly_peak = nsm * 16 * sm_mhz_max * 1e6
     # the issue rates the ALU peak is derived from, measured on this GPU (mm_probe_issue)
     clk_hz = sm_mhz_max * 1e6
-    rates = {nm: round(mm.probe_issue(kind, 3000) / (nsm * clk_hz), 3) for kind, nm in ((0, "IMAD"), (1, "IMAD.HI"))}
+    rates = {nm: round(mm.probe_issue(kind, 8000) / (nsm * clk_hz), 3) for kind, nm in ((0, "IMAD"), (1, "IMAD.HI"))}
     for k_, (cnt, tot) in prof.items():
         per = tot / cnt
         entry = {"launches": cnt, "avg_ms": round(per, 4), "share": round(tot / (ms_serial * args.steps), 3)}
