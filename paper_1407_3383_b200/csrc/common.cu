@@ -28,6 +28,39 @@ int num_sms() {
     return n > 0 ? n : 148;
 }
 
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+static cudaMemPool_t lib_pool(int dev) {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    auto it = g_pools.find(dev);
+    if (it != g_pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = pool;
+    return pool;
+}
+cudaError_t alloc_async(void **p, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = lib_pool(dev);
+    if (!pool) return cudaMallocAsync(p, bytes, st);
+    return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+void trim_pool() {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    for (auto &kv : g_pools) cudaMemPoolTrimTo(kv.second, 0);
+}
+
 bool debug_checks() {
     const char *e = getenv("MMNTT_DEBUG");
     return e && e[0] == '1';
@@ -79,7 +112,7 @@ __global__ void k_rows_range(const T* __restrict__ x, long long rows, long long 
 mm_status check_rows(const void *x, int word_bits, size_t rows, size_t len, size_t ld, uint64_t p, cudaStream_t st) {
     if (!x || !rows || !len) return MM_OK;
     unsigned long long *d = nullptr, h = 0;
-    MM_CUDA_TRY(cudaMallocAsync((void **)&d, sizeof(*d), st));
+    MM_CUDA_TRY(alloc_async((void **)&d, sizeof(*d), st));
     MM_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(*d), st));
     {
         LaunchScope ls("debug_range_check", st);

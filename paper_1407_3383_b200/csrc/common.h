@@ -13,6 +13,12 @@ namespace mm {
 mm_status set_err(mm_status s, const char *fmt, ...);
 int num_sms();
 bool debug_checks();
+// Stream-ordered allocation from the library's own memory pool (one per
+// device, release threshold unlimited: freed blocks stay in the pool for the
+// next call instead of going back to the driver at every synchronisation;
+// mm_release_cached trims it).  Used for every temporary and workspace.
+cudaError_t alloc_async(void **p, size_t bytes, cudaStream_t st);
+void trim_pool();
 // MMNTT_DEBUG=1 range check of [rows][len] residues at row stride ld (word_bits
 // 32 / 64: integers < p; 52: integral doubles in [0, p)); synchronises st
 mm_status check_rows(const void *x, int word_bits, size_t rows, size_t len, size_t ld, uint64_t p, cudaStream_t st);

@@ -350,7 +350,7 @@ extern "C" mm_status mm_ntt_forward_dist(mm_dist* D, const mm_ntt_plan* plan, co
         return signal(D, G + r, e, st);                                               // free[r] = e at every peer
     }
     void* ws = nullptr;
-    MM_CUDA_TRY(cudaMallocAsync(&ws, 2 * blk, st));
+    MM_CUDA_TRY(alloc_async(&ws, 2 * blk, st));
     char* send = (char*)ws;
     char* recv = send + blk;
     if ((s = mm_ntt_fwd_cols(plan, local_in, send, (size_t)r * g.c1, g.c1, stream)) == MM_OK &&
@@ -370,7 +370,7 @@ extern "C" mm_status mm_ntt_inverse_dist(mm_dist* D, const mm_ntt_plan* plan, co
     const int r = D->rank;
     const size_t blk = (size_t)g.n2 * g.c1 * g.es;
     void* ws = nullptr;
-    MM_CUDA_TRY(cudaMallocAsync(&ws, 2 * blk, st));
+    MM_CUDA_TRY(alloc_async(&ws, 2 * blk, st));
     char* send = (char*)ws;
     char* recv = send + blk;
     if ((s = mm_ntt_inv_rows_seg(plan, local_in, send, (size_t)r * g.r2, g.r2, g.c1, g.r2 * g.c1, stream)) == MM_OK &&
@@ -413,7 +413,7 @@ extern "C" mm_status mm_int_mul_u16_dist(mm_dist* D, const uint16_t* a, size_t n
     // workspace: send, recvA, recvB, coefficients, halo out / in, aggregates
     const size_t halo = (size_t)g.n2 * 4 * 8, agg = (size_t)g.n2 * 4, agg_all = (size_t)G * g.n2 * 4;
     void* ws = nullptr;
-    MM_CUDA_TRY(cudaMallocAsync(&ws, 4 * blk + 2 * halo + agg + agg_all + 256, st));
+    MM_CUDA_TRY(alloc_async(&ws, 4 * blk + 2 * halo + agg + agg_all + 256, st));
     char* send = (char*)ws;
     char* ra = send + blk;
     char* rb = ra + blk;

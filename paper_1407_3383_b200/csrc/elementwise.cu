@@ -112,7 +112,7 @@ static mm_status range_check(const uint32_t* v, size_t n, uint32_t p, cudaStream
     if (!v || !n) return MM_OK;
     unsigned long long* d = nullptr;
     unsigned long long h = 0;
-    MM_CUDA_TRY(cudaMallocAsync(&d, sizeof(*d), st));
+    MM_CUDA_TRY(alloc_async((void**)&d, sizeof(*d), st));
     MM_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(*d), st));
     {
         LaunchScope ls("range_check", st);

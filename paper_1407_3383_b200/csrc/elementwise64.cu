@@ -51,7 +51,7 @@ __global__ void k_range64(const uint64_t* __restrict__ x, long long n, unsigned*
 
 static mm_status range64(const uint64_t* x, size_t n, cudaStream_t st) {
     unsigned* bad = nullptr;
-    MM_CUDA_TRY(cudaMallocAsync((void**)&bad, sizeof(unsigned), st));
+    MM_CUDA_TRY(alloc_async((void**)&bad, sizeof(unsigned), st));
     MM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
     {
         LaunchScope ls("debug_range_check", st);

@@ -1292,7 +1292,7 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
 
 // NATURAL-order transforms on the four-step path go through a bit-mirror
 // permutation of a temporary: a stream-ordered allocation
-// (cudaMallocAsync / cudaFreeAsync from the device's default pool), so the
+// (alloc_async / cudaFreeAsync from the library's memory pool), so the
 // plan holds no mutable workspace and calls on different streams sharing a
 // plan never touch the same buffer, and nothing here synchronises.
 template <class T>
@@ -1380,7 +1380,7 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     }
     if (order == MM_ORDER_NATURAL) {   // Algorithm 1's TFT order into a temporary, then the permutation
         void* tmp = nullptr;
-        MM_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * P->batch * sizeof(T), st));
+        MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));
         mm_status s = fwd_impl<F>(P, in, tmp, MM_ORDER_BITREV, st);
         if (s == MM_OK) s = bitrev_rows<T>(tmp, out, P->k, (long long)P->batch, st);
         cudaFreeAsync(tmp, st);
@@ -1471,7 +1471,7 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     const void* src = in;
     if (order == MM_ORDER_NATURAL) {   // permute into a temporary, then the TFT-order inverse
         void* tmp = nullptr;
-        MM_CUDA_TRY(cudaMallocAsync(&tmp, (size_t)n * P->batch * sizeof(T), st));
+        MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));
         s = bitrev_rows<T>(in, tmp, P->k, (long long)P->batch, st);
         if (s == MM_OK) s = inv_impl<F>(P, tmp, out, MM_ORDER_BITREV, st);
         cudaFreeAsync(tmp, st);
@@ -1786,7 +1786,7 @@ static mm_status stream_ws(cudaStream_t st, size_t bytes, void** out) {
             e.first = nullptr;
             e.second = 0;
         }
-        MM_CUDA_TRY(cudaMallocAsync(&e.first, bytes, st));
+        MM_CUDA_TRY(alloc_async(&e.first, bytes, st));
         e.second = bytes;
     }
     *out = e.first;
@@ -1816,7 +1816,7 @@ static mm_status stream_ws_slot(cudaStream_t st, int slot, size_t bytes, void** 
             e.first = nullptr;
             e.second = 0;
         }
-        MM_CUDA_TRY(cudaMallocAsync(&e.first, bytes, st));
+        MM_CUDA_TRY(alloc_async(&e.first, bytes, st));
         e.second = bytes;
     }
     *out = e.first;
@@ -2411,10 +2411,7 @@ extern "C" mm_status mm_release_cached(void) {
         }
     }
     MM_CUDA_TRY(cudaDeviceSynchronize());
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    trim_pool();
     return MM_OK;
 }
 

@@ -932,7 +932,7 @@ static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
     if (s != MM_OK) return s;
     long long tiles = (a.nrows + K::Lay::C - 1) / K::Lay::C;
     const int grid = grid_for(kern, smem, tiles, NTr<F, LOGL>::v);
-    if (K::SB) MM_CUDA_TRY(cudaMallocAsync(&a.scratch, (size_t)grid * (1u << LOGL) * sizeof(T), st));
+    if (K::SB) MM_CUDA_TRY(alloc_async(&a.scratch, (size_t)grid * (1u << LOGL) * sizeof(T), st));
     {
         LaunchScope ls(a.fs ? "pmul_rows_fourstep" : "pmul_rows_single", st);
         kern<<<grid, NTr<F, LOGL>::v, smem, st>>>(f, a);

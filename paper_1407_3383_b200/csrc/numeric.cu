@@ -211,7 +211,7 @@ static const char* num_name(int v, bool mul) {
 template <class F>
 static mm_status range_check(const F* x, size_t n, F bound, cudaStream_t st) {
     unsigned* bad = nullptr;
-    MM_CUDA_TRY(cudaMallocAsync((void**)&bad, sizeof(unsigned), st));
+    MM_CUDA_TRY(alloc_async((void**)&bad, sizeof(unsigned), st));
     MM_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
     {
         LaunchScope ls("debug_range_check", st);

@@ -884,6 +884,39 @@ def test_dist_int_mul_c_abi_single_rank(mm, O, na, nb):
     D.close()
 
 
+@pytest.mark.slow
+def test_dist_int_mul_c_abi_c5_full(mm, O, c5_ref):
+    # mm_int_mul_u16_dist (one-rank communicator) at the full C5 shape, every
+    # limb against the oracle's product
+    n = 1 << 24
+    a = gen.limbs16_torch(config_seed(5), 1, n, DEV).view(torch.uint16)
+    b = gen.limbs16_torch(config_seed(5), 2, n, DEV).view(torch.uint16)
+    D = mm.Dist.single()
+    got = host(D.int_mul_u16(a, b)).reshape(-1)
+    D.close()
+    assert np.array_equal(got[:2 * n], c5_ref[2])
+
+
+def test_ntt_natural_order_stream_temporaries(mm, O):
+    # NATURAL-order four-step calls permute through library-pool temporaries:
+    # repeated calls on two streams sharing one plan stay correct
+    p, k, B = P30, 16, 64
+    w = O.root_of_unity(3, k, p)
+    plan = mm.NttPlan(32, p, k, w, B)
+    x = gen.residues_torch(config_seed(3), 9, B << k, p, DEV).view(torch.uint32)
+    ref = plan.forward(x, out=torch.empty_like(x), order=mm.NATURAL)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for s in (s1, s2, s1, s2):
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            outs.append(plan.forward(x, out=torch.empty_like(x), order=mm.NATURAL))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int32), ref.view(torch.int32))
+    assert np.array_equal(u64(host(ref[:1 << k])), O.ntt(host(x[:1 << k]), w, p))
+
+
 def _ipc_worker(rank, world, port):
     import os
     import torch.distributed as dist
