@@ -497,11 +497,14 @@ def extras_run(mm, torch, dev, peaks):
     y16 = torch.empty_like(x16)
     msf = tloop(lambda: pl16.forward(x16, out=y16, order=mm.BITREV), 10)
     msi = tloop(lambda: pl16.inverse(y16, out=x16, order=mm.BITREV), 10)
+    msn = tloop(lambda: pl16.forward(x16, out=y16, order=mm.NATURAL), 10)
+    msni = tloop(lambda: pl16.inverse(y16, out=x16, order=mm.NATURAL), 10)
     bf16 = 4096 * (1 << 15) * 16
     out["C3_fwd_4096x2^16"] = {"forward_ms": round(msf, 4), "forward_Gbutterfly_per_s": round(bf16 / (msf * 1e-3) / 1e9, 1),
                                "inverse_ms": round(msi, 4), "inverse_Gbutterfly_per_s": round(bf16 / (msi * 1e-3) / 1e9, 1),
                                "hbm_frac_2pass": round(4 * 4096 * (1 << 16) * 4 / (msf * 1e-3) / 1e9 / hbm, 3),
                                "hbm_frac_1pass": round(2 * 4096 * (1 << 16) * 4 / (msf * 1e-3) / 1e9 / hbm, 3),
+                               "forward_natural_ms": round(msn, 4), "inverse_natural_ms": round(msni, 4),
                                "alu_frac": round(bf16 / (msf * 1e-3) / (nsm * 16 * clk), 3),
                                "note": "SURVEY 8(d) C3-fwd: 1-pass = 8 B/elem (the contract), 2-pass = 16 B/elem"}
     del x16, y16, pl16

@@ -71,6 +71,10 @@ mm_status launch_row_fwd(const RowArgs32& a, cudaStream_t st);
 mm_status launch_row_inv(const RowArgs32& a, cudaStream_t st);
 mm_status launch_row_pmul(const RowPmulArgs& a, cudaStream_t st);
 mm_status launch_col_inv(const ColInvArgs& a, cudaStream_t st);
+// NATURAL-order variants of the plain row passes (no permutation pass):
+// forward rows -> natural spectrum; natural spectrum -> inverse rows
+mm_status launch_row_fwd_nat(const RowArgs32& a, cudaStream_t st);
+mm_status launch_row_inv_nat(const RowArgs32& a, cudaStream_t st);
 
 }  // namespace f32
 }  // namespace mm

@@ -1378,6 +1378,34 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
         a.lvl = (const W*)P->lvl_f1;
         return launch_rows<F, false, T, T>(f, a, st);
     }
+    if constexpr (sizeof(T) == 4) {
+        if (order == MM_ORDER_NATURAL && P->fast16 && ((uintptr_t)out & 15) == 0) {
+            // 256 x 256: column pass into a temporary, natural-order row pass into out
+            void* tmp = nullptr;
+            MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::ColFwdArgs cf{};
+            cf.in = (const uint32_t*)in; cf.out = (uint32_t*)tmp;
+            cf.nbatch = (long long)P->batch;
+            cf.in_bs = cf.in_len = cf.out_bs = n;
+            cf.lvl = (const uint2*)P->lvl_f2;
+            cf.fs = (const uint2*)P->fs_full_f;
+            cf.tc = P->tw_f2;
+            cf.f = ff;
+            mm_status s = f32::launch_col_fwd(cf, st);
+            if (s == MM_OK) {
+                f32::RowArgs32 ra{};
+                ra.in = (const uint32_t*)tmp; ra.out = (uint32_t*)out;
+                ra.nrows = (long long)P->batch << 8;
+                ra.lvl = (const uint2*)P->lvl_f1;
+                ra.tc = P->tw_f1;
+                ra.f = ff;
+                s = f32::launch_row_fwd_nat(ra, st);
+            }
+            cudaFreeAsync(tmp, st);
+            return s;
+        }
+    }
     if (order == MM_ORDER_NATURAL) {   // Algorithm 1's TFT order into a temporary, then the permutation
         void* tmp = nullptr;
         MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));
@@ -1469,6 +1497,35 @@ static mm_status inv_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     }
     mm_status s;
     const void* src = in;
+    if constexpr (sizeof(T) == 4) {
+        if (order == MM_ORDER_NATURAL && P->fast16 && ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+            // 256 x 256: natural-order inverse row pass into a temporary, column pass into out
+            void* tmp = nullptr;
+            MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));
+            const f32::Fld ff{(uint32_t)P->p, 2 * (uint32_t)P->p, P->pinv};
+            f32::RowArgs32 ra{};
+            ra.in = (const uint32_t*)in; ra.out = (uint32_t*)tmp;
+            ra.nrows = (long long)P->batch << 8;
+            ra.lvl = (const uint2*)P->lvl_i1;
+            ra.fsi = (const uint2*)P->fs_ni_i;
+            ra.tc = P->tw_i1;
+            ra.f = ff;
+            s = f32::launch_row_inv_nat(ra, st);
+            if (s == MM_OK) {
+                f32::ColInvArgs ci{};
+                ci.in = (const uint32_t*)tmp; ci.out = (uint32_t*)out;
+                ci.nbatch = (long long)P->batch;
+                ci.in_bs = n;
+                ci.out_bs = ci.out_len = n;
+                ci.lvl = (const uint2*)P->lvl_i2;
+                ci.tc = P->tw_i2;
+                ci.f = ff;
+                s = f32::launch_col_inv(ci, st);
+            }
+            cudaFreeAsync(tmp, st);
+            return s;
+        }
+    }
     if (order == MM_ORDER_NATURAL) {   // permute into a temporary, then the TFT-order inverse
         void* tmp = nullptr;
         MM_CUDA_TRY(alloc_async(&tmp, (size_t)n * P->batch * sizeof(T), st));

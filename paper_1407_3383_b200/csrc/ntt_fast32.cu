@@ -519,6 +519,105 @@ __global__ void __launch_bounds__(NT, 4) k_row_inv(RowArgs32 a) {
     }
 }
 
+// ---------------------------------------------------------------- natural-order row passes
+// NATURAL order without a permutation pass.  The output of Algorithm 1 at
+// row i2, position i1 is frequency f1 256 + f2 with f1 = [i1]_8, f2 = [i2]_8
+// ([i2 256 + i1]_16 = [i1]_8 256 + [i2]_8).  A tile takes the 16 rows
+// whose frequencies f2 = 16 g + r are consecutive (row i2 = [f2]_8), so for
+// every f1 it owns 16 consecutive output words (64 B): the row results are
+// staged in shared memory as [f1][r] (pitch 17: conflict-free both ways) and
+// leave as 128-bit stores.  The inverse reads the natural spectrum the same
+// way and hands the rows to the column pass in its usual layout.
+constexpr int NATP = 17;            // staging pitch (words) of one f1 row
+__device__ __forceinline__ int brev8i(int x) { return (int)(__brev((unsigned)x) >> 24); }
+
+__global__ void __launch_bounds__(NT, 4) k_row_fwd_nat(RowArgs32 a) {
+    __shared__ uint2 tw[256];
+    __shared__ __align__(16) uint32_t sa[16 * ROWP];   // row exchange, then the [256][NATP] staging
+    for (int i = threadIdx.x; i < 256; i += NT) tw[i] = a.lvl[i];
+    const int r = threadIdx.x >> 4, lo = threadIdx.x & 15;
+    const long long ntiles = a.nrows >> 4;
+    const Fld f = a.f;
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long b = tile >> 4;
+        const int g = (int)(tile & 15);
+        const long long row = b * 256 + brev8i(16 * g + r);
+        uint32_t v[1][16];
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[0][t] = __ldg(a.in + row * 256 + lo + 16 * t);
+        dif_tab<1>(v, lo, tw, f, false);
+#pragma unroll
+        for (int t = 0; t < 16; t++) sa[r * ROWP + pad_word(lo + 16 * t)] = v[0][t];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint4 x = *(const uint4*)(sa + r * ROWP + pad_word(16 * lo + 4 * i));
+            v[0][4 * i] = x.x; v[0][4 * i + 1] = x.y; v[0][4 * i + 2] = x.z; v[0][4 * i + 3] = x.w;
+        }
+        dif_const(v[0], a.tc, f);
+        __syncthreads();                                  // every warp is done with its exchange rows
+#pragma unroll
+        for (int j = 0; j < 16; j++) sa[brev8i(16 * lo + j) * NATP + r] = canon4(v[0][j], f);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; k++) {                     // four lanes per 64-byte segment: whole sectors per warp
+            const int f1 = 64 * k + (threadIdx.x >> 2), q = threadIdx.x & 3;
+            const uint32_t* src = sa + f1 * NATP + 4 * q;
+            *(uint4*)(a.out + b * 65536 + (long long)f1 * 256 + 16 * g + 4 * q) =
+                make_uint4(src[0], src[1], src[2], src[3]);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NT, 4) k_row_inv_nat(RowArgs32 a) {
+    __shared__ uint2 tw[256];
+    __shared__ __align__(16) uint32_t sa[16 * ROWP];
+    for (int i = threadIdx.x; i < 256; i += NT) tw[i] = a.lvl[i];
+    const int r = threadIdx.x >> 4, lo = threadIdx.x & 15;
+    const long long ntiles = a.nrows >> 4;
+    const Fld f = a.f;
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long b = tile >> 4;
+        const int g = (int)(tile & 15);
+        const int i2 = brev8i(16 * g + r);
+        {
+            uint4 x[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {                 // four lanes per 64-byte segment
+                const int f1 = 64 * k + (threadIdx.x >> 2), q = threadIdx.x & 3;
+                x[k] = __ldg((const uint4*)(a.in + b * 65536 + (long long)f1 * 256 + 16 * g + 4 * q));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int f1 = 64 * k + (threadIdx.x >> 2), q = threadIdx.x & 3;
+                uint32_t* d = sa + f1 * NATP + 4 * q;
+                d[0] = x[k].x; d[1] = x[k].y; d[2] = x[k].z; d[3] = x[k].w;
+            }
+        }
+        __syncthreads();
+        uint32_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) v[j] = sa[brev8i(16 * lo + j) * NATP + r];   // position 16 lo + j of row i2
+        __syncthreads();                                  // staging read before the exchange reuses sa
+        dit_const(v, a.tc, f);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            *(uint4*)(sa + r * ROWP + pad_word(16 * lo + 4 * i)) = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 16; t++) v[t] = sa[r * ROWP + pad_word(lo + 16 * t)];
+        dit_tab<false>(v, lo, tw, f);
+        const uint2* fsr = a.fsi + i2 * 256 + lo;
+        uint32_t* dst = a.out + (b * 256 + i2) * 256 + lo;
+#pragma unroll
+        for (int t = 0; t < 16; t++) dst[16 * t] = mulw(v[t], __ldg(fsr + 16 * t), f);
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
     int per_sm = 0;
@@ -616,6 +715,24 @@ mm_status launch_row_inv(const RowArgs32& a, cudaStream_t st) {
     {
         LaunchScope ls("ntt_rows_inv", st);
         k_row_inv<<<grid_of(k_row_inv, a.nrows / 16, 0), NT, 0, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_row_fwd_nat(const RowArgs32& a, cudaStream_t st) {
+    if (a.nrows % 256 || (((uintptr_t)a.out) & 15)) return set_err(MM_E_ARG, "natural row pass needs whole 2^16 rows");
+    {
+        LaunchScope ls("ntt_rows_fwd_natural", st);
+        k_row_fwd_nat<<<grid_of(k_row_fwd_nat, a.nrows / 16, 0), NT, 0, st>>>(a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+mm_status launch_row_inv_nat(const RowArgs32& a, cudaStream_t st) {
+    if (a.nrows % 256 || (((uintptr_t)a.in) & 15)) return set_err(MM_E_ARG, "natural row pass needs whole 2^16 rows");
+    {
+        LaunchScope ls("ntt_rows_inv_natural", st);
+        k_row_inv_nat<<<grid_of(k_row_inv_nat, a.nrows / 16, 0), NT, 0, st>>>(a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
