@@ -496,8 +496,9 @@ def extras_run(mm, torch, dev, peaks):
     for fbits, pn, nn, variants in ((64, 33554393, 1 << 27, (0, 1, 2, 3, 4, 5)), (64, 1125899906842597, 1 << 27, (4, 5)),
                                     (32, 2039, 1 << 28, (0, 1, 2, 3, 4, 5)), (32, 2097143, 1 << 28, (4, 5))):
         dt = torch.float64 if fbits == 64 else torch.float32
-        xn = gen.residues_torch(11, 1, nn, pn, dev).view(torch.int64).to(dt)
-        yn = gen.residues_torch(11, 2, nn, pn, dev).view(torch.int64).to(dt)
+        xn = gen.residues_torch(11, 1, nn, pn, dev).to(torch.int64).to(dt)    # int32 (p < 2^32) or int64 words
+        yn = gen.residues_torch(11, 2, nn, pn, dev).to(torch.int64).to(dt)
+        assert xn.numel() == nn
         zn = torch.empty_like(xn)
         MN = mm.ModNum(fbits, pn)
         names = ["F14", "F14_up", "F15_up", "F15_near", "F16", "F16_up"]
@@ -842,9 +843,10 @@ def run_ours(args, world, rank, local):
     # butterflies / clk / SM, at the max SM clock.
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_bfly_peak = nsm * 16 * sm_mhz_max * 1e6
-    # the issue rates the ALU peak is derived from, measured on this GPU (mm_probe_issue)
+    # the issue rates the ALU peak is derived from, measured on this GPU (mm_probe_issue),
+    # after the timed regions so that the clocks have ramped up
     clk_hz = sm_mhz_max * 1e6
-    rates = {nm: round(mm.probe_issue(kind, 8000) / (nsm * clk_hz), 3) for kind, nm in ((0, "IMAD"), (1, "IMAD.HI"))}
+    rates = {nm: round(mm.probe_issue(kind, 4000) / (nsm * clk_hz), 3) for kind, nm in ((0, "IMAD"), (1, "IMAD.HI"))}
     for k_, (cnt, tot) in prof.items():
         per = tot / cnt
         entry = {"launches": cnt, "avg_ms": round(per, 4), "share": round(tot / (ms_serial * args.steps), 3)}

@@ -80,6 +80,14 @@ def launches(path: str, out: str):
     lines = [f"# ncu launch list summary: {path}", "# family launches mean_ms total_ms share"]
     for f, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"{f:45s} {n:6d} {ms / n:10.4f} {ms:10.4f} {ms / tot:7.3f}")
+    # the list also holds the generator, probe, e2e-chunk and warm-up launches:
+    # the shares to compare with bench.py's "kernels" are those within the C3 step
+    step = [f for f in ("k_col_fwd", "k_row_pmul", "k_col_inv") if f in agg]
+    if step:
+        st = sum(agg[f][1] for f in step)
+        lines.append("# shares within the C3 step kernels (compare bench.py kernels[*].share):")
+        for f in step:
+            lines.append(f"#   {f:20s} {agg[f][1] / st:7.3f}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
