@@ -13,6 +13,7 @@ which = sys.argv[1] if len(sys.argv) > 1 else "c3"
 dev = torch.device("cuda")
 P30, PG = 998244353, (1 << 64) - (1 << 32) + 1
 if which == "c3":
+    mm.set_product_streams(1)   # whole-batch launches, as bench.py's per-kernel roofline pass
     B, d = 4096, 1 << 15
     a = gen.residues_torch(gen.config_seed(3), 1, B * d, P30, dev).view(torch.uint32).reshape(B, d)
     b = gen.residues_torch(gen.config_seed(3), 2, B * d, P30, dev).view(torch.uint32).reshape(B, d)
