@@ -1040,3 +1040,42 @@ def test_poly_mul_fork_streams(mm, O):
             mm.set_product_streams(0)
     finally:
         mm.set_product_streams(2)
+
+
+def test_poly_mul_fork_odd_batch_strided(mm, O):
+    # 257 products (sub-batches of 129 + 128) with padded output rows (ldc = 2^16):
+    # the fork path equals the one-stream path, sampled rows equal the oracle
+    p, g, B, d = P30, 3, 257, (1 << 15) - 3
+    a = gen.residues_torch(config_seed(3), 11, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    b = gen.residues_torch(config_seed(3), 12, B * d, p, DEV).view(torch.uint32).reshape(B, d)
+    cp = torch.zeros((B, 1 << 16), dtype=torch.uint32, device=DEV)
+    c = cp[:, :2 * d - 1]
+    mm.set_product_streams(2)
+    mm.poly_mul(a, b, p, g, out=c)
+    mm.set_product_streams(1)
+    try:
+        ref = mm.poly_mul(a, b, p, g)
+    finally:
+        mm.set_product_streams(2)
+    assert torch.equal(c.contiguous().view(torch.int32), ref.view(torch.int32))
+    assert not cp[:, 2 * d - 1:].view(torch.int32).any()          # padding columns untouched
+    for r in (0, 128, 129, 256):
+        assert np.array_equal(u64(host(ref[r])), O.poly_mul_ntt(host(a[r]), host(b[r]), p, g)), r
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+def test_ntt16_natural_in_place(mm, O, batch):
+    # the natural-order 2^16 row passes, in place and out of place, batch 1 and 3
+    p, k = P30, 16
+    w = O.root_of_unity(3, k, p)
+    plan = mm.NttPlan(32, p, k, w, batch)
+    x = residues(17, batch, batch << k, p).reshape(batch, 1 << k)
+    xt = dev(x)
+    y = xt.clone()
+    plan.forward(y, order=mm.NATURAL)                                 # in place
+    nat = O.ntt_rows(x, w, p)
+    assert np.array_equal(u64(host(y)), nat)
+    z = plan.inverse(y, out=torch.empty_like(y), order=mm.NATURAL)
+    assert torch.equal(z, xt)
+    plan.inverse(y, order=mm.NATURAL)                                 # in place
+    assert torch.equal(y, xt)
