@@ -5,6 +5,7 @@ tiles and a ragged tail; the BASELINE full-size configs are checked on
 sampled outputs (or properties that hold at any size) in the launch
 configuration bench.py uses.
 """
+import os
 import random
 
 import numpy as np
@@ -103,6 +104,37 @@ def test_elementwise_inplace_and_empty(mm, O):
     assert np.array_equal(u64(host(xt)), O.vec_addmod(u64(x), u64(y), P32))
     e = torch.empty(0, dtype=torch.uint32, device=DEV)
     M.mul(e, e)
+
+
+@pytest.mark.slow
+def test_elementwise_full_c2_all(mm, O):
+    # BASELINE C2 at full size: every one of the 2^28 outputs of every operation
+    # against the oracle (2^24-element chunks checked on host threads)
+    from concurrent.futures import ThreadPoolExecutor
+    p, n, CH = P32, 1 << 28, 1 << 24
+    x = gen.residues_torch(config_seed(2), 1, n, p, DEV).view(torch.uint32)
+    y = gen.residues_torch(config_seed(2), 2, n, p, DEV).view(torch.uint32)
+    M = mm.Mod32(p)
+    ysh = M.shoup_precompute(y)
+    xh = u64(host(x.view(torch.int32)).view(np.uint32))
+    yh = u64(host(y.view(torch.int32)).view(np.uint32))
+    ops = [("add", lambda: M.add(x, y), lambda a, b: O.vec_addmod(a, b, p)),
+           ("sub", lambda: M.sub(x, y), lambda a, b: O.vec_submod(a, b, p)),
+           ("mont", lambda: M.mul(x, y, mm.MUL_MONTGOMERY), lambda a, b: O.vec_montmul(a, b, p, 32)),
+           ("barrett", lambda: M.mul(x, y, mm.MUL_BARRETT), lambda a, b: O.vec_mulmod(a, b, p)),
+           ("shoup", lambda: M.mul(x, y, mm.MUL_SHOUP, y_shoup=ysh), lambda a, b: O.vec_mulmod(a, b, p)),
+           ("shoup_psi", lambda: ysh, lambda a, b: O.vec_shoup_psi(b, p, 32))]
+    nt = max(1, min(32, os.cpu_count() or 1))
+    for name, gpu, ref in ops:
+        z = u64(host(gpu().view(torch.int32)).view(np.uint32))
+
+        def ok(i):
+            sl = slice(i * CH, (i + 1) * CH)
+            return np.array_equal(z[sl], ref(xh[sl], yh[sl]))
+        with ThreadPoolExecutor(nt) as ex:
+            res = list(ex.map(ok, range(n // CH)))
+        assert all(res), (name, [i for i, r in enumerate(res) if not r][:5])
+        del z
 
 
 def test_elementwise_full_c2_sampled(mm, O):
@@ -330,16 +362,29 @@ def test_ntt_c1_batch(mm, O):
     assert np.array_equal(host(plan.inverse(y, order=mm.NATURAL)), x)
 
 
-def test_ntt_c3_forward_sampled(mm, O):
-    # BASELINE C3 forward: 4096 x 2^16 over 998244353, sampled rows vs oracle
+def test_ntt_c3_forward_full(mm, O):
+    # BASELINE C3 forward: 4096 x 2^16 over 998244353, every row against the
+    # oracle's textbook NTT (host threads over rows), TFT and natural order
+    from concurrent.futures import ThreadPoolExecutor
     p, k, B = P30, 16, 4096
     w = O.root_of_unity(3, k, p)
     x = gen.residues_torch(config_seed(3), 1, B << k, p, DEV).view(torch.uint32).reshape(B, 1 << k)
     plan = mm.NttPlan(32, p, k, w, B)
-    y = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
-    for r in (0, 1, 1234, 4095):
-        xr = u64(host(x[r]))
-        assert np.array_equal(u64(host(y[r])), O.to_bitrev(O.ntt(xr, w, p))), r
+    yb = host(plan.forward(x, out=torch.empty_like(x), order=mm.BITREV))
+    yn = host(plan.forward(x, out=torch.empty_like(x), order=mm.NATURAL))
+    xh = host(x)
+
+    def bad_rows(rows):
+        out = []
+        for r in rows:
+            nat = O.ntt(u64(xh[r]), w, p)
+            if not (np.array_equal(u64(yn[r]), nat) and np.array_equal(u64(yb[r]), O.to_bitrev(nat))):
+                out.append(r)
+        return out
+    nt = max(1, min(32, os.cpu_count() or 1))
+    with ThreadPoolExecutor(nt) as ex:
+        bad = sum(ex.map(bad_rows, [range(t, B, nt) for t in range(nt)]), [])
+    assert not bad, bad[:10]
 
 
 def test_ntt_c4_sampled(mm, O):
@@ -363,30 +408,28 @@ def test_ntt_c4_sampled(mm, O):
 
 @pytest.mark.slow
 def test_ntt_c4_full(mm, O):
-    # BASELINE C4 at full size: one of the 8 transforms of 2^24 compared element by
+    # BASELINE C4 at full size: all 8 transforms of 2^24 compared element by
     # element with the oracle's textbook NTT in both output orders, in the
-    # bench launch configuration (batch 8, the 2^13-row x 2^11-column four-step
-    # with the full 2^24 step-2 table); the other 7 rows by sampled points
-    k, B, t = 24, 8, 5
+    # bench launch configuration (batch 8: the 2^13-row x 2^11-column four-step
+    # with the full 2^24 step-2 table, sub-batches on the fork streams); the
+    # oracle transforms run on host threads (~10 s each)
+    from concurrent.futures import ThreadPoolExecutor
+    k, B = 24, 8
     w = O.root_of_unity(7, k, PG)
     x = gen.residues_torch(config_seed(4), 1, B << k, PG, DEV).view(torch.uint64).reshape(B, 1 << k)
     plan = mm.NttPlan(64, PG, k, w, B)
-    xt = host(x[t])
-    nat = O.ntt(xt, w, PG)                                   # ~10 s on one host core
+    xh = host(x)
+    with ThreadPoolExecutor(B) as ex:
+        nat = list(ex.map(lambda t: O.ntt(xh[t], w, PG), range(B)))
     yb = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
-    assert np.array_equal(host(yb[t]), O.to_bitrev(nat))
-    yb_t = host(yb[t])
+    ybh = host(yb)
+    for t in range(B):
+        assert np.array_equal(ybh[t], O.to_bitrev(nat[t])), t
     del yb
     yn = plan.forward(x, out=torch.empty_like(x), order=mm.NATURAL)
-    assert np.array_equal(host(yn[t]), nat)
-    rng = np.random.default_rng(44)
-    for b in range(B):
-        if b == t:
-            continue
-        xb = host(x[b])
-        for pos in rng.integers(0, 1 << k, 2):
-            assert int(host(yn[b, int(pos)])) == O.dft_point(xb, w, int(pos), PG), (b, pos)
-    assert np.array_equal(yb_t, O.to_bitrev(host(yn[t])))
+    ynh = host(yn)
+    for t in range(B):
+        assert np.array_equal(ynh[t], nat[t]), t
     z = plan.inverse(yn, out=torch.empty_like(yn), order=mm.NATURAL)
     assert torch.equal(z.view(torch.int64), x.view(torch.int64))
 
@@ -534,9 +577,9 @@ def test_poly_mul_c3_small_batch(mm, O):
         assert np.array_equal(c[r], O.poly_mul_ntt(a[r], b[r], p, g)), r
 
 
-def test_poly_mul_c3_full_sampled(mm, O):
+def test_poly_mul_c3_full(mm, O):
     # BASELINE C3 product: 4096 pairs of degree < 2^15 (bench launch config);
-    # every row checked by c(r) = a(r) b(r) at a random point, 3 rows in full.
+    # every row checked by c(r) = a(r) b(r) at a random point and in full.
     p, g, B, d = P30, 3, 4096, 1 << 15
     a = gen.residues_torch(config_seed(3), 1, B * d, p, DEV).view(torch.uint32).reshape(B, d)
     b = gen.residues_torch(config_seed(3), 2, B * d, p, DEV).view(torch.uint32).reshape(B, d)
@@ -550,8 +593,16 @@ def test_poly_mul_c3_full_sampled(mm, O):
     for r in range(0, B, 1):
         x = rng.randrange(1, p)
         assert O.poly_eval(ch[r], x, p) == O.mulmod(O.poly_eval(ah[r], x, p), O.poly_eval(bh[r], x, p), p), r
-    for r in (0, 2047, 4095):
-        assert np.array_equal(u64(ch[r]), O.poly_mul_ntt(ah[r], bh[r], p, g)), r
+    # every one of the 4096 products element by element against the oracle's NTT
+    # product (threads over rows: the ctypes calls release the GIL)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def bad_rows(rows):
+        return [r for r in rows if not np.array_equal(u64(ch[r]), O.poly_mul_ntt(ah[r], bh[r], p, g))]
+    nt = max(1, min(32, os.cpu_count() or 1))
+    with ThreadPoolExecutor(nt) as ex:
+        bad = sum(ex.map(bad_rows, [range(t, B, nt) for t in range(nt)]), [])
+    assert not bad, bad[:10]
 
 
 # ------------------------------------------------------------------ polynomial matrix product
