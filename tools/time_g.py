@@ -28,6 +28,7 @@ def tloop(fn, reps=10, warm=3):
 
 
 def kern(fn, reps=5):
+    mm.set_product_streams(1)   # kernels serialised on one stream: their times add up
     fn()
     torch.cuda.synchronize()
     mm.prof_collect()
@@ -36,6 +37,7 @@ def kern(fn, reps=5):
         fn()
     r = mm.prof_collect()
     mm.prof_enable(False)
+    mm.set_product_streams(2)
     return {k: round(v[1] / reps, 4) for k, v in r.items()}
 
 
@@ -48,6 +50,9 @@ f = lambda: plan.forward(x, out=y, order=mm.BITREV)
 g = lambda: plan.inverse(y, out=z, order=mm.BITREV)
 out["C4_fwd_ms"] = round(tloop(f), 4)
 out["C4_inv_ms"] = round(tloop(g), 4)
+mm.set_product_streams(1)
+out["C4_fwd_ms_one_stream"] = round(tloop(f), 4)
+mm.set_product_streams(2)
 out["C4_fwd_kernels"] = kern(f)
 out["C4_roundtrip_ok"] = bool(torch.equal(z, x))
 del x, y, z, plan
