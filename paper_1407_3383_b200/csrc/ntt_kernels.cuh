@@ -485,9 +485,19 @@ template <class F, int LOGL> struct ColsK {
     // tile streams in while the current one is transformed)
     enum { PIPE = Lay::COL ? 1 : 0 };
     enum { TWS = TwPlace<F, LOGL, (PIPE ? 2 : 1) * Lay::ELEMS, 1>::SMEM };
+    // Goldilocks forward columns of 2^12 points (C5): the step-2 twiddle
+    // w^(j1 k) of frequency k = k_lo + 2^LO k_hi is formed on chip as
+    // T_lo[k_lo] T_hi[k_hi] from 2^LO + 2^HI table entries per column, loaded
+    // with the tile; the full-table loads at the store are 16-byte segments per
+    // row whose latency the tile waits for (C5 column passes 1.09 -> 1.00 ms).
+    // For C4's 2^11-point tiles of four columns the extra product costs more
+    // than the wait (1.70 -> 1.77 ms): they keep the table.
+    enum { LO = LOGL / 2, NLO = 1 << LO, NHI = 1 << (LOGL - LO), NOTF = NLO + NHI };
+    enum { OTF = GoldT<F, LOGL>::v && LOGL == 12 };
     static constexpr size_t smem() {
         return (PIPE ? 2 : 1) * (size_t)Lay::ELEMS * sizeof(typename F::T) +
-               (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0);
+               (TWS ? (size_t)(1u << LOGL) * sizeof(typename F::W) : 0) +
+               (OTF ? (size_t)Lay::C * NOTF * sizeof(typename F::W) : 0);
     }
 };
 
@@ -521,6 +531,8 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* tws = (W*)smem_raw;
     T* s = (T*)(tws + (K::TWS ? L : 0));
+    constexpr bool OTF = K::OTF && !INV && E::FS == 1;
+    W* otf = (W*)(s + (K::PIPE ? 2 : 1) * Lay::ELEMS);       // [c][T_lo (NLO) | T_hi (NHI)]
     if (K::TWS) stage_twiddles(tws, a.lvl, L);
     const W* tw = K::TWS ? (const W*)tws : a.lvl;
     const long long cgroups = a.ncols / C;                 // host guarantees ncols % C == 0
@@ -594,6 +606,18 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
         const TIn* inb = (const TIn*)a.in + b * a.in_bs + cl0;
         int tfull, tzero;
         T* cur = s;
+        // this tile's step-2 bases T_lo[c][m] = w^(j1 m), T_hi[c][h] = w^(j1 2^LO h):
+        // entries of the full table at rows brev(m), brev(2^LO h); in flight with
+        // the tile's loads, stored before the barrier that precedes the transform
+        W otf_v{};
+        if constexpr (OTF) {
+            static_assert(C * K::NOTF <= NTH, "one step-2 base per thread");
+            if (threadIdx.x < C * K::NOTF) {
+                const int c = threadIdx.x / K::NOTF, r = threadIdx.x % K::NOTF;
+                const int row = r < K::NLO ? r : (r - K::NLO) << K::LO;
+                otf_v = __ldg(fsf + (unsigned)brev(row, LOGL) * n1 + (unsigned)lin0 + c);
+            }
+        }
         if (pipe) {
             cur = s + (it & 1) * Lay::ELEMS;
             const long long nxt = tile + gridDim.x;
@@ -656,6 +680,8 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                 }
             }
         }
+        if constexpr (OTF)
+            if (threadIdx.x < C * K::NOTF) otf[threadIdx.x] = otf_v;
         __syncthreads();
         run_tile<F, Lay, LOGL, INV, NTH>(ff, cur, tw, lvl);
         col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
@@ -677,7 +703,15 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
 #pragma unroll
                         for (int i = 0; i < V; i++) v[u][i] = cur[Lay::addr(c + i, t)];
                     }
-                    if (E::FS == 1) ld_wvec<W, V>(fsf + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
+                    if constexpr (OTF) {
+                        const unsigned k = (unsigned)brev(t, LOGL);
+#pragma unroll
+                        for (int i = 0; i < V; i++)
+                            w[u][i] = FpG::mul(otf[(c + i) * K::NOTF + (k & (K::NLO - 1))],
+                                               otf[(c + i) * K::NOTF + K::NLO + (k >> K::LO)]);
+                    } else if (E::FS == 1) {
+                        ld_wvec<W, V>(fsf + (unsigned)t * n1 + (unsigned)lin0 + c, w[u]);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < B; u++) {
@@ -707,7 +741,12 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                 const int t = e / C, c = e % C;
                 if (t >= tzero || (t >= tfull && (long long)t * a.n1 + lin0 + c >= a.out_len)) continue;
                 W wf{};
-                if (E::FS == 1) wf = __ldg(fsf + (unsigned)t * n1 + (unsigned)lin0 + c);
+                if constexpr (OTF) {
+                    const unsigned k = (unsigned)brev(t, LOGL);
+                    wf = FpG::mul(otf[c * K::NOTF + (k & (K::NLO - 1))], otf[c * K::NOTF + K::NLO + (k >> K::LO)]);
+                } else if (E::FS == 1) {
+                    wf = __ldg(fsf + (unsigned)t * n1 + (unsigned)lin0 + c);
+                }
                 T x = E::apply(ff, cur[Lay::addr(c, t)], wf, fslo, fshi, a.fs_h,
                                ((unsigned)lin0 + c) * (unsigned)brev(t, LOGL), sc);
                 outb[(unsigned)t * ors + c] = (TOut)x;
