@@ -434,6 +434,31 @@ def test_ntt_c4_full(mm, O):
     assert torch.equal(z.view(torch.int64), x.view(torch.int64))
 
 
+@pytest.mark.slow
+def test_ntt64_2e25_full(mm, O):
+    # 2^25 Goldilocks transforms from 64-bit words: 2^13 columns of 2^12 points
+    # whose step-2 twiddles w^(j1 k) are formed on chip from per-column bases
+    # (T_lo[k mod 64] T_hi[k / 64], ColsK::OTF; C5 reaches the same tiles from
+    # 16-bit limbs), batch 2 so the sub-batches run on the fork streams; every
+    # output against the oracle's textbook NTT, then the round trip
+    from concurrent.futures import ThreadPoolExecutor
+    k, B = 25, 2
+    w = O.root_of_unity(7, k, PG)
+    x = gen.residues_torch(config_seed(4), 3, B << k, PG, DEV).view(torch.uint64).reshape(B, 1 << k)
+    plan = mm.NttPlan(64, PG, k, w, B)
+    inf = plan.info()
+    assert inf["n2"] == 1 << 12 and inf["n1"] == 1 << 13, inf
+    xh = host(x)
+    with ThreadPoolExecutor(B) as ex:
+        nat = list(ex.map(lambda t: O.ntt(xh[t], w, PG), range(B)))
+    yb = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
+    ybh = host(yb)
+    for t in range(B):
+        assert np.array_equal(ybh[t], O.to_bitrev(nat[t])), t
+    z = plan.inverse(yb, out=torch.empty_like(yb), order=mm.BITREV)
+    assert torch.equal(z.view(torch.int64), x.view(torch.int64))
+
+
 @pytest.mark.parametrize("k", [10, 11, 12, 20, 22, 23])
 @pytest.mark.parametrize("e", [1, 3, 65])
 def test_ntt64_gold_and_generic_tiles(mm, O, k, e):
