@@ -325,6 +325,18 @@ template <int NA, int CT> __device__ __forceinline__ void decode_a(int q, int& A
 // full[TS * e] = w_LN^e (natural powers, e < LN); the 64-th roots w_64^e = 2^(S e)
 // are shifts (rot), the digit they depend on being warp-uniform.
 // LN = NA * 64 with NA in {16, 32, 64}; RA = NA / 8.
+// stage A of dif_ln on RA values in registers: the RA-point DFT over ah
+// (j = 512 ah + 64 al + b), then w_NA^(al r) (al warp-uniform)
+template <int RA, int S> __device__ __forceinline__ void dif_a(uint64_t v[8], int al) {
+    if constexpr (RA == 8) dif8<S>(v);
+    else if constexpr (RA == 4) dif4<S>(v);
+    else dft2(v);
+    rot<S, 8 / RA, RA>(v, al);
+}
+
+template <class Lay, int LN, int H, int NT, int S>
+__device__ __forceinline__ void dif_ln_bcd(uint64_t* s, const uint64_t* __restrict__ full, int TS, int LQ);
+
 template <class Lay, int LN, int H, int NT, int S>
 __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__ full, int TS, int LQ) {
     constexpr int NA = LN / 64, RA = NA / 8, C = Lay::C;
@@ -337,14 +349,19 @@ __device__ __forceinline__ void dif_ln(uint64_t* s, const uint64_t* __restrict__
         uint64_t v[8];
 #pragma unroll
         for (int t = 0; t < RA; t++) v[t] = p0[Lay::off(512 * t)];
-        if constexpr (RA == 8) dif8<S>(v);
-        else if constexpr (RA == 4) dif4<S>(v);
-        else dft2(v);
-        rot<S, 8 / RA, RA>(v, al);      // w_NA^(al r), al warp-uniform
+        dif_a<RA, S>(v, al);
 #pragma unroll
         for (int t = 0; t < RA; t++) p0[Lay::off(512 * t)] = v[t];
     }
     __syncthreads();
+    dif_ln_bcd<Lay, LN, H, NT, S>(s, full, TS, LQ);
+}
+
+// stages B-D of dif_ln (stage A's output in s)
+template <class Lay, int LN, int H, int NT, int S>
+__device__ __forceinline__ void dif_ln_bcd(uint64_t* s, const uint64_t* __restrict__ full, int TS, int LQ) {
+    constexpr int NA = LN / 64, RA = NA / 8, C = Lay::C;
+    constexpr int CT = C * H;
     // stage B: 8-point DFTs over al (j = 512 P + 64 al + b), then w_LN^(b k_a)
     for (int q = threadIdx.x; q < CT * RA * 64; q += NT) {
         const int b = q & 63, P = (q >> 6) % RA, ct = q / (64 * RA);

@@ -25,6 +25,7 @@
 #include "common.h"
 #include "arith.cuh"
 #include "fast32.h"
+#include "tma.cuh"
 
 namespace mm {
 namespace f32 {
@@ -170,34 +171,6 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_by
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
-// TMA (cp.async.bulk.tensor): one elected thread moves a whole 32-column tile
-// (3-D tensor map {256 columns, rows per batch row, batch}, box {32, R, 1},
-// rows beyond the tensor zero-filled) and arms an mbarrier with its byte
-// count; every thread waits on the barrier's phase parity.
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile("{\n\t.reg .pred P1;\n"
-                 "LAB_WAIT:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-                 "@P1 bra DONE;\n\t"
-                 "bra LAB_WAIT;\n"
-                 "DONE:\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// issued by one thread: generic-proxy reads of dst must be ordered before the async write
-__device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar,
-                                              unsigned bytes) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-        ::"r"(smem_u32(dst)), "l"((const void*)tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // rows [0, RIN) of the 32-column block `tile` -> st[row * 32 + c]; element
 // (row, col) of batch row b is in[b * in_bs + row * 256 + col], valid iff
@@ -632,18 +605,6 @@ template <class K> static int grid_of(K kern, long long tiles, size_t smem) {
     return (int)(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }();
-    return fn;
-}
 // 3-D map of 32-bit words {256 columns, rows per batch row, batch}, box {32, box_rows, 1}
 static mm_status make_col_map(CUtensorMap* tm, const void* base, long long rows, long long batch, long long bstride_words,
                               int box_rows) {

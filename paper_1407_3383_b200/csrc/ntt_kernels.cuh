@@ -153,6 +153,12 @@ template <class F> struct ColArgs {
     const W* fshim[3];
     const W* fsfullm[3];
 };
+// Goldilocks forward column pass of 2^11-point columns with TMA-staged tiles
+// and step-2 twiddles (gold_cols.cu); taken by launch_cols_e when
+// gold_cols_tma_ok (full-length input, one modulus, no peer scatter)
+bool gold_cols_tma_ok(const ColArgs<FpG>& a);
+mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
+
 template <class F> struct PmulArgs {
     typedef typename F::W W;
     const void* a;
@@ -944,6 +950,9 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     a.vec_out = sizeof(TOut) == sizeof(T) && a.out_rs % V == 0 && (a.out_bs % V == 0 || a.nbatch == 1) &&
                 aligned16(a.out);
     if (a.npeers && !a.vec_out) return set_err(MM_E_ARG, "peer scatter needs 16-byte aligned rows");
+    if constexpr (std::is_same<F, FpG>::value && LOGL == 11 && !INV && EPIV == EPI_FS_FULL && sizeof(TIn) == 8 &&
+                  sizeof(TOut) == 8)
+        if (gold_cols_tma_ok(a)) return launch_gold_cols_tma(f, a, st);
     auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
