@@ -27,8 +27,20 @@ namespace mm {
 namespace gcols {
 
 constexpr int LOGL = 11, L = 1 << LOGL, C = 4;
-typedef typename ColsTile<FpG, LOGL>::Lay Lay;          // RowLayoutG<u64, 11, 4>
-static_assert(Lay::C == C, "four columns per tile");
+// RowLayoutG with a column pitch of 4 mod 16 words (8-byte bank pairs): stage
+// A's stores (lanes = 4 columns x 4 rows per half-warp) and the step-2 loop's
+// loads (8 rows x columns {c, c + 2}) hit 16 distinct bank pairs; stages B-D
+// (lanes along one column, stride 1 or 65 words) are unaffected
+struct Lay : RowLayoutG<uint64_t, LOGL, C> {
+    static constexpr int SROW = [] {
+        int s = L + (L >> 6);
+        while ((s & 15) != 4) s++;
+        return s;
+    }();
+    static constexpr int ELEMS = C * SROW;
+    __device__ __forceinline__ static int addr(int c, int j) { return c * SROW + j + (j >> 6); }
+    __device__ __forceinline__ static int chunk_base(int c, int base) { return c * SROW + base + (base >> 6); }
+};
 constexpr int BOXR = 256, NBOX = L / BOXR;             // box {4, 256, 8}: the whole tile
 constexpr unsigned TILE_BYTES = L * C * 8;               // 64 KiB
 constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + (size_t)Lay::ELEMS * 8 + 16;
