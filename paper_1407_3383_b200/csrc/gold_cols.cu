@@ -17,7 +17,8 @@
 //   stores -> barrier -> TMA twiddles(i+1)
 //
 // so the next tile streams in under stages B-D and the twiddles under the
-// whole transform.  Shared memory: 64 + 64 + 65 KiB, one CTA per SM.
+// whole transform.  Shared memory per CTA: two landing tiles + the padded compute tile
+// (64 + 64 + 65 KiB, one CTA per SM).
 #include <string.h>
 #include <stdlib.h>
 #include "ntt_kernels.cuh"
@@ -26,31 +27,42 @@
 namespace mm {
 namespace gcols {
 
-constexpr int LOGL = 11, L = 1 << LOGL, C = 4;
-// RowLayoutG with a column pitch of 4 mod 16 words (8-byte bank pairs): stage
-// A's stores (lanes = 4 columns x 4 rows per half-warp) and the step-2 loop's
-// loads (8 rows x columns {c, c + 2}) hit 16 distinct bank pairs; stages B-D
-// (lanes along one column, stride 1 or 65 words) are unaffected
-struct Lay : RowLayoutG<uint64_t, LOGL, C> {
+constexpr int LOGL = 11, L = 1 << LOGL;
+constexpr int BOXR = 256, NBOX = L / BOXR;             // box {C, 256, 8}: the whole tile
+// RowLayoutG with a column pitch of 16 / C mod 16 words (8-byte bank pairs):
+// stage A's stores (lanes = C columns x 16 / C rows per half-warp) and the
+// step-2 loop's loads hit 16 distinct bank pairs; stages B-D (lanes along one
+// column, stride 1 or 65 words) are unaffected
+template <int C> struct LayC : RowLayoutG<uint64_t, LOGL, C> {
     static constexpr int SROW = [] {
         int s = L + (L >> 6);
-        while ((s & 15) != 4) s++;
+        while ((s & 15) != 16 / C) s++;
         return s;
     }();
     static constexpr int ELEMS = C * SROW;
     __device__ __forceinline__ static int addr(int c, int j) { return c * SROW + j + (j >> 6); }
     __device__ __forceinline__ static int chunk_base(int c, int base) { return c * SROW + base + (base >> 6); }
 };
-constexpr int BOXR = 256, NBOX = L / BOXR;             // box {4, 256, 8}: the whole tile
-constexpr unsigned TILE_BYTES = L * C * 8;               // 64 KiB
-constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + (size_t)Lay::ELEMS * 8 + 16;
+// C columns per tile: 4 (32-byte row segments, 64 KiB tiles, one 1024-thread
+// CTA per SM).  C = 2 (16-byte segments, two 512-thread CTAs per SM) measured
+// 3.34 ms against 1.34 for C4's column pass: box copies of 16-byte rows are
+// slow, so only C = 4 is launched.
+template <int C> struct TileCfg {
+    static constexpr unsigned TILE_BYTES = L * C * 8;
+    static constexpr size_t SMEM = 2 * (size_t)TILE_BYTES + (size_t)LayC<C>::ELEMS * 8 + 16;
+    static constexpr int NTH = C == 4 ? 1024 : 512;
+};
 
-template <int NTH>
-__global__ void __launch_bounds__(NTH, 1) k_gcols_fwd(const __grid_constant__ CUtensorMap tmx,
-                                                       const __grid_constant__ CUtensorMap tmw, FpG f, ColArgs<FpG> a) {
+template <int C>
+__global__ void __launch_bounds__(TileCfg<C>::NTH, C == 4 ? 1 : 2) k_gcols_fwd(const __grid_constant__ CUtensorMap tmx,
+                                                              const __grid_constant__ CUtensorMap tmw, FpG f,
+                                                              ColArgs<FpG> a) {
+    typedef LayC<C> Lay;
+    constexpr int NTH = TileCfg<C>::NTH;
+    constexpr unsigned TILE_BYTES = TileCfg<C>::TILE_BYTES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    uint64_t* land = (uint64_t*)smem_raw;                 // [row][4] input tile (TMA)
-    uint64_t* twl = land + L * C;                          // [row][4] step-2 twiddles (TMA)
+    uint64_t* land = (uint64_t*)smem_raw;                 // [row][C] input tile (TMA)
+    uint64_t* twl = land + L * C;                          // [row][C] step-2 twiddles (TMA)
     uint64_t* s = twl + L * C;                             // padded compute tile [c][j]
     uint64_t* bar = s + Lay::ELEMS;                        // 0: data, 1: twiddles
     const uint64_t* full = (const uint64_t*)a.lvl + L;     // w_L^e, e < L
@@ -84,7 +96,7 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols_fwd(const __grid_constant__ CU
             // stage A (gold::dif_ln with NA = 32): radix-4 DFTs over ah of
             // j = 512 ah + 64 al + b6, then w_32^(al r); lanes: c fastest
             for (int q = threadIdx.x; q < C * 512; q += NTH) {
-                const int c = q & 3, b6 = (q >> 2) & 63, al = q >> 8;
+                const int c = q % C, b6 = (q / C) & 63, al = q / (64 * C);
                 const int j0 = 64 * al + b6;
                 uint64_t v[8];
 #pragma unroll
@@ -94,7 +106,7 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols_fwd(const __grid_constant__ CU
                 for (int t = 0; t < 4; t++) s[Lay::addr(c, j0 + 512 * t)] = v[t];
             }
         } else {
-            for (int e = threadIdx.x; e < L * C; e += NTH) s[Lay::addr(e & 3, e >> 2)] = land[e];
+            for (int e = threadIdx.x; e < L * C; e += NTH) s[Lay::addr(e % C, e / C)] = land[e];
         }
         __syncthreads();
         // the landing buffer is free: the next tile streams in under stages B-D
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols_fwd(const __grid_constant__ CU
         mbar_wait(&bar[1], it & 1);
         uint64_t* ob = (uint64_t*)a.out + b * a.out_bs + cl0;
         for (int e = threadIdx.x; e < L * C / 2; e += NTH) {
-            const int t = e >> 1, c = (e & 1) * 2;
+            const int t = e / (C / 2), c = (e % (C / 2)) * 2;
             const ulonglong2 w = *(const ulonglong2*)(twl + t * C + c);
             const uint64_t v0 = f.mulw(s[Lay::addr(c, t)], w.x);
             const uint64_t v1 = f.mulw(s[Lay::addr(c + 1, t)], w.y);
@@ -125,8 +137,8 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols_fwd(const __grid_constant__ CU
 }
 
 // 3-D view {cols, 256 rows, groups of 256 rows} of a row-major u64 matrix with
-// row stride rs words; box {4, 256, 8} = one whole tile
-static mm_status make_map(CUtensorMap* tm, const void* base, long long cols, long long rs, long long groups) {
+// row stride rs words; box {C, 256, 8} = one whole tile
+static mm_status make_map(CUtensorMap* tm, const void* base, long long cols, long long rs, long long groups, int C) {
     auto enc = tma_encoder();
     if (!enc) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled is not available");
     cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)BOXR, (cuuint64_t)groups};
@@ -140,28 +152,24 @@ static mm_status make_map(CUtensorMap* tm, const void* base, long long cols, lon
     return MM_OK;
 }
 
-static int threads_cfg() {
-    static int nt = [] {
-        const char* e = getenv("MMNTT_GOLD_TMA_NT");
-        return e && atoi(e) == 512 ? 512 : 1024;
-    }();
-    return nt;
-}
-
-template <int NTH> static mm_status launch(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {
+template <int C> static mm_status launch(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {
     CUtensorMap tmx, tmw;
     memset(&tmx, 0, sizeof(tmx));
     memset(&tmw, 0, sizeof(tmw));
-    mm_status s = make_map(&tmx, a.in, a.ncols, a.in_rs, a.nbatch * NBOX);
-    if (s == MM_OK) s = make_map(&tmw, a.fs_full, a.n1, a.n1, NBOX);
+    mm_status s = make_map(&tmx, a.in, a.ncols, a.in_rs, a.nbatch * NBOX, C);
+    if (s == MM_OK) s = make_map(&tmw, a.fs_full, a.n1, a.n1, NBOX, C);
     if (s != MM_OK) return s;
-    auto kern = k_gcols_fwd<NTH>;
+    auto kern = k_gcols_fwd<C>;
+    constexpr size_t SMEM = TileCfg<C>::SMEM;
     MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    const long long tiles = a.ncols / C * a.nbatch;
-    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TileCfg<C>::NTH, SMEM);
+    if (per_sm < 1) per_sm = 1;
+    const long long tiles = a.ncols / C * a.nbatch, cap = (long long)num_sms() * per_sm;
+    const int grid = (int)(tiles < cap ? tiles : cap);
     {
         LaunchScope ls("ntt_cols_fwd", st);
-        kern<<<grid, NTH, SMEM, st>>>(tmx, tmw, f, a);
+        kern<<<grid, TileCfg<C>::NTH, SMEM, st>>>(tmx, tmw, f, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
@@ -176,13 +184,13 @@ bool gold_cols_tma_ok(const ColArgs<FpG>& a) {
     }();
     using namespace gcols;
     return on && tma_encoder() != nullptr && a.nmod <= 1 && a.npeers == 0 && a.fs_full != nullptr &&
-           a.vec_in && a.vec_out && a.ncols % C == 0 && a.in_rs % 2 == 0 && a.n1 % 2 == 0 &&
+           a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && a.n1 % 2 == 0 &&
            a.in_bs == (long long)L * a.in_rs && a.in_len >= (long long)L * a.n1 && a.out_len >= (long long)L * a.n1 &&
            ((uintptr_t)a.fs_full & 15) == 0 && a.nbatch * NBOX < (1ll << 31) && a.n1 < (1ll << 31);
 }
 
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {
-    return gcols::threads_cfg() == 512 ? gcols::launch<512>(f, a, st) : gcols::launch<1024>(f, a, st);
+    return gcols::launch<4>(f, a, st);
 }
 
 }  // namespace mm
