@@ -333,6 +333,38 @@ mm_status mm_ntt_inv_rows(const mm_ntt_plan *plan, const void *in, void *out, si
 mm_status mm_ntt_inv_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
                           void *stream);
 
+/* ------------------------------------------------------------------------
+ * Many small problems in one launch (BASELINE C1: 16 forward + inverse
+ * transforms of 2^10 and one 512 x 512 product).  Each job is one 32-bit
+ * problem of length n = 2^k <= 2^12, run by its own CTA of a single kernel
+ * launch (the job table is the kernel parameter; nothing is uploaded):
+ *   MM_JOB_FORWARD   : out = forward transform of in (P:889 / P:893; `order`
+ *                      as mm_ntt_forward), plan = a 32-bit single-pass plan
+ *                      (log2n <= 12; its batch is ignored: one row per job).
+ *   MM_JOB_INVERSE   : out = inverse of the spectrum in (`order` = order of
+ *                      the input, n^-1 included, as mm_ntt_inverse).
+ *   MM_JOB_ROUNDTRIP : out = forward(in) in `order` (out may be NULL) and
+ *                      out2 = inverse(forward(in)) (BASELINE's
+ *                      inverse(forward(x)) = x), the spectrum kept on chip.
+ *   MM_JOB_POLY_MUL  : out[0 .. la+lb-2] = in * in2 mod p, in: la
+ *                      words, in2: lb words, la + lb - 1 <= 4096; plan NULL,
+ *                      (p, g) as mm_poly_mul (p < 2^30, g a generator).
+ * Buffers are device memory, residues < p; outputs must not alias another
+ * job's buffers (jobs run concurrently).  Asynchronous on `stream`;
+ * invalid jobs fail the whole call before anything launches (MM_E_ARG,
+ * MM_E_UNSUPPORTED_SIZE).  More than 256 jobs take several launches. */
+typedef enum { MM_JOB_FORWARD = 0, MM_JOB_INVERSE = 1, MM_JOB_ROUNDTRIP = 2, MM_JOB_POLY_MUL = 3 } mm_job_kind;
+typedef struct {
+    int kind;                  /* mm_job_kind */
+    int order;                 /* mm_order of the forward output / inverse input */
+    const mm_ntt_plan *plan;   /* transform jobs */
+    uint64_t p, g;             /* product jobs */
+    const void *in, *in2;
+    void *out, *out2;
+    size_t la, lb;             /* product jobs */
+} mm_job;
+mm_status mm_run_jobs(const mm_job *jobs, int njobs, void *stream);
+
 /* Sub-batch concurrency of the batched products (default 2): mm_poly_mul /
  * mm_poly_mul_ld with the 2^16-point kernels (C3 shape) split batches of at
  * least 128 n rows into n sub-batches on the library's own streams, forked

@@ -18,7 +18,7 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
-__all__ = ["lib", "MMError", "Mod32", "Mod64", "ModF64", "ModNum", "Dist", "NttPlan", "poly_mul", "poly_mul_tft", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "GOLDILOCKS",
+__all__ = ["lib", "MMError", "Mod32", "Mod64", "ModF64", "ModNum", "Dist", "NttPlan", "poly_mul", "poly_mul_tft", "poly_matmul", "poly_mul_host", "int_mul_u16", "int_mul_u32", "int_matmul_u32", "Jobs", "GOLDILOCKS",
            "MUL_BARRETT", "MUL_SHOUP", "MUL_MONTGOMERY", "NATURAL", "BITREV", "EXPORTS"]
 
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
@@ -99,6 +99,7 @@ EXPORTS = {
     "mm_int_mul_u16_dist": (_ST, [_P, _P, _sz, _P, _sz, _P, _P]),
     "mm_int_mul_u16_dist_layout": (_ST, [_P, _sz, _sz, ctypes.POINTER(_u64)]),
     "mm_release_cached": (_ST, []),
+    "mm_run_jobs": (_ST, [_P, _i32, _P]),
     "mm_set_product_streams": (_ST, [_i32]),
     "mm_probe_butterfly": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
     "mm_probe_issue": (_ST, [_i32, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), _P]),
@@ -185,6 +186,83 @@ def _need(t: torch.Tensor | None, numel: int, esize: int, name: str, like: torch
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return t
+
+
+class _Job(ctypes.Structure):
+    """mm_job (include/mmntt.h)."""
+    _fields_ = [("kind", ctypes.c_int), ("order", ctypes.c_int), ("plan", _P), ("p", _u64), ("g", _u64),
+                ("in_", _P), ("in2", _P), ("out", _P), ("out2", _P), ("la", _sz), ("lb", _sz)]
+
+
+class Jobs:
+    """Many small 32-bit problems in ONE launch (mm_run_jobs): transforms of
+    one row of length n <= 2^12 (a single-pass NttPlan), forward-then-inverse
+    round trips and polynomial products with la + lb - 1 <= 4096.  Add jobs,
+    then ``run()`` on the current stream; the tensors and plans stay
+    referenced until the builder is dropped or cleared."""
+    FORWARD, INVERSE, ROUNDTRIP, POLY_MUL = range(4)
+
+    def __init__(self):
+        self._jobs: list[_Job] = []
+        self._keep: list = []
+        self._dev = None
+        self._arr = None
+
+    def _add(self, job: _Job, tensors, plan=None):
+        if plan is not None:
+            self._keep.append(plan)       # the C table holds the plan handle
+        for t in tensors:
+            if t is None:
+                continue
+            if self._dev is None:
+                self._dev = t.device
+            elif t.device != self._dev:
+                raise ValueError(f"job tensor on {t.device}, expected {self._dev}")
+        self._jobs.append(job)
+        self._keep.extend(tensors)
+        self._arr = None
+        return self
+
+    def _row(self, plan: "NttPlan", t, name):
+        if plan.word_bits != 32:
+            raise ValueError("jobs take 32-bit plans")
+        return _need(t, plan.n, 4, name)
+
+    def forward(self, plan: "NttPlan", x, out, order=BITREV):
+        self._row(plan, x, "x"), self._row(plan, out, "out")
+        return self._add(_Job(self.FORWARD, order, plan._h, 0, 0, _ptr(x), None, _ptr(out), None, 0, 0), (x, out), plan)
+
+    def inverse(self, plan: "NttPlan", x, out, order=BITREV):
+        self._row(plan, x, "x"), self._row(plan, out, "out")
+        return self._add(_Job(self.INVERSE, order, plan._h, 0, 0, _ptr(x), None, _ptr(out), None, 0, 0), (x, out), plan)
+
+    def roundtrip(self, plan: "NttPlan", x, out2, out=None, order=BITREV):
+        """out = forward(x) in `order` (optional), out2 = inverse(forward(x))."""
+        self._row(plan, x, "x"), self._row(plan, out2, "out2")
+        if out is not None:
+            self._row(plan, out, "out")
+        return self._add(_Job(self.ROUNDTRIP, order, plan._h, 0, 0, _ptr(x), None, _ptr(out), _ptr(out2), 0, 0),
+                         (x, out, out2), plan)
+
+    def poly_mul(self, a, b, p: int, g: int, out):
+        la, lb = a.numel(), b.numel()
+        _need(a, la, 4, "a"), _need(b, lb, 4, "b", a), _need(out, la + lb - 1, 4, "out", a)
+        return self._add(_Job(self.POLY_MUL, 0, None, int(p), int(g), _ptr(a), _ptr(b), _ptr(out), None, la, lb),
+                         (a, b, out))
+
+    def __len__(self):
+        return len(self._jobs)
+
+    def clear(self):
+        self._jobs, self._keep, self._dev, self._arr = [], [], None, None
+
+    def run(self):
+        if not self._jobs:
+            return
+        if self._arr is None:
+            self._arr = (_Job * len(self._jobs))(*self._jobs)
+        s = ctypes.c_void_p(torch.cuda.current_stream(self._dev).cuda_stream)
+        _check(lib().mm_run_jobs(self._arr, len(self._jobs), s))
 
 
 # ------------------------------------------------------------------ modulus context

@@ -15,6 +15,7 @@
 #include "ntt_kernels.cuh"
 #include "fast32.h"
 #include "tft.h"
+#include "jobs.h"
 #include <new>
 #include <string.h>
 #include <type_traits>
@@ -3088,4 +3089,60 @@ extern "C" mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t* a, 
     it.inv2 = mkw32((p + 1) / 2, p);
     for (int j = 0; j <= P->k2 && j < 11; j++) it.inv_pow2[j] = mkw32(hpowmod((p + 1) / 2, (uint64_t)j, p), p);
     return tft::launch_col_itft(it, st);
+}
+
+// ---- many small problems in one launch (jobs.cu) ----------------------------------
+// Validates every job and resolves its plan before anything launches: a bad
+// job fails the whole call with nothing queued.
+extern "C" mm_status mm_run_jobs(const mm_job* jobs, int njobs, void* stream) {
+    if (njobs < 0 || (njobs > 0 && !jobs)) return set_err(MM_E_ARG, "null or negative job table");
+    if (njobs == 0) return MM_OK;
+    std::vector<DevJob> dj((size_t)njobs);
+    for (int i = 0; i < njobs; i++) {
+        const mm_job& J = jobs[i];
+        DevJob& d = dj[(size_t)i];
+        memset(&d, 0, sizeof(d));
+        d.kind = J.kind;
+        d.order = J.order;
+        const mm_ntt_plan* P = nullptr;
+        if (J.kind == MM_JOB_POLY_MUL) {
+            if (!J.in || !J.in2 || !J.out) return set_err(MM_E_ARG, "job %d: null product buffer", i);
+            if (J.la == 0 || J.lb == 0) return set_err(MM_E_ARG, "job %d: empty operand", i);
+            const size_t lc = J.la + J.lb - 1;
+            int k = 0;
+            while ((1ull << k) < lc) k++;
+            if (k == 0) k = 1;
+            if (k > MAX_BLOCK_LOG)
+                return set_err(MM_E_UNSUPPORTED_SIZE, "job %d: product length %zu > 2^%d", i, lc, MAX_BLOCK_LOG);
+            mm_status s = check_modulus(32, J.p, k);
+            if (s != MM_OK) return s;
+            mm_ntt_plan* Q = nullptr;
+            if ((s = cached_plan(32, J.p, k, hpowmod(J.g % J.p, (J.p - 1) >> k, J.p), &Q)) != MM_OK) return s;
+            P = Q;
+            d.sc = mkw32(P->ninv_r, P->p);   // n^-1 2^32: the REDC product's 2^-32 folded in
+            d.la = (long long)J.la;
+            d.lb = (long long)J.lb;
+            d.in2 = (const uint32_t*)J.in2;
+        } else if (J.kind == MM_JOB_FORWARD || J.kind == MM_JOB_INVERSE || J.kind == MM_JOB_ROUNDTRIP) {
+            P = J.plan;
+            if (!P) return set_err(MM_E_ARG, "job %d: null plan", i);
+            if (P->word_bits != 32 || P->k2 != 0)
+                return set_err(MM_E_UNSUPPORTED_SIZE, "job %d: jobs take 32-bit single-pass plans (log2n <= %d)", i,
+                               MAX_BLOCK_LOG);
+            if (!J.in || (J.kind != MM_JOB_ROUNDTRIP && !J.out) || (J.kind == MM_JOB_ROUNDTRIP && !J.out2))
+                return set_err(MM_E_ARG, "job %d: null buffer", i);
+            if (J.order != MM_ORDER_NATURAL && J.order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "job %d: bad order", i);
+            d.sc = mkw32(P->ninv, P->p);
+        } else {
+            return set_err(MM_E_ARG, "job %d: unknown kind %d", i, J.kind);
+        }
+        d.k = P->k;
+        d.f = make_field<Fp32>(P);
+        d.lvl_f = (const uint2*)P->lvl_f1;
+        d.lvl_i = (const uint2*)P->lvl_i1;
+        d.in = (const uint32_t*)J.in;
+        d.out = (uint32_t*)J.out;
+        d.out2 = (uint32_t*)J.out2;
+    }
+    return launch_jobs(dj.data(), njobs, (cudaStream_t)stream);
 }

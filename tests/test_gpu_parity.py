@@ -1155,3 +1155,94 @@ def test_ntt16_natural_in_place(mm, O, batch):
     assert torch.equal(z, xt)
     plan.inverse(y, order=mm.NATURAL)                                 # in place
     assert torch.equal(y, xt)
+
+
+# ------------------------------------------------------------------ mm_run_jobs (one launch)
+def test_jobs_c1_one_launch(mm, O):
+    # BASELINE C1 as ONE launch: 16 round trips of 2^10 (forward spectrum in
+    # natural order kept) and the 512 x 512 product, against the oracle
+    p, k = P30, 10
+    w = O.root_of_unity(3, k, p)
+    x = residues(config_seed(1), 1, 16 << k, p).reshape(16, 1 << k)
+    a = residues(config_seed(1), 2, 512, p)
+    b = residues(config_seed(1), 3, 512, p)
+    plan = mm.NttPlan(32, p, k, w, 16)
+    xt = dev(x)
+    y, z = torch.empty_like(xt), torch.empty_like(xt)
+    c = torch.empty(1023, dtype=torch.uint32, device=DEV)
+    jb = mm.Jobs()
+    for r in range(16):
+        jb.roundtrip(plan, xt[r], z[r], out=y[r], order=mm.NATURAL)
+    jb.poly_mul(dev(a), dev(b), p, 3, c)
+    n0 = mm.lib().mm_launch_count()
+    jb.run()
+    assert mm.lib().mm_launch_count() - n0 == 1
+    assert np.array_equal(u64(host(y)), O.ntt_rows(x, w, p))
+    assert np.array_equal(host(z), x)
+    assert np.array_equal(u64(host(c)), O.poly_mul_schoolbook(a, b, p))
+
+
+@pytest.mark.parametrize("p,g", [(P30, 3), (469762049, 3), (7681, 17)])
+def test_jobs_mixed_sizes(mm, O, p, g):
+    # every size 2^1 .. 2^12, forward and inverse in both orders, round trips,
+    # ragged products -- all in one call
+    rng = random.Random(p)
+    jb, checks = mm.Jobs(), []
+    for k in range(1, 13):
+        if (p - 1) % (1 << k):
+            continue
+        w = O.root_of_unity(g, k, p)
+        plan = mm.NttPlan(32, p, k, w, 1)
+        x = residues(rng.randrange(1 << 30), 1, 1 << k, p)
+        for order in (mm.NATURAL, mm.BITREV):
+            ref = O.ntt(u64(x), w, p)
+            ref = ref if order == mm.NATURAL else O.to_bitrev(ref)
+            yf = torch.empty(1 << k, dtype=torch.uint32, device=DEV)
+            jb.forward(plan, dev(x), yf, order=order)
+            checks.append((yf, ref))
+            yi = torch.empty_like(yf)
+            jb.inverse(plan, dev(ref.astype(np.uint32)), yi, order=order)
+            checks.append((yi, u64(x)))
+        yr = torch.empty(1 << k, dtype=torch.uint32, device=DEV)
+        jb.roundtrip(plan, dev(x), yr)
+        checks.append((yr, u64(x)))
+    for la, lb in [(1, 1), (1, 9), (3, 2), (100, 29), (513, 511), (2048, 2049), (4000, 97)]:
+        if (p - 1) % (1 << max(1, (la + lb - 2).bit_length())):
+            continue
+        a = residues(rng.randrange(1 << 30), 2, la, p)
+        b = residues(rng.randrange(1 << 30), 3, lb, p)
+        c = torch.empty(la + lb - 1, dtype=torch.uint32, device=DEV)
+        jb.poly_mul(dev(a), dev(b), p, g, c)
+        checks.append((c, O.poly_mul_schoolbook(a, b, p)))
+    jb.run()
+    for t, ref in checks:
+        assert np.array_equal(u64(host(t)), ref)
+
+
+def test_jobs_many_and_errors(mm, O):
+    # 600 jobs: a 256-job launch, another, then an 88-job one
+    p, k = P30, 6
+    w = O.root_of_unity(3, k, p)
+    plan = mm.NttPlan(32, p, k, w, 1)
+    x = residues(config_seed(1), 9, 600 << k, p).reshape(600, 1 << k)
+    xt = dev(x)
+    y = torch.empty_like(xt)
+    jb = mm.Jobs()
+    for r in range(600):
+        jb.forward(plan, xt[r], y[r], order=mm.BITREV)
+    n0 = mm.lib().mm_launch_count()
+    jb.run()
+    assert mm.lib().mm_launch_count() - n0 == 3
+    yh = u64(host(y))
+    for r in range(0, 600, 37):
+        assert np.array_equal(yh[r], O.to_bitrev(O.ntt(u64(x[r]), w, p)))
+    # a job outside the scope fails the whole call before anything launches
+    big = mm.NttPlan(32, p, 14, O.root_of_unity(3, 14, p), 1)
+    xb = torch.zeros(1 << 14, dtype=torch.uint32, device=DEV)
+    bad = mm.Jobs().forward(plan, xt[0], y[0]).forward(big, xb, torch.empty_like(xb))
+    n0 = mm.lib().mm_launch_count()
+    with pytest.raises(mm.MMError):
+        bad.run()
+    assert mm.lib().mm_launch_count() == n0
+    with pytest.raises(mm.MMError):
+        mm.Jobs().poly_mul(dev(x[0]), dev(x[1]), 1000003, 2, torch.empty(127, dtype=torch.uint32, device=DEV)).run()
