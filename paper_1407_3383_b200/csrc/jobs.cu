@@ -31,12 +31,17 @@ template <int LOGL> __device__ __forceinline__ void run_job(const DevJob& j, uin
     auto vec = [](const void* p) { return L >= 4 && ((uintptr_t)p & 15) == 0; };
     const bool nat = j.order == MM_ORDER_NATURAL;
     if (j.kind == MM_JOB_POLY_MUL) {
+        // a and b as the two rows of one tile: both forward transforms run in
+        // the same passes (a small transform leaves most threads idle)
+        typedef RowLayout<uint32_t, LOGL, 2> Lay2;
+        static_assert(Lay2::SROW == Lay::SROW, "row pitch independent of the row count");
         const long long lc = j.la + j.lb - 1;
+        sb = sa + Lay::SROW;
         load_rows<Fp32, Lay, LOGL, uint32_t, JNT>(sa, j.in, 0, 1, L, j.la, vec(j.in), false);
+        if (Lay::C > 1) __syncthreads();   // n = 2: a's load zero-fills the empty second row
         load_rows<Fp32, Lay, LOGL, uint32_t, JNT>(sb, j.in2, 0, 1, L, j.lb, vec(j.in2), false);
         __syncthreads();
-        run_tile<Fp32, Lay, LOGL, false, JNT>(f, sa, j.lvl_f, j.lvl_f);
-        run_tile<Fp32, Lay, LOGL, false, JNT>(f, sb, j.lvl_f, j.lvl_f);
+        run_tile<Fp32, Lay2, LOGL, false, JNT>(f, sa, j.lvl_f, j.lvl_f);
         constexpr int R = L < 16 ? L : 16;
         for (int ch = threadIdx.x; ch < L / R; ch += JNT) {
             const int base = Lay::chunk_base(0, ch * R);
