@@ -175,6 +175,122 @@ template <int C> static mm_status launch(const FpG& f, const ColArgs<FpG>& a, cu
     return MM_OK;
 }
 
+
+// ---------------------------------------------------------------- 16-bit limbs (C5)
+// The forward column pass of a zero-padded 16-bit limb vector (C5: 2^25 =
+// 2^12 columns x 2^13 rows, limbs in rows t < R <= 2^11).  A tile holds four
+// 2^12-point columns (130 KiB, one 1024-thread CTA per SM; its 32-byte output
+// row segments are whole sectors -- two-column tiles processed one after the
+// other by the same CTA wrote half sectors twice as many bytes to DRAM),
+// whose rows are 8 bytes of limbs: one TMA box {8 columns, 256 rows} per 256
+// rows lands the limbs of TWO tiles at once ([R][8] x 2 B = 32 KiB), the CTA
+// transforms them one after the other and the next super-tile's limbs stream
+// in under the last tile's stages B-D.  The step-2 twiddle is formed on chip
+// from per-column bases T_lo, T_hi (k_cols' OTF path, C5: faster than the
+// table loads); T_hi is stored at bit-reversed positions so that the store
+// loop's lanes read consecutive words.
+namespace g16 {
+constexpr int LOGL = 12, L = 1 << LOGL, C = 4, SUPER = 8, NSUB = SUPER / C, RMAX = L / 2;
+constexpr int LO = LOGL / 2, NLO = 1 << LO, NHI = 1 << (LOGL - LO), NOTF = NLO + NHI;
+constexpr int NTH = 1024, BOXR = 256;
+struct Lay : RowLayoutG<uint64_t, LOGL, C> {
+    static constexpr int SROW = [] {
+        int s = L + (L >> 6);
+        while ((s & 15) != 16 / C) s++;     // stage A's stores: 4 columns x 4 rows per half-warp
+        return s;
+    }();
+    static constexpr int ELEMS = C * SROW;
+    __device__ __forceinline__ static int addr(int c, int j) { return c * SROW + j + (j >> 6); }
+    __device__ __forceinline__ static int chunk_base(int c, int base) { return c * SROW + base + (base >> 6); }
+};
+constexpr unsigned LAND_BYTES = RMAX * SUPER * 2;                 // 32 KiB
+constexpr size_t SMEM = LAND_BYTES + (size_t)Lay::ELEMS * 8 + (size_t)C * NOTF * 8 + 16;
+
+__global__ void __launch_bounds__(NTH, 1) k_gcols16_fwd(const __grid_constant__ CUtensorMap tmx, FpG f,
+                                                       ColArgs<FpG> a, int nrows) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint16_t* land = (uint16_t*)smem_raw;                 // [row][8] limbs (TMA)
+    uint64_t* s = (uint64_t*)(smem_raw + LAND_BYTES);      // padded compute tile [c][j]
+    uint64_t* otf = s + Lay::ELEMS;                        // [c][T_lo | T_hi]
+    uint64_t* bar = otf + C * NOTF;
+    const uint64_t* full = (const uint64_t*)a.lvl + L;
+    const bool fast = __ldg(full + (L >> 6)) == gold::Pow2Val<gold::S_FWD>::v;
+    const uint64_t* fsf = a.fs_full;
+    const long long nsuper = a.ncols / SUPER;
+    const unsigned ors = (unsigned)a.out_rs, n1 = (unsigned)a.n1;
+    const int nbox = (nrows + BOXR - 1) / BOXR;
+    const unsigned bytes = (unsigned)nbox * BOXR * SUPER * 2;
+    auto issue = [&](long long st) {
+        mbar_arrive_tx(&bar[0], bytes);
+        for (int i = 0; i < nbox; i++)
+            tma_load_box2(land + i * BOXR * SUPER, &tmx, (int)(st * SUPER), i * BOXR, &bar[0]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < nsuper) issue(blockIdx.x);
+    }
+    __syncthreads();
+    int it = 0;
+    for (long long st = blockIdx.x; st < nsuper; st += gridDim.x, it++) {
+        mbar_wait(&bar[0], it & 1);
+        for (int sub = 0; sub < NSUB; sub++) {
+            const long long cl0 = st * SUPER + sub * C;
+            const long long lin0 = a.col0 + cl0;
+            // this tile's step-2 bases (in flight with stage A)
+            uint64_t otf_v = 0;
+            int otf_slot = 0;
+            if (threadIdx.x < C * NOTF) {
+                const int c = threadIdx.x / NOTF, r = threadIdx.x % NOTF;
+                const int row = r < NLO ? r : (r - NLO) << LO;
+                otf_v = __ldg(fsf + (unsigned)brev(row, LOGL) * n1 + (unsigned)lin0 + c);
+                otf_slot = c * NOTF + (r < NLO ? r : NLO + brev(r - NLO, LOGL - LO));
+            }
+            if (fast) {
+                // stage A (NA = 64): 8-point DFTs over ah of j = 512 ah + 64 al + b6,
+                // rows >= nrows zero; lanes: c fastest
+                for (int q = threadIdx.x; q < C * 512; q += NTH) {
+                    const int c = q % C, b6 = (q / C) & 63, al = q / (64 * C);
+                    const int j0 = 64 * al + b6;
+                    uint64_t v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; t++) {
+                        const int row = j0 + 512 * t;
+                        v[t] = (t < RMAX / 512 && row < nrows) ? land[row * SUPER + sub * C + c] : 0ull;
+                    }
+                    gold::dif_a<8, gold::S_FWD>(v, al);
+#pragma unroll
+                    for (int t = 0; t < 8; t++) s[Lay::addr(c, j0 + 512 * t)] = v[t];
+                }
+            } else {
+                for (int e = threadIdx.x; e < L * C; e += NTH) {
+                    const int row = e / C, c = e % C;
+                    s[Lay::addr(c, row)] = row < nrows ? land[row * SUPER + sub * C + c] : 0ull;
+                }
+            }
+            if (threadIdx.x < C * NOTF) otf[otf_slot] = otf_v;
+            __syncthreads();
+            // the last tile of the super-tile has read its limbs: the next super-tile streams in
+            if (sub == NSUB - 1 && threadIdx.x == 0 && st + gridDim.x < nsuper) issue(st + gridDim.x);
+            if (fast) gold::dif_ln_bcd<Lay, L, 1, NTH, gold::S_FWD>(s, full, 1, L / 64);
+            else run_tile<FpG, Lay, LOGL, false, NTH>(f, s, a.lvl, a.lvl);
+            uint64_t* ob = (uint64_t*)a.out + cl0;
+            // w^(j1 k), k = [t]: T_lo[k mod 2^LO] (warp-uniform) T_hi[k >> LO]
+            // (stored at [t mod 2^LO]); lanes: 2 per row, 32-byte row segments
+            for (int e = threadIdx.x; e < L * C / 2; e += NTH) {
+                const int t = e / (C / 2), c = (e % (C / 2)) * 2;
+                const unsigned lo = (unsigned)brev(t, LOGL) & (NLO - 1), hi = (unsigned)t & (NHI - 1);
+                const uint64_t w0 = FpG::mul(otf[c * NOTF + lo], otf[c * NOTF + NLO + hi]);
+                const uint64_t w1 = FpG::mul(otf[(c + 1) * NOTF + lo], otf[(c + 1) * NOTF + NLO + hi]);
+                const uint64_t v0 = f.mulw(s[Lay::addr(c, t)], w0);
+                const uint64_t v1 = f.mulw(s[Lay::addr(c + 1, t)], w1);
+                *(ulonglong2*)(ob + (unsigned)t * ors + c) = make_ulonglong2(v0, v1);
+            }
+            __syncthreads();
+        }
+    }
+}
+}  // namespace g16
 }  // namespace gcols
 
 bool gold_cols_tma_ok(const ColArgs<FpG>& a) {
@@ -187,6 +303,50 @@ bool gold_cols_tma_ok(const ColArgs<FpG>& a) {
            a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && a.n1 % 2 == 0 &&
            a.in_bs == (long long)L * a.in_rs && a.in_len >= (long long)L * a.n1 && a.out_len >= (long long)L * a.n1 &&
            ((uintptr_t)a.fs_full & 15) == 0 && a.nbatch * NBOX < (1ll << 31) && a.n1 < (1ll << 31);
+}
+
+bool gold_cols16_tma_ok(const ColArgs<FpG>& a) {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    using namespace gcols::g16;
+    // limbs in whole rows t < in_len / n1 <= 2^11 (every column of the block
+    // valid exactly up to that row), one batch row, 16-byte aligned rows
+    return on && tma_encoder() != nullptr && a.nbatch == 1 && a.nmod <= 1 && a.npeers == 0 && a.fs_full != nullptr &&
+           a.vec_out && a.ncols % SUPER == 0 && a.in_rs == a.n1 && a.n1 % 8 == 0 && a.in_len % a.n1 == 0 &&
+           a.in_len / a.n1 <= RMAX && a.in_len > 0 && a.out_len >= (long long)L * a.n1 && ((uintptr_t)a.in & 15) == 0 &&
+           a.n1 < (1ll << 31);
+}
+
+mm_status launch_gold_cols16_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {
+    using namespace gcols::g16;
+    auto enc = tma_encoder();
+    if (!enc) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled is not available");
+    const int nrows = (int)(a.in_len / a.n1);
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    cuuint64_t dims[2] = {(cuuint64_t)a.ncols, (cuuint64_t)nrows};
+    cuuint64_t strides[1] = {(cuuint64_t)a.in_rs * 2};
+    cuuint32_t box[2] = {(cuuint32_t)SUPER, (cuuint32_t)BOXR};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(a.in), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    auto kern = k_gcols16_fwd;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, SMEM);
+    if (per_sm < 1) per_sm = 1;
+    const long long tiles = a.ncols / SUPER, cap = (long long)num_sms() * per_sm;
+    const int grid = (int)(tiles < cap ? tiles : cap);
+    {
+        LaunchScope ls("ntt_cols_fwd", st);
+        kern<<<grid, NTH, SMEM, st>>>(tm, f, a, nrows);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
 }
 
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {

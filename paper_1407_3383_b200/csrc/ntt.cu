@@ -1274,6 +1274,8 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
         // on the interleaved generic tiles (2^19..2^21: 10-11 % faster than the
         // balanced split; 2^18, 2^22, 2^23 measured slower)
         if (word_bits == 64 && log2n >= 19 && log2n <= 21) k2 = log2n - 13;   // measured: tools/time_split.py
+        if (const char* e = getenv("MMNTT_K2_64"))   // split experiments (tools/time_g.py)
+            if (word_bits == 64 && atoi(e) >= log2n - 13 && atoi(e) <= 12 && atoi(e) < log2n) k2 = atoi(e);
         P->k2 = k2;
         P->k1 = log2n - k2;
     }

@@ -158,6 +158,9 @@ template <class F> struct ColArgs {
 // gold_cols_tma_ok (full-length input, one modulus, no peer scatter)
 bool gold_cols_tma_ok(const ColArgs<FpG>& a);
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
+// the same for 2^12-point columns of zero-padded 16-bit limbs (C5, gold_cols.cu)
+bool gold_cols16_tma_ok(const ColArgs<FpG>& a);
+mm_status launch_gold_cols16_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
 
 template <class F> struct PmulArgs {
     typedef typename F::W W;
@@ -953,6 +956,9 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     if constexpr (std::is_same<F, FpG>::value && LOGL == 11 && !INV && EPIV == EPI_FS_FULL && sizeof(TIn) == 8 &&
                   sizeof(TOut) == 8)
         if (gold_cols_tma_ok(a)) return launch_gold_cols_tma(f, a, st);
+    if constexpr (std::is_same<F, FpG>::value && LOGL == 12 && !INV && EPIV == EPI_FS_FULL && sizeof(TIn) == 2 &&
+                  sizeof(TOut) == 8)
+        if (gold_cols16_tma_ok(a)) return launch_gold_cols16_tma(f, a, st);
     auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;

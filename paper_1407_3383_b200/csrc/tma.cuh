@@ -36,6 +36,19 @@ __device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tm, 
         : "memory");
 }
 
+// arm the barrier for `bytes` of box copies issued after it (several boxes, one phase)
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// one 2-D box copy completing on a barrier armed by mbar_arrive_tx
+__device__ __forceinline__ void tma_load_box2(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"((const void*)tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 static inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
