@@ -176,6 +176,107 @@ template <int C> static mm_status launch(const FpG& f, const ColArgs<FpG>& a, cu
 }
 
 
+// ---------------------------------------------------------------- inverse columns
+// Inverse column pass (the last step of an inverse transform or product,
+// P:923) of 2^11- or 2^12-point columns, 4 columns per tile: the tile arrives
+// by box copies into a 64 KiB landing buffer -- the whole 2^11-point tile, or
+// a 2^12-point tile in two halves -- and is copied into the padded compute
+// tile (lanes: c fastest, conflict-free with the 4 mod 16 pitch); the next
+// tile's (first half) streams in under the whole DIT.
+template <int LOGL> struct Inv {
+    static constexpr int L = 1 << LOGL, C = 4, HALVES = LOGL == 12 ? 2 : 1, LR = L / HALVES;
+    static constexpr unsigned LAND_BYTES = LR * C * 8;       // 64 KiB
+    struct Lay : RowLayoutG<uint64_t, LOGL, C> {
+        static constexpr int SROW = [] {
+            int s = L + (L >> 6);
+            while ((s & 15) != 4) s++;
+            return s;
+        }();
+        static constexpr int ELEMS = C * SROW;
+        __device__ __forceinline__ static int addr(int c, int j) { return c * SROW + j + (j >> 6); }
+        __device__ __forceinline__ static int chunk_base(int c, int base) { return c * SROW + base + (base >> 6); }
+    };
+    static constexpr size_t SMEM = LAND_BYTES + (size_t)Lay::ELEMS * 8 + 16;
+};
+
+template <int LOGL, int EPIV>
+__global__ void __launch_bounds__(1024, 1) k_gcols_inv(const __grid_constant__ CUtensorMap tmx, FpG f,
+                                                       ColArgs<FpG> a) {
+    typedef Inv<LOGL> K;
+    typedef typename K::Lay Lay;
+    typedef Epi<FpG, EPIV> E;
+    constexpr int NTH = 1024, C = K::C, L = K::L, LR = K::LR, HALVES = K::HALVES, GPH = LR / BOXR;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* land = (uint64_t*)smem_raw;
+    uint64_t* s = land + LR * C;
+    uint64_t* bar = s + Lay::ELEMS;
+    const long long ntiles = a.ncols / C * a.nbatch;
+    const unsigned ors = (unsigned)a.out_rs;
+    auto coords = [&](long long tile, long long& b, long long& cl0) {
+        b = tile % a.nbatch;
+        cl0 = tile / a.nbatch * C;
+    };
+    auto issue = [&](long long tile, int h) {
+        long long b, cl0;
+        coords(tile, b, cl0);
+        tma_load_tile(land, &tmx, (int)cl0, 0, (int)(b * (L / BOXR) + h * GPH), &bar[0], K::LAND_BYTES);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    }
+    __syncthreads();
+    unsigned ph = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        long long b, cl0;
+        coords(tile, b, cl0);
+        const long long nxt = tile + gridDim.x;
+        for (int h = 0; h < HALVES; h++) {
+            mbar_wait(&bar[0], ph & 1);
+            ph++;
+            for (int e = threadIdx.x; e < LR * C; e += NTH) s[Lay::addr(e % C, h * LR + e / C)] = land[e];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (h + 1 < HALVES) issue(tile, h + 1);
+                else if (nxt < ntiles) issue(nxt, 0);
+            }
+        }
+        run_tile<FpG, Lay, LOGL, true, NTH>(f, s, a.lvl, a.lvl);
+        // canonical (and n^-1 for a standalone inverse), truncated to out_len
+        const long long lin0 = a.col0 + cl0;
+        uint64_t* ob = (uint64_t*)a.out + b * a.out_bs + cl0;
+        for (int e = threadIdx.x; e < L * C / 2; e += NTH) {
+            const int t = e >> 1, c = (e & 1) * 2;
+            const long long lin = (long long)t * a.n1 + lin0 + c;
+            if (lin >= a.out_len) continue;
+            const uint64_t v0 = E::apply(f, s[Lay::addr(c, t)], 0, nullptr, nullptr, 0, 0u, a.sc);
+            const uint64_t v1 = E::apply(f, s[Lay::addr(c + 1, t)], 0, nullptr, nullptr, 0, 0u, a.sc);
+            if (lin + 1 < a.out_len) *(ulonglong2*)(ob + (unsigned)t * ors + c) = make_ulonglong2(v0, v1);
+            else ob[(unsigned)t * ors + c] = v0;
+        }
+        __syncthreads();
+    }
+}
+
+template <int LOGL, int EPIV> static mm_status launch_inv(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {
+    typedef Inv<LOGL> K;
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    mm_status s = make_map(&tm, a.in, a.ncols, a.in_rs, a.nbatch * (K::L / BOXR), K::C);
+    if (s != MM_OK) return s;
+    auto kern = k_gcols_inv<LOGL, EPIV>;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
+    const long long tiles = a.ncols / K::C * a.nbatch;
+    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    {
+        LaunchScope ls("ntt_cols_inv", st);
+        kern<<<grid, 1024, K::SMEM, st>>>(tm, f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
 // ---------------------------------------------------------------- 16-bit limbs (C5)
 // The forward column pass of a zero-padded 16-bit limb vector (C5: 2^25 =
 // 2^12 columns x 2^13 rows, limbs in rows t < R <= 2^11).  A tile holds four
@@ -347,6 +448,26 @@ mm_status launch_gold_cols16_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream
     }
     MM_LAUNCH_CHECK();
     return MM_OK;
+}
+
+bool gold_cols_inv_tma_ok(const ColArgs<FpG>& a, int logl) {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    const long long L = 1ll << logl;
+    return on && (logl == 11 || logl == 12) && tma_encoder() != nullptr && a.nmod <= 1 && a.npeers == 0 &&
+           a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && a.in_bs == L * a.in_rs &&
+           a.in_len >= L * a.n1 && a.nbatch * (L / 256) < (1ll << 31) && a.n1 < (1ll << 31);
+}
+
+mm_status launch_gold_cols_inv_tma(const FpG& f, const ColArgs<FpG>& a, int logl, int epiv, cudaStream_t st) {
+    using namespace gcols;
+    if (logl == 11 && epiv == EPI_CANON) return launch_inv<11, EPI_CANON>(f, a, st);
+    if (logl == 11 && epiv == (EPI_SCALE | EPI_CANON)) return launch_inv<11, EPI_SCALE | EPI_CANON>(f, a, st);
+    if (logl == 12 && epiv == EPI_CANON) return launch_inv<12, EPI_CANON>(f, a, st);
+    if (logl == 12 && epiv == (EPI_SCALE | EPI_CANON)) return launch_inv<12, EPI_SCALE | EPI_CANON>(f, a, st);
+    return set_err(MM_E_ARG, "no TMA inverse column kernel for 2^%d points, epilogue %d", logl, epiv);
 }
 
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st) {

@@ -160,6 +160,9 @@ bool gold_cols_tma_ok(const ColArgs<FpG>& a);
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
 // the same for 2^12-point columns of zero-padded 16-bit limbs (C5, gold_cols.cu)
 bool gold_cols16_tma_ok(const ColArgs<FpG>& a);
+// inverse Goldilocks column passes of 2^11 / 2^12 points with TMA-staged tiles (gold_cols.cu)
+bool gold_cols_inv_tma_ok(const ColArgs<FpG>& a, int logl);
+mm_status launch_gold_cols_inv_tma(const FpG& f, const ColArgs<FpG>& a, int logl, int epiv, cudaStream_t st);
 mm_status launch_gold_cols16_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
 
 template <class F> struct PmulArgs {
@@ -959,6 +962,9 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     if constexpr (std::is_same<F, FpG>::value && LOGL == 12 && !INV && EPIV == EPI_FS_FULL && sizeof(TIn) == 2 &&
                   sizeof(TOut) == 8)
         if (gold_cols16_tma_ok(a)) return launch_gold_cols16_tma(f, a, st);
+    if constexpr (std::is_same<F, FpG>::value && (LOGL == 11 || LOGL == 12) && INV &&
+                  (EPIV == EPI_CANON || EPIV == (EPI_SCALE | EPI_CANON)) && sizeof(TIn) == 8 && sizeof(TOut) == 8)
+        if (gold_cols_inv_tma_ok(a, LOGL)) return launch_gold_cols_inv_tma(f, a, LOGL, EPIV, st);
     auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;

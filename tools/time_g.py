@@ -54,6 +54,7 @@ mm.set_product_streams(1)
 out["C4_fwd_ms_one_stream"] = round(tloop(f), 4)
 mm.set_product_streams(2)
 out["C4_fwd_kernels"] = kern(f)
+out["C4_inv_kernels"] = kern(g)
 out["C4_roundtrip_ok"] = bool(torch.equal(z, x))
 del x, y, z, plan
 n = 1 << 24
