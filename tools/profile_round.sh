@@ -17,18 +17,18 @@ ncu --set full --clock-control none --import-source on -k "regex:k_col|k_row" -s
     -o gpurun_out/${R}_full_c3 python tools/prof_run.py c3 > gpurun_out/${R}_ncu_full_c3.log 2>&1
 echo full_c3_rc=$?
 python tools/prof_run.py c4 > gpurun_out/${R}_plain_c4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_cols|k_rows" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_cols|k_rows" -s 2 -c 2 \
     -o gpurun_out/${R}_full_c4 python tools/prof_run.py c4 > gpurun_out/${R}_ncu_full_c4.log 2>&1
 echo full_c4_rc=$?
 python tools/prof_run.py c5 > gpurun_out/${R}_plain_c5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_cols|k_rows|k_carry" -s 5 -c 5 \
+ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_cols|k_rows|k_carry" -s 5 -c 5 \
     -o gpurun_out/${R}_full_c5 python tools/prof_run.py c5 > gpurun_out/${R}_ncu_full_c5.log 2>&1
 echo full_c5_rc=$?
 python tools/ncu_summary.py launches gpurun_out/${R}_launches.csv gpurun_out/${R}_launches_summary.txt > /dev/null
 python tools/ncu_summary.py full gpurun_out/${R}_full_c5.ncu-rep gpurun_out/${R}_full_c5_summary.txt gpurun_out/${R}_traffic_c5.json > /dev/null
-ncu -i gpurun_out/${R}_full_c4.ncu-rep --page source --csv --print-source sass -k "regex:k_cols" --launch-count 1 \
+ncu -i gpurun_out/${R}_full_c4.ncu-rep --page source --csv --print-source sass -k "regex:k_gcols" --launch-count 1 \
     > gpurun_out/${R}_sass_k_cols_c4.csv 2>/dev/null
-ncu -i gpurun_out/${R}_full_c4.ncu-rep --page source --csv --print-source cuda -k "regex:k_cols" --launch-count 1 \
+ncu -i gpurun_out/${R}_full_c4.ncu-rep --page source --csv --print-source cuda -k "regex:k_gcols" --launch-count 1 \
     > gpurun_out/${R}_src_k_cols_c4.csv 2>/dev/null
 python tools/ncu_summary.py full gpurun_out/${R}_full_c3.ncu-rep gpurun_out/${R}_full_c3_summary.txt gpurun_out/${R}_traffic_c3.json > /dev/null
 python tools/ncu_summary.py full gpurun_out/${R}_full_c4.ncu-rep gpurun_out/${R}_full_c4_summary.txt gpurun_out/${R}_traffic_c4.json > /dev/null
