@@ -814,26 +814,27 @@ __global__ void __launch_bounds__(NTr<F, LOGL>::v, NTr<F, LOGL>::v == 512 ? 2 : 
         T* scr = (T*)a.scratch + (size_t)blockIdx.x * L;
         for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const long long r0 = tile;
-            load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.a, r0, a.nrows, a.a_rs, a.la, a.vec_in, false,
-                                         a.in_seg_log, a.in_seg_stride);
-            __syncthreads();
-            run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
-            for (int j = 2 * threadIdx.x; j < L; j += 2 * NTH) {
-                const int ix = Lay::addr(0, j);            // j even: j, j + 1 share a 64-block
-                *(ulonglong2*)(scr + j) = make_ulonglong2(sa[ix], sa[ix + 1]);
+            // both operands through ONE copy of the forward tile code (a loop,
+            // not two inlined calls: the 2^13-point tile is large enough that
+            // two copies plus the inverse missed in the instruction cache)
+#pragma unroll 1
+            for (int op = 0; op < 2; op++) {
+                load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)(op ? a.b : a.a), r0, a.nrows, op ? a.b_rs : a.a_rs,
+                                             op ? a.lb : a.la, a.vec_in, false, a.in_seg_log, a.in_seg_stride);
+                __syncthreads();
+                run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
+                for (int j = 2 * threadIdx.x; j < L; j += 2 * NTH) {
+                    const int ix = Lay::addr(0, j);            // j even: j, j + 1 share a 64-block
+                    if (op == 0) {
+                        *(ulonglong2*)(scr + j) = make_ulonglong2(sa[ix], sa[ix + 1]);
+                    } else {
+                        const ulonglong2 u = *(const ulonglong2*)(scr + j);
+                        sa[ix] = f.mulw(f.mul_redc((T)u.x, sa[ix]), a.sc);
+                        sa[ix + 1] = f.mulw(f.mul_redc((T)u.y, sa[ix + 1]), a.sc);
+                    }
+                }
+                __syncthreads();
             }
-            __syncthreads();
-            load_rows<F, Lay, LOGL, TIn, NTH>(sa, (const TIn*)a.b, r0, a.nrows, a.b_rs, a.lb, a.vec_in, false,
-                                         a.in_seg_log, a.in_seg_stride);
-            __syncthreads();
-            run_tile<F, Lay, LOGL, false, NTH>(f, sa, twf, a.lvl_f);
-            for (int j = 2 * threadIdx.x; j < L; j += 2 * NTH) {
-                const int ix = Lay::addr(0, j);
-                const ulonglong2 u = *(const ulonglong2*)(scr + j);
-                sa[ix] = f.mulw(f.mul_redc((T)u.x, sa[ix]), a.sc);
-                sa[ix + 1] = f.mulw(f.mul_redc((T)u.y, sa[ix + 1]), a.sc);
-            }
-            __syncthreads();
             run_tile<F, Lay, LOGL, true, NTH>(f, sa, twi, a.lvl_i);
             store_rows<F, Lay, LOGL, TOut, EPIV, NTH>(f, sa, (TOut*)a.c, r0, a.nrows, a.c_rs, a.lc, a.vec_out, false,
                                                  a.fs_full, a.fs_lo, a.fs_hi, a.fs_h, a.row0, a.k2, a.sc,
