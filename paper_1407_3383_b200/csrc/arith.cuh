@@ -115,6 +115,7 @@ struct Fp32 {
     typedef uint32_t T;
     typedef uint2 W;         // twiddle (w, floor(w 2^32 / p))
     uint32_t p, p2, pinv;    // pinv = p^-1 mod 2^32 (Montgomery, pointwise)
+    uint32_t pr = 0;         // floor(2^32 / p): raw 32-bit words reduced on load (reduce_raw)
     // x w mod p in [0, 2p) for any x < 2^32 (Function 8, lazy).
     __device__ __forceinline__ uint32_t mulw(uint32_t x, W w) const {
         uint32_t c = __umulhi(x, w.y);
@@ -149,6 +150,10 @@ struct Fp32 {
         x = xx + yy;
         y = xx - yy + p2;
     }
+    // any x < 2^32 -> [0, 2p), congruent (the lazy range of the butterflies):
+    // q = hi(x floor(2^32/p)) is floor(x/p) or one less (Function 8's argument
+    // with the multiplier 1), so x - q p < 2p
+    __device__ __forceinline__ uint32_t reduce_raw(uint32_t x) const { return x - __umulhi(x, pr) * p; }
     // [0, 4p) -> [0, p)
     __device__ __forceinline__ uint32_t canon(uint32_t x) const {
         x = umin32(x, x - p2);

@@ -1068,6 +1068,7 @@ template <> Fp32 make_field<Fp32>(const mm_ntt_plan* P) {
     f.p = (uint32_t)P->p;
     f.p2 = 2 * (uint32_t)P->p;
     f.pinv = P->pinv;
+    f.pr = (uint32_t)((1ull << 32) / P->p);
     return f;
 }
 template <> FpG make_field<FpG>(const mm_ntt_plan*) { return FpG(); }
@@ -2070,12 +2071,27 @@ static mm_status product_impl(mm_ntt_plan* P, const TIn* a, long long la, const 
 // p_q's field constants and tables selected per tile.  R = residues [3][rs]
 // (a at offset 0, b at offset na), Cp = products [3][lc]; the three plans
 // share k (hence the split and the table geometry).
-static mm_status product3_impl(mm_ntt_plan* const PL[3], const uint32_t* R, long long rs, long long na, long long nb,
-                               uint32_t* Cp, long long lc, cudaStream_t st) {
+static mm_status product3_impl(mm_ntt_plan* const PL[3], const uint32_t* A, const uint32_t* B, const Crt3& K,
+                               uint32_t* R, long long rs, long long na, long long nb, uint32_t* Cp, long long lc,
+                               cudaStream_t st) {
     typedef uint2 W;
     mm_ntt_plan* P = PL[0];
     Fp32 f = make_field<Fp32>(P);
+    const int rgrid = num_sms() * 8;
+    // residues of operand op modulo the three primes -> R (a at 0, b at na)
+    auto residues = [&](int op, cudaStream_t cs) -> mm_status {
+        {
+            LaunchScope ls("crt_residues", cs);
+            k_residues3<<<rgrid, 256, 0, cs>>>(op ? B : A, op ? nb : na, R + (op ? na : 0), rs, K);
+        }
+        MM_LAUNCH_CHECK();
+        return MM_OK;
+    };
     if (P->k2 == 0) {
+        for (int op = 0; op < 2; op++) {
+            mm_status s = residues(op, st);
+            if (s != MM_OK) return s;
+        }
         // one-pass products: a product tile holds several rows, which would mix
         // moduli -- one launch per prime (these sizes are launch-latency bound)
         for (int q = 0; q < 3; q++) {
@@ -2091,14 +2107,31 @@ static mm_status product3_impl(mm_ntt_plan* const PL[3], const uint32_t* R, long
     if (s != MM_OK) return s;
     uint32_t* WA = (uint32_t*)ws;
     uint32_t* WB = WA + 3 * n;
+    // a's and b's forward column passes on the two fork streams: at Table-16
+    // sizes each launch is a wave or two, so the two overlap
+    const bool fork2 = product_streams() > 1;
+    Fork* FK = nullptr;
+    std::unique_lock<std::mutex> flk;
+    if (fork2) {
+        if ((s = fork_streams(&FK)) != MM_OK) return s;
+        flk = std::unique_lock<std::mutex>(FK->mu);
+        MM_CUDA_TRY(cudaEventRecord(FK->fork, st));
+    }
     for (int op = 0; op < 2; op++) {
+        cudaStream_t cs = st;
+        if (fork2) {
+            cs = FK->s[op];
+            MM_CUDA_TRY(cudaStreamWaitEvent(cs, FK->fork, 0));
+        }
         ColArgs<Fp32> cc{};
-        cc.in = op == 0 ? R : R + na;
+        // the raw 32-bit limbs, reduced modulo p_q by the loader of batch row q
+        cc.in = op == 0 ? (const void*)A : (const void*)B;
+        cc.reduce_in = 1;
         cc.out = op == 0 ? WA : WB;
         cc.ncols = n1;
         cc.nbatch = 3;
         cc.in_rs = n1; cc.out_rs = n1;
-        cc.in_bs = rs; cc.out_bs = n;
+        cc.in_bs = 0; cc.out_bs = n;
         cc.in_len = op == 0 ? na : nb; cc.out_len = n;
         cc.n1 = n1;
         cc.k = P->k2;
@@ -2117,8 +2150,13 @@ static mm_status product3_impl(mm_ntt_plan* const PL[3], const uint32_t* R, long
             cc.fshim[q] = (const W*)PL[q]->fs_hi_f;
             cc.fsfullm[q] = (const W*)PL[q]->fs_full_f;
         }
-        if ((s = launch_cols<Fp32, false, uint32_t, uint32_t>(f, cc, st)) != MM_OK) return s;
+        if ((s = launch_cols<Fp32, false, uint32_t, uint32_t>(f, cc, cs)) != MM_OK) return s;
+        if (fork2) {
+            MM_CUDA_TRY(cudaEventRecord(FK->join[op], cs));
+            MM_CUDA_TRY(cudaStreamWaitEvent(st, FK->join[op], 0));
+        }
     }
+    if (fork2) flk.unlock();
     PmulArgs<Fp32> m{};
     m.a = WA; m.b = WB; m.c = WA;
     m.nrows = 3ll << P->k2;
@@ -2607,20 +2645,13 @@ extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t
     uint32_t* Cp = R + 3 * rs;            // Cp[i * lc + k]: c_k mod p_i
     uint32_t* Wd = Cp + 3 * lc;           // 96-bit coefficients
     uint32_t* agg = Wd + 3 * lc;
-    const int grid = num_sms() * 8;
-    {
-        LaunchScope ls("crt_residues", st);
-        k_residues3<<<grid, 256, 0, st>>>(a, (long long)na, R, (long long)rs, K);
-        k_residues3<<<grid, 256, 0, st>>>(b, (long long)nb, R + na, (long long)rs, K);
-    }
-    MM_LAUNCH_CHECK();
     mm_ntt_plan* PL[3];
     for (int i = 0; i < 3; i++) {
         uint64_t omega = hpowmod(GEN[i], (PR[i] - 1) >> k, PR[i]);
         if ((s = cached_plan(32, PR[i], k, omega, &PL[i])) != MM_OK) return s;
     }
     // the three products modulo p1, p2, p3 in one launch per pass (Remark 6)
-    if ((s = product3_impl(PL, R, (long long)rs, (long long)na, (long long)nb, Cp, (long long)lc, st)) != MM_OK)
+    if ((s = product3_impl(PL, a, b, K, R, (long long)rs, (long long)na, (long long)nb, Cp, (long long)lc, st)) != MM_OK)
         return s;
     // Garner CRT and carries in one pass (crt_carry32); Wd is its look-back scratch
     (void)agg;

@@ -131,6 +131,7 @@ template <class F> struct ColArgs {
     void* out;
     long long ncols, nbatch, in_rs, out_rs, in_bs, out_bs, in_len, out_len, col0, n1;
     int k, fs, scale, canon, vec_in, vec_out;
+    int reduce_in;        // 32-bit fields: input words are raw (any u32), reduced on load (Fp32::reduce_raw)
     W sc;
     const W* lvl;
     const W* fs_lo;
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
     int curq = 0;
     const unsigned irs = (unsigned)a.in_rs, ors = (unsigned)a.out_rs, n1 = (unsigned)a.n1;
     constexpr bool PIPE = K::PIPE && sizeof(TIn) == sizeof(T);
-    const bool pipe = PIPE && a.vec_in;
+    const bool pipe = PIPE && a.vec_in && !a.reduce_in;   // cp.async lands words unseen: no reduction on load
     // cp.async the whole column tile `tile` into dst (zero-fill beyond in_len)
     // tiles run column-group-major (tile = cg nbatch + b): the nbatch tiles of one
     // column group are in flight together and share their step-2 table segment
@@ -662,6 +663,11 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                             v[i] = (t < tzero && (long long)t * a.n1 + lin0 + c + i < a.in_len)
                                        ? __ldg(tb + (unsigned)t * irs + c + i) : (T)0;
                     }
+                    if constexpr (std::is_same<F, Fp32>::value)
+                        if (a.reduce_in) {
+#pragma unroll
+                            for (int i = 0; i < V; i++) v[i] = ff.reduce_raw(v[i]);
+                        }
                     if (Lay::COL) {
                         *(TV*)(s + Lay::addr(c, t)) = vmake<T>(v);
                     } else {
@@ -684,6 +690,8 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
                     v[u] = 0;
                     if (e < TOTE && (t < tfull || (t < tzero && (long long)t * a.n1 + lin0 + c < a.in_len)))
                         v[u] = ld_conv<TIn, T>(inb + (unsigned)t * irs + c);
+                    if constexpr (std::is_same<F, Fp32>::value)
+                        if (a.reduce_in) v[u] = ff.reduce_raw(v[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < BE; u++) {
