@@ -321,10 +321,35 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_apply(D d, long long nout, co
 // coefficients per limb from global memory).
 constexpr int C16_SM = CARRY_B + 4 + (CARRY_B + 4) / 16 + 1;
 __device__ __forceinline__ int c16_pad(int r) { return r + (r >> 4); }
+// Coefficient pairs (16-byte loads when the window is aligned), all of a
+// thread's loads in flight before its shared stores (the one-load-at-a-time
+// loop left the carry pass latency-bound).
 __device__ __forceinline__ void c16_stage(uint64_t* sc, const uint64_t* __restrict__ c, long long nc, long long jb) {
-    for (int r = threadIdx.x; r < CARRY_B + 4; r += blockDim.x) {
-        const long long k = jb - 4 + r;
-        sc[c16_pad(r)] = (k >= 0 && k < nc) ? c[k] : 0ull;
+    constexpr int NP = (CARRY_B + 4) / 2, U = (NP + CARRY_T - 1) / CARRY_T;
+    static_assert((CARRY_B + 4) % 2 == 0, "pairs");
+    const long long k0 = jb - 4;
+    const bool vec = (((uintptr_t)(c + k0)) & 15) == 0 && k0 >= 0 && k0 + 2 * NP <= nc;
+    ulonglong2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int pr = threadIdx.x + u * CARRY_T;
+        if (pr < NP) {
+            if (vec) {
+                v[u] = __ldg((const ulonglong2*)(c + k0) + pr);
+            } else {
+                const long long k = k0 + 2 * pr;
+                v[u].x = (k >= 0 && k < nc) ? __ldg(c + k) : 0ull;
+                v[u].y = (k + 1 >= 0 && k + 1 < nc) ? __ldg(c + k + 1) : 0ull;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int pr = threadIdx.x + u * CARRY_T;
+        if (pr < NP) {
+            sc[c16_pad(2 * pr)] = v[u].x;
+            sc[c16_pad(2 * pr + 1)] = v[u].y;
+        }
     }
 }
 // w[e], g[e] for limbs j = jb + 16 t + e (see the Dig16 comment above)
