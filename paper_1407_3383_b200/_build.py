@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmmntt.so")
 SOURCES = ["common.cu", "elementwise.cu", "ntt.cu", "probe.cu", "ntt_inst32a.cu", "ntt_inst32b.cu",
-           "ntt_inst64a.cu", "ntt_inst64b.cu", "ntt_fast32.cu", "elementwise_f64.cu", "ntt_instf64.cu", "tft.cu", "numeric.cu", "elementwise64.cu", "dist.cu", "gold_cols.cu", "jobs.cu"]
+           "ntt_inst64a.cu", "ntt_inst64b.cu", "ntt_fast32.cu", "elementwise_f64.cu", "ntt_instf64.cu", "tft.cu", "numeric.cu", "elementwise64.cu", "dist.cu", "gold_cols.cu", "gold_rows.cu", "jobs.cu"]
 HEADERS = ["common.h", "arith.cuh", "ntt_core.cuh", "ntt_kernels.cuh", "gold.cuh", "fast32.h", "tft.h", "tma.cuh", "jobs.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -1,0 +1,100 @@
+// gold_rows.cu -- the Goldilocks forward row pass of 2^13-point rows (C4:
+// Algorithm 1 steps 3-4) with its rows staged by bulk copies.
+//
+// k_rows (ntt_kernels.cuh) loads a row with per-thread 16-byte loads into
+// the padded tile and then runs the radix-2 level of span 4096 as a separate
+// shared-memory pass.  Here one thread moves each 64 KiB row with ONE bulk
+// copy (cp.async.bulk, mbarrier completion) into a landing buffer, the
+// radix-2 level reads the landing buffer and writes the padded tile (that
+// pass's shared-memory round trip is gone), and the next row streams in under
+// the two 4096-point halves (gold.cuh) and the store.  Shared memory 64 + 65
+// KiB: one 1024-thread CTA per SM.
+#include <stdlib.h>
+#include "ntt_kernels.cuh"
+#include "tma.cuh"
+
+namespace mm {
+namespace grows {
+
+constexpr int LOGL = 13, L = 1 << LOGL, H = L / 2, NTH = 1024;
+typedef RowLayoutG<uint64_t, LOGL, 1> Lay;
+constexpr unsigned ROW_BYTES = L * 8;
+constexpr size_t SMEM = ROW_BYTES + (size_t)Lay::ELEMS * 8 + 16;
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(NTH, 1) k_grows_fwd(FpG f, RowArgs<FpG> a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* land = (uint64_t*)smem_raw;
+    uint64_t* s = land + L;
+    uint64_t* bar = s + Lay::ELEMS;
+    const uint64_t* full = (const uint64_t*)a.lvl + L;    // w_L^e, e < L
+    const bool fast = __ldg(full + (L >> 6)) == gold::Pow2Val<gold::S_FWD>::v;
+    const uint64_t* in = (const uint64_t*)a.in;
+    uint64_t* out = (uint64_t*)a.out;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < a.nrows) bulk_load(land, in + blockIdx.x * a.in_rs, ROW_BYTES, &bar[0]);
+    }
+    __syncthreads();
+    int it = 0;
+    for (long long r = blockIdx.x; r < a.nrows; r += gridDim.x, it++) {
+        mbar_wait(&bar[0], it & 1);
+        if (fast) {
+            // radix-2 level of span 4096 (twiddle w_8192^j) from the landing buffer
+            for (int j = threadIdx.x; j < H; j += NTH) {
+                const uint64_t x = land[j], y = land[j + H];
+                s[Lay::addr(0, j)] = FpG::add(x, y);
+                s[Lay::addr(0, j + H)] = FpG::mul(FpG::sub(x, y), __ldg(full + j));
+            }
+        } else {
+            for (int j = threadIdx.x; j < L; j += NTH) s[Lay::addr(0, j)] = land[j];
+        }
+        __syncthreads();
+        const long long nxt = r + gridDim.x;
+        if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(land, in + nxt * a.in_rs, ROW_BYTES, &bar[0]);
+        if (fast) gold::dif_ln<Lay, 4096, 2, NTH, gold::S_FWD>(s, full, 2, L / 64);
+        else run_tile<FpG, Lay, LOGL, false, NTH>(f, s, a.lvl, a.lvl);
+        // canonical output, 16-byte stores (TFT order within the row)
+        uint64_t* ob = out + r * a.out_rs;
+        for (int e = threadIdx.x; e < L / 2; e += NTH) {
+            const int j = 2 * e;
+            *(ulonglong2*)(ob + j) = make_ulonglong2(f.canon(s[Lay::addr(0, j)]), f.canon(s[Lay::addr(0, j + 1)]));
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace grows
+
+bool gold_rows_tma_ok(const RowArgs<FpG>& a) {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    using namespace grows;
+    return on && !a.perm && a.vec_in && a.vec_out && a.in_seg_log == 0 && a.out_seg_log == 0 && a.in_len == L &&
+           a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0;
+}
+
+mm_status launch_gold_rows_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st) {
+    using namespace grows;
+    auto kern = k_grows_fwd;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    const int grid = (int)(a.nrows < num_sms() ? a.nrows : num_sms());
+    {
+        LaunchScope ls("ntt_rows_fwd", st);
+        kern<<<grid, NTH, SMEM, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+}  // namespace mm
