@@ -1,5 +1,6 @@
-// gold_rows.cu -- the Goldilocks forward row pass of 2^13-point rows (C4:
-// Algorithm 1 steps 3-4) with its rows staged by bulk copies.
+// gold_rows.cu -- the Goldilocks 2^13-point row passes with their rows
+// staged by bulk copies: the forward row pass (C4: Algorithm 1 steps 3-4,
+// P:895-913) and the fused product rows (C5).
 //
 // k_rows (ntt_kernels.cuh) loads a row with per-thread 16-byte loads into
 // the padded tile and then runs the radix-2 level of span 4096 as a separate
@@ -72,6 +73,80 @@ __global__ void __launch_bounds__(NTH, 1) k_grows_fwd(FpG f, RowArgs<FpG> a) {
     }
 }
 
+
+// ---------------------------------------------------------------- fused product rows (C5)
+// Steps 3-4 of both operands, the entry-wise product with n^-1 and
+// the inverse row transform with the inverse step-2 twiddle, per row of
+// 2^13 points.  k_rows_pmul keeps one row in shared memory (two CTAs per SM)
+// and parks the first spectrum in an L2 scratch row; here one 1024-thread CTA
+// per SM holds both spectra (2 x 65 KiB) beside a 64 KiB landing buffer that
+// the operand rows stream through by bulk copies: a_r, then b_r while a_r is
+// transformed, then a_{r+1} while b_r is transformed and the product row is
+// formed and transformed back.
+constexpr size_t PSMEM = ROW_BYTES + 2 * (size_t)Lay::ELEMS * 8 + 16;
+
+__global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* land = (uint64_t*)smem_raw;
+    uint64_t* sa = land + L;
+    uint64_t* sb = sa + Lay::ELEMS;
+    uint64_t* bar = sb + Lay::ELEMS;
+    const uint64_t* fullf = (const uint64_t*)a.lvl_f + L;
+    const bool fast = __ldg(fullf + (L >> 6)) == gold::Pow2Val<gold::S_FWD>::v;
+    const uint64_t* A = (const uint64_t*)a.a;
+    const uint64_t* B = (const uint64_t*)a.b;
+    uint64_t* Cc = (uint64_t*)a.c;
+    const unsigned i2mask = (1u << a.k2) - 1;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < a.nrows) bulk_load(land, A + blockIdx.x * a.a_rs, ROW_BYTES, &bar[0]);
+    }
+    __syncthreads();
+    unsigned ph = 0;
+    for (long long r = blockIdx.x; r < a.nrows; r += gridDim.x) {
+        const long long nxt = r + gridDim.x;
+#pragma unroll 1
+        for (int op = 0; op < 2; op++) {
+            uint64_t* s = op ? sb : sa;
+            mbar_wait(&bar[0], ph & 1);
+            ph++;
+            if (fast) {
+                for (int j = threadIdx.x; j < H; j += NTH) {
+                    const uint64_t x = land[j], y = land[j + H];
+                    s[Lay::addr(0, j)] = FpG::add(x, y);
+                    s[Lay::addr(0, j + H)] = FpG::mul(FpG::sub(x, y), __ldg(fullf + j));
+                }
+            } else {
+                for (int j = threadIdx.x; j < L; j += NTH) s[Lay::addr(0, j)] = land[j];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (op == 0) bulk_load(land, B + r * a.b_rs, ROW_BYTES, &bar[0]);
+                else if (nxt < a.nrows) bulk_load(land, A + nxt * a.a_rs, ROW_BYTES, &bar[0]);
+            }
+            if (fast) gold::dif_ln<Lay, 4096, 2, NTH, gold::S_FWD>(s, fullf, 2, L / 64);
+            else run_tile<FpG, Lay, LOGL, false, NTH>(f, s, a.lvl_f, a.lvl_f);
+        }
+        // entry-wise product with n^-1 (same positions in both bit-reversed spectra)
+        for (int j = threadIdx.x; j < L; j += NTH) {
+            const int ix = Lay::addr(0, j);
+            sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
+        }
+        __syncthreads();
+        run_tile<FpG, Lay, LOGL, true, NTH>(f, sa, a.lvl_i, a.lvl_i);
+        // inverse step-2 twiddle w^-(j1 [i2]) (the plan's full table row), 16-byte I/O
+        const uint64_t* tw = a.fs_full + (size_t)((unsigned)(a.row0 + r) & i2mask) * L;
+        uint64_t* ob = Cc + r * a.c_rs;
+        for (int e = threadIdx.x; e < L / 2; e += NTH) {
+            const int j = 2 * e;
+            const ulonglong2 w = __ldg((const ulonglong2*)(tw + j));
+            *(ulonglong2*)(ob + j) =
+                make_ulonglong2(f.mulw(sa[Lay::addr(0, j)], w.x), f.mulw(sa[Lay::addr(0, j + 1)], w.y));
+        }
+        __syncthreads();
+    }
+}
 }  // namespace grows
 
 bool gold_rows_tma_ok(const RowArgs<FpG>& a) {
@@ -82,6 +157,30 @@ bool gold_rows_tma_ok(const RowArgs<FpG>& a) {
     using namespace grows;
     return on && !a.perm && a.vec_in && a.vec_out && a.in_seg_log == 0 && a.out_seg_log == 0 && a.in_len == L &&
            a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0;
+}
+
+bool gold_pmul_rows_tma_ok(const PmulArgs<FpG>& a) {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    using namespace grows;
+    return on && a.nmod <= 1 && a.fs == 1 && a.fs_full != nullptr && a.vec_in && a.vec_out && a.in_seg_log == 0 &&
+           a.out_seg_log == 0 && a.la == L && a.lb == L && a.lc == L && a.a_rs % 2 == 0 && a.b_rs % 2 == 0 &&
+           a.rows_per == 0 && ((uintptr_t)a.fs_full & 15) == 0;
+}
+
+mm_status launch_gold_pmul_rows_tma(const FpG& f, const PmulArgs<FpG>& a, cudaStream_t st) {
+    using namespace grows;
+    auto kern = k_gpmul_rows;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSMEM));
+    const int grid = (int)(a.nrows < num_sms() ? a.nrows : num_sms());
+    {
+        LaunchScope ls("pmul_rows_fourstep", st);
+        kern<<<grid, NTH, PSMEM, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
 }
 
 mm_status launch_gold_rows_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st) {

@@ -200,6 +200,10 @@ template <class F> struct PmulArgs {
     const W* fsfullm[3];
 };
 
+// Goldilocks fused product rows of 2^13 points with bulk-copied rows (gold_rows.cu)
+bool gold_pmul_rows_tma_ok(const PmulArgs<FpG>& a);
+mm_status launch_gold_pmul_rows_tma(const FpG& f, const PmulArgs<FpG>& a, cudaStream_t st);
+
 // Epilogue selector (compile time): bits 0-1 = step-2 twiddle (0 none, 1 full
 // table, 2 two-level split table), bit 2 = multiply by a constant (n^-1),
 // bit 3 = canonicalise to [0, p).
@@ -1002,6 +1006,9 @@ static mm_status launch_pmul_e(const F& f, PmulArgs<F> a, cudaStream_t st) {
                (!a.in_seg_log || (1 << a.in_seg_log) >= V) && aligned16(a.a) && aligned16(a.b);
     a.vec_out = sizeof(TOut) == sizeof(T) && a.c_rs % V == 0 && a.out_seg_stride % V == 0 &&
                 (!a.out_seg_log || (1 << a.out_seg_log) >= V) && aligned16(a.c);
+    if constexpr (std::is_same<F, FpG>::value && LOGL == 13 && EPIV == EPI_FS_FULL && sizeof(TIn) == 8 &&
+                  sizeof(TOut) == 8)
+        if (gold_pmul_rows_tma_ok(a)) return launch_gold_pmul_rows_tma(f, a, st);
     auto kern = k_rows_pmul<F, LOGL, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
