@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
     uint64_t* bar = sb + Lay::ELEMS;
     const uint64_t* fullf = (const uint64_t*)a.lvl_f + L;
     const bool fast = __ldg(fullf + (L >> 6)) == gold::Pow2Val<gold::S_FWD>::v;
+    const uint64_t* fulli = (const uint64_t*)a.lvl_i + L;
+    const bool fasti = __ldg(fulli + (L >> 6)) == gold::Pow2Val<gold::S_INV>::v;
     const uint64_t* A = (const uint64_t*)a.a;
     const uint64_t* B = (const uint64_t*)a.b;
     uint64_t* Cc = (uint64_t*)a.c;
@@ -134,15 +136,26 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
             sa[ix] = f.mulw(f.mul_redc(sa[ix], sb[ix]), a.sc);
         }
         __syncthreads();
-        run_tile<FpG, Lay, LOGL, true, NTH>(f, sa, a.lvl_i, a.lvl_i);
-        // inverse step-2 twiddle w^-(j1 [i2]) (the plan's full table row), 16-byte I/O
+        // inverse row transform and the inverse step-2 twiddle w^-(j1 [i2]) (the
+        // plan's full table row); on the gold path the last DIT level (span
+        // 4096, twiddle w_8192^-j) runs in the store loop
         const uint64_t* tw = a.fs_full + (size_t)((unsigned)(a.row0 + r) & i2mask) * L;
         uint64_t* ob = Cc + r * a.c_rs;
-        for (int e = threadIdx.x; e < L / 2; e += NTH) {
-            const int j = 2 * e;
-            const ulonglong2 w = __ldg((const ulonglong2*)(tw + j));
-            *(ulonglong2*)(ob + j) =
-                make_ulonglong2(f.mulw(sa[Lay::addr(0, j)], w.x), f.mulw(sa[Lay::addr(0, j + 1)], w.y));
+        if (fast && fasti) {
+            gold::dit_ln<Lay, 4096, 2, NTH, gold::S_INV>(sa, fulli, 2, L / 64);
+            for (int j = threadIdx.x; j < H; j += NTH) {
+                const uint64_t x = sa[Lay::addr(0, j)], t = FpG::mul(sa[Lay::addr(0, j + H)], __ldg(fulli + j));
+                ob[j] = f.mulw(FpG::add(x, t), __ldg(tw + j));
+                ob[j + H] = f.mulw(FpG::sub(x, t), __ldg(tw + j + H));
+            }
+        } else {
+            run_tile<FpG, Lay, LOGL, true, NTH>(f, sa, a.lvl_i, a.lvl_i);
+            for (int e = threadIdx.x; e < L / 2; e += NTH) {
+                const int j = 2 * e;
+                const ulonglong2 w = __ldg((const ulonglong2*)(tw + j));
+                *(ulonglong2*)(ob + j) =
+                    make_ulonglong2(f.mulw(sa[Lay::addr(0, j)], w.x), f.mulw(sa[Lay::addr(0, j + 1)], w.y));
+            }
         }
         __syncthreads();
     }
