@@ -1,6 +1,6 @@
 // gold_rows.cu -- the Goldilocks 2^13-point row passes with their rows
 // staged by bulk copies: the forward row pass (C4: Algorithm 1 steps 3-4,
-// P:895-913) and the fused product rows (C5).
+// P:895-913), the inverse row pass and the fused product rows (C5).
 //
 // k_rows (ntt_kernels.cuh) loads a row with per-thread 16-byte loads into
 // the padded tile and then runs the radix-2 level of span 4096 as a separate
@@ -160,6 +160,62 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
         __syncthreads();
     }
 }
+
+// ---------------------------------------------------------------- inverse rows (C4 inverse)
+// Inverse row transform (DIT) of 2^13-point rows with the inverse step-2
+// twiddle: the row and its twiddle row (the plan's full table) arrive by bulk
+// copies a row ahead; the row is copied into the padded tile (the DIT's first
+// stage reads 8 consecutive words per thread), the last DIT level runs in the
+// store loop.  64 + 64 + 65 KiB: one 1024-thread CTA per SM.
+constexpr size_t ISMEM = 2 * (size_t)ROW_BYTES + (size_t)Lay::ELEMS * 8 + 16;
+
+__global__ void __launch_bounds__(NTH, 1) k_grows_inv(FpG f, RowArgs<FpG> a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* land = (uint64_t*)smem_raw;
+    uint64_t* twl = land + L;
+    uint64_t* s = twl + L;
+    uint64_t* bar = s + Lay::ELEMS;
+    const uint64_t* fulli = (const uint64_t*)a.lvl + L;
+    const bool fast = __ldg(fulli + (L >> 6)) == gold::Pow2Val<gold::S_INV>::v;
+    const uint64_t* in = (const uint64_t*)a.in;
+    uint64_t* out = (uint64_t*)a.out;
+    const unsigned i2mask = (1u << a.k2) - 1;
+    auto twrow = [&](long long r) { return a.fs_full + (size_t)((unsigned)(a.row0 + r) & i2mask) * L; };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < a.nrows) {
+            bulk_load(land, in + blockIdx.x * a.in_rs, ROW_BYTES, &bar[0]);
+            bulk_load(twl, twrow(blockIdx.x), ROW_BYTES, &bar[1]);
+        }
+    }
+    __syncthreads();
+    int it = 0;
+    for (long long r = blockIdx.x; r < a.nrows; r += gridDim.x, it++) {
+        const long long nxt = r + gridDim.x;
+        mbar_wait(&bar[0], it & 1);
+        for (int j = threadIdx.x; j < L; j += NTH) s[Lay::addr(0, j)] = land[j];
+        __syncthreads();
+        if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(land, in + nxt * a.in_rs, ROW_BYTES, &bar[0]);
+        uint64_t* ob = out + r * a.out_rs;
+        if (fast) {
+            gold::dit_ln<Lay, 4096, 2, NTH, gold::S_INV>(s, fulli, 2, L / 64);
+            mbar_wait(&bar[1], it & 1);
+            for (int j = threadIdx.x; j < H; j += NTH) {
+                const uint64_t x = s[Lay::addr(0, j)], t = FpG::mul(s[Lay::addr(0, j + H)], __ldg(fulli + j));
+                ob[j] = f.mulw(FpG::add(x, t), twl[j]);
+                ob[j + H] = f.mulw(FpG::sub(x, t), twl[j + H]);
+            }
+        } else {
+            run_tile<FpG, Lay, LOGL, true, NTH>(f, s, a.lvl, a.lvl);
+            mbar_wait(&bar[1], it & 1);
+            for (int j = threadIdx.x; j < L; j += NTH) ob[j] = f.mulw(s[Lay::addr(0, j)], twl[j]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(twl, twrow(nxt), ROW_BYTES, &bar[1]);
+    }
+}
 }  // namespace grows
 
 bool gold_rows_tma_ok(const RowArgs<FpG>& a) {
@@ -191,6 +247,30 @@ mm_status launch_gold_pmul_rows_tma(const FpG& f, const PmulArgs<FpG>& a, cudaSt
     {
         LaunchScope ls("pmul_rows_fourstep", st);
         kern<<<grid, NTH, PSMEM, st>>>(f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
+bool gold_rows_inv_tma_ok(const RowArgs<FpG>& a) {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    using namespace grows;
+    return on && !a.perm && a.fs == 1 && a.fs_full != nullptr && a.vec_in && a.vec_out && a.in_seg_log == 0 &&
+           a.out_seg_log == 0 && a.in_len == L && a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0 &&
+           ((uintptr_t)a.fs_full & 15) == 0;
+}
+
+mm_status launch_gold_rows_inv_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st) {
+    using namespace grows;
+    auto kern = k_grows_inv;
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ISMEM));
+    const int grid = (int)(a.nrows < num_sms() ? a.nrows : num_sms());
+    {
+        LaunchScope ls("ntt_rows_inv", st);
+        kern<<<grid, NTH, ISMEM, st>>>(f, a);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;

@@ -164,6 +164,8 @@ bool gold_cols16_tma_ok(const ColArgs<FpG>& a);
 // Goldilocks forward row pass of 2^13 points with bulk-copied rows (gold_rows.cu)
 bool gold_rows_tma_ok(const RowArgs<FpG>& a);
 mm_status launch_gold_rows_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st);
+bool gold_rows_inv_tma_ok(const RowArgs<FpG>& a);
+mm_status launch_gold_rows_inv_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st);
 // inverse Goldilocks column passes of 2^11 / 2^12 points with TMA-staged tiles (gold_cols.cu)
 bool gold_cols_inv_tma_ok(const ColArgs<FpG>& a, int logl);
 mm_status launch_gold_cols_inv_tma(const FpG& f, const ColArgs<FpG>& a, int logl, int epiv, cudaStream_t st);
@@ -949,6 +951,9 @@ static mm_status launch_rows_e(const F& f, RowArgs<F> a, cudaStream_t st) {
     if constexpr (std::is_same<F, FpG>::value && LOGL == 13 && !INV && EPIV == EPI_CANON && sizeof(TIn) == 8 &&
                   sizeof(TOut) == 8)
         if (gold_rows_tma_ok(a)) return launch_gold_rows_tma(f, a, st);
+    if constexpr (std::is_same<F, FpG>::value && LOGL == 13 && INV && EPIV == EPI_FS_FULL && sizeof(TIn) == 8 &&
+                  sizeof(TOut) == 8)
+        if (gold_rows_inv_tma_ok(a)) return launch_gold_rows_inv_tma(f, a, st);
     auto kern = k_rows<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;
