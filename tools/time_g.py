@@ -52,6 +52,7 @@ out["C4_fwd_ms"] = round(tloop(f), 4)
 out["C4_inv_ms"] = round(tloop(g), 4)
 mm.set_product_streams(1)
 out["C4_fwd_ms_one_stream"] = round(tloop(f), 4)
+out["C4_inv_ms_one_stream"] = round(tloop(g), 4)
 mm.set_product_streams(2)
 out["C4_fwd_kernels"] = kern(f)
 out["C4_inv_kernels"] = kern(g)
@@ -62,5 +63,8 @@ a = gen.limbs16_torch(gen.config_seed(5), 1, n, dev).view(torch.uint16)
 b = gen.limbs16_torch(gen.config_seed(5), 2, n, dev).view(torch.uint16)
 h = lambda: mm.int_mul_u16(a, b)
 out["C5_ms"] = round(tloop(h, 5), 4)
+mm.set_product_streams(1)
+out["C5_ms_one_stream"] = round(tloop(h, 5), 4)
+mm.set_product_streams(2)
 out["C5_kernels"] = kern(h, 3)
 print(json.dumps(out))
