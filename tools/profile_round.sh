@@ -17,11 +17,11 @@ ncu --set full --clock-control none --import-source on -k "regex:k_col|k_row" -s
     -o gpurun_out/${R}_full_c3 python tools/prof_run.py c3 > gpurun_out/${R}_ncu_full_c3.log 2>&1
 echo full_c3_rc=$?
 python tools/prof_run.py c4 > gpurun_out/${R}_plain_c4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_cols|k_rows" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_grows|k_cols|k_rows" -s 2 -c 2 \
     -o gpurun_out/${R}_full_c4 python tools/prof_run.py c4 > gpurun_out/${R}_ncu_full_c4.log 2>&1
 echo full_c4_rc=$?
 python tools/prof_run.py c5 > gpurun_out/${R}_plain_c5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_cols|k_rows|k_carry" -s 5 -c 5 \
+ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_gpmul|k_cols|k_rows|k_carry" -s 5 -c 5 \
     -o gpurun_out/${R}_full_c5 python tools/prof_run.py c5 > gpurun_out/${R}_ncu_full_c5.log 2>&1
 echo full_c5_rc=$?
 python tools/ncu_summary.py launches gpurun_out/${R}_launches.csv gpurun_out/${R}_launches_summary.txt > /dev/null
