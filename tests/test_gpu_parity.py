@@ -1248,3 +1248,40 @@ def test_jobs_many_and_errors(mm, O):
     assert mm.lib().mm_launch_count() == n0
     with pytest.raises(mm.MMError):
         mm.Jobs().poly_mul(dev(x[0]), dev(x[1]), 1000003, 2, torch.empty(127, dtype=torch.uint32, device=DEV)).run()
+
+
+def test_gold_tma_and_plain_kernels_agree(mm, O):
+    # The TMA-staged Goldilocks passes (column tiles, bulk-copied rows) and the
+    # per-thread-load kernels they replace (still used for sharded / segmented
+    # / partial inputs) on the same C4-shaped transforms and a C5-shaped
+    # product, each in a fresh process (MMNTT_GOLD_TMA is read once)
+    import hashlib
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import hashlib, sys, torch
+sys.path.insert(0, %r)
+import gen, paper_1407_3383_b200 as mm
+PG = (1 << 64) - (1 << 32) + 1
+dev = torch.device("cuda")
+x = gen.residues_torch(gen.config_seed(4), 21, 2 << 24, PG, dev).view(torch.uint64)
+plan = mm.NttPlan(64, PG, 24, pow(7, (PG - 1) >> 24, PG), 2)
+y = plan.forward(x, out=torch.empty_like(x), order=mm.BITREV)
+z = plan.inverse(y, out=torch.empty_like(y), order=mm.BITREV)
+a = gen.limbs16_torch(gen.config_seed(5), 21, 1 << 24, dev).view(torch.uint16)
+b = gen.limbs16_torch(gen.config_seed(5), 22, 1 << 24, dev).view(torch.uint16)
+c = mm.int_mul_u16(a, b)
+h = hashlib.sha256()
+for t in (y, z, c):
+    h.update(t.cpu().numpy().tobytes())
+print(h.hexdigest(), bool(torch.equal(z, x)))
+""" % root
+    outs = []
+    for v in ("1", "0"):
+        env = dict(os.environ, MMNTT_GOLD_TMA=v)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split()[-2:])
+    assert outs[0][1] == "True" and outs[1][1] == "True"
+    assert outs[0][0] == outs[1][0]
