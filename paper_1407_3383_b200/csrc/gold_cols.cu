@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(TileCfg<C>::NTH, C == 4 ? 1 : 2) k_gcols_fwd(c
             const ulonglong2 w = *(const ulonglong2*)(twl + t * C + c);
             const uint64_t v0 = f.mulw(s[Lay::addr(c, t)], w.x);
             const uint64_t v1 = f.mulw(s[Lay::addr(c + 1, t)], w.y);
-            *(ulonglong2*)(ob + (unsigned)t * ors + c) = make_ulonglong2(v0, v1);
+            // fused transpose (sharded transform): row t goes to its owner's receive buffer
+            uint64_t* dst = a.npeers ? (uint64_t*)a.peer_out[t >> a.peer_shift] + cl0 : ob;
+            *(ulonglong2*)(dst + (unsigned)t * ors + c) = make_ulonglong2(v0, v1);
         }
         __syncthreads();
         if (threadIdx.x == 0 && nxt < ntiles) {
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(TileCfg<C>::NTH, C == 4 ? 1 : 2) k_gcols_fwd(c
             tma_load_tile(twl, &tmw, (int)(a.col0 + ncl0), 0, 0, &bar[1], TILE_BYTES);
         }
     }
+    // peer stores ordered system-wide before the stream's next kernel raises the ready flags
+    if (a.npeers) __threadfence_system();
 }
 
 // 3-D view {cols, 256 rows, groups of 256 rows} of a row-major u64 matrix with
@@ -400,9 +404,10 @@ bool gold_cols_tma_ok(const ColArgs<FpG>& a) {
         return !(e && e[0] == '0');
     }();
     using namespace gcols;
-    return on && tma_encoder() != nullptr && a.nmod <= 1 && a.npeers == 0 && a.fs_full != nullptr &&
+    return on && tma_encoder() != nullptr && a.nmod <= 1 && a.fs_full != nullptr &&
            a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && a.n1 % 2 == 0 &&
-           a.in_bs == (long long)L * a.in_rs && a.in_len >= (long long)L * a.n1 && a.out_len >= (long long)L * a.n1 &&
+           (a.nbatch == 1 || a.in_bs == (long long)L * a.in_rs) && a.in_len >= (long long)L * a.n1 &&
+           a.out_len >= (long long)L * a.n1 &&
            ((uintptr_t)a.fs_full & 15) == 0 && a.nbatch * NBOX < (1ll << 31) && a.n1 < (1ll << 31);
 }
 
@@ -457,7 +462,7 @@ bool gold_cols_inv_tma_ok(const ColArgs<FpG>& a, int logl) {
     }();
     const long long L = 1ll << logl;
     return on && (logl == 11 || logl == 12) && tma_encoder() != nullptr && a.nmod <= 1 && a.npeers == 0 &&
-           a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && a.in_bs == L * a.in_rs &&
+           a.vec_in && a.vec_out && a.ncols % 4 == 0 && a.in_rs % 2 == 0 && (a.nbatch == 1 || a.in_bs == L * a.in_rs) &&
            a.in_len >= L * a.n1 && a.nbatch * (L / 256) < (1ll << 31) && a.n1 < (1ll << 31);
 }
 
