@@ -30,6 +30,25 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                  : "memory");
 }
 
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// row r of a (possibly segmented) row array into the landing buffer: element
+// j at base + r rs + seg_j(j) -- one copy per 2^seglog-element segment (the
+// sharded transform's rows are G segments in G receive buffers)
+__device__ __forceinline__ void load_row(uint64_t* land, const uint64_t* base, long long r, long long rs, int seglog,
+                                         long long segstride, uint64_t* bar) {
+    if (!seglog) {
+        bulk_load(land, base + r * rs, ROW_BYTES, bar);
+        return;
+    }
+    mbar_arrive_tx(bar, ROW_BYTES);
+    const int seg = 1 << seglog;
+    for (int i = 0; i < L / seg; i++) bulk_copy(land + i * seg, base + i * segstride + r * rs, (unsigned)seg * 8, bar);
+}
+
 __global__ void __launch_bounds__(NTH, 1) k_grows_fwd(FpG f, RowArgs<FpG> a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     uint64_t* land = (uint64_t*)smem_raw;
@@ -42,7 +61,8 @@ __global__ void __launch_bounds__(NTH, 1) k_grows_fwd(FpG f, RowArgs<FpG> a) {
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_fence_init();
-        if ((long long)blockIdx.x < a.nrows) bulk_load(land, in + blockIdx.x * a.in_rs, ROW_BYTES, &bar[0]);
+        if ((long long)blockIdx.x < a.nrows)
+            load_row(land, in, blockIdx.x, a.in_rs, a.in_seg_log, a.in_seg_stride, &bar[0]);
     }
     __syncthreads();
     int it = 0;
@@ -60,7 +80,7 @@ __global__ void __launch_bounds__(NTH, 1) k_grows_fwd(FpG f, RowArgs<FpG> a) {
         }
         __syncthreads();
         const long long nxt = r + gridDim.x;
-        if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(land, in + nxt * a.in_rs, ROW_BYTES, &bar[0]);
+        if (threadIdx.x == 0 && nxt < a.nrows) load_row(land, in, nxt, a.in_rs, a.in_seg_log, a.in_seg_stride, &bar[0]);
         if (fast) gold::dif_ln<Lay, 4096, 2, NTH, gold::S_FWD>(s, full, 2, L / 64);
         else run_tile<FpG, Lay, LOGL, false, NTH>(f, s, a.lvl, a.lvl);
         // canonical output, 16-byte stores (TFT order within the row)
@@ -102,7 +122,8 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_fence_init();
-        if ((long long)blockIdx.x < a.nrows) bulk_load(land, A + blockIdx.x * a.a_rs, ROW_BYTES, &bar[0]);
+        if ((long long)blockIdx.x < a.nrows)
+            load_row(land, A, blockIdx.x, a.a_rs, a.in_seg_log, a.in_seg_stride, &bar[0]);
     }
     __syncthreads();
     unsigned ph = 0;
@@ -124,8 +145,8 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
             }
             __syncthreads();
             if (threadIdx.x == 0) {
-                if (op == 0) bulk_load(land, B + r * a.b_rs, ROW_BYTES, &bar[0]);
-                else if (nxt < a.nrows) bulk_load(land, A + nxt * a.a_rs, ROW_BYTES, &bar[0]);
+                if (op == 0) load_row(land, B, r, a.b_rs, a.in_seg_log, a.in_seg_stride, &bar[0]);
+                else if (nxt < a.nrows) load_row(land, A, nxt, a.a_rs, a.in_seg_log, a.in_seg_stride, &bar[0]);
             }
             if (fast) gold::dif_ln<Lay, 4096, 2, NTH, gold::S_FWD>(s, fullf, 2, L / 64);
             else run_tile<FpG, Lay, LOGL, false, NTH>(f, s, a.lvl_f, a.lvl_f);
@@ -140,20 +161,22 @@ __global__ void __launch_bounds__(NTH, 1) k_gpmul_rows(FpG f, PmulArgs<FpG> a) {
         // plan's full table row); on the gold path the last DIT level (span
         // 4096, twiddle w_8192^-j) runs in the store loop
         const uint64_t* tw = a.fs_full + (size_t)((unsigned)(a.row0 + r) & i2mask) * L;
-        uint64_t* ob = Cc + r * a.c_rs;
+        uint64_t* ob = Cc + r * a.c_rs;        // element j at ob + seg_j(j): plain or segmented rows
+        const int osl = a.out_seg_log;
+        const long long oss = a.out_seg_stride;
         if (fast && fasti) {
             gold::dit_ln<Lay, 4096, 2, NTH, gold::S_INV>(sa, fulli, 2, L / 64);
             for (int j = threadIdx.x; j < H; j += NTH) {
                 const uint64_t x = sa[Lay::addr(0, j)], t = FpG::mul(sa[Lay::addr(0, j + H)], __ldg(fulli + j));
-                ob[j] = f.mulw(FpG::add(x, t), __ldg(tw + j));
-                ob[j + H] = f.mulw(FpG::sub(x, t), __ldg(tw + j + H));
+                ob[seg_j(j, osl, oss)] = f.mulw(FpG::add(x, t), __ldg(tw + j));
+                ob[seg_j(j + H, osl, oss)] = f.mulw(FpG::sub(x, t), __ldg(tw + j + H));
             }
         } else {
             run_tile<FpG, Lay, LOGL, true, NTH>(f, sa, a.lvl_i, a.lvl_i);
             for (int e = threadIdx.x; e < L / 2; e += NTH) {
-                const int j = 2 * e;
+                const int j = 2 * e;           // j, j + 1 in one segment (segments >= 2 elements)
                 const ulonglong2 w = __ldg((const ulonglong2*)(tw + j));
-                *(ulonglong2*)(ob + j) =
+                *(ulonglong2*)(ob + seg_j(j, osl, oss)) =
                     make_ulonglong2(f.mulw(sa[Lay::addr(0, j)], w.x), f.mulw(sa[Lay::addr(0, j + 1)], w.y));
             }
         }
@@ -198,19 +221,21 @@ __global__ void __launch_bounds__(NTH, 1) k_grows_inv(FpG f, RowArgs<FpG> a) {
         for (int j = threadIdx.x; j < L; j += NTH) s[Lay::addr(0, j)] = land[j];
         __syncthreads();
         if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(land, in + nxt * a.in_rs, ROW_BYTES, &bar[0]);
-        uint64_t* ob = out + r * a.out_rs;
+        uint64_t* ob = out + r * a.out_rs;     // element j at ob + seg_j(j): plain or segmented rows
+        const int osl = a.out_seg_log;
+        const long long oss = a.out_seg_stride;
         if (fast) {
             gold::dit_ln<Lay, 4096, 2, NTH, gold::S_INV>(s, fulli, 2, L / 64);
             mbar_wait(&bar[1], it & 1);
             for (int j = threadIdx.x; j < H; j += NTH) {
                 const uint64_t x = s[Lay::addr(0, j)], t = FpG::mul(s[Lay::addr(0, j + H)], __ldg(fulli + j));
-                ob[j] = f.mulw(FpG::add(x, t), twl[j]);
-                ob[j + H] = f.mulw(FpG::sub(x, t), twl[j + H]);
+                ob[seg_j(j, osl, oss)] = f.mulw(FpG::add(x, t), twl[j]);
+                ob[seg_j(j + H, osl, oss)] = f.mulw(FpG::sub(x, t), twl[j + H]);
             }
         } else {
             run_tile<FpG, Lay, LOGL, true, NTH>(f, s, a.lvl, a.lvl);
             mbar_wait(&bar[1], it & 1);
-            for (int j = threadIdx.x; j < L; j += NTH) ob[j] = f.mulw(s[Lay::addr(0, j)], twl[j]);
+            for (int j = threadIdx.x; j < L; j += NTH) ob[seg_j(j, osl, oss)] = f.mulw(s[Lay::addr(0, j)], twl[j]);
         }
         __syncthreads();
         if (threadIdx.x == 0 && nxt < a.nrows) bulk_load(twl, twrow(nxt), ROW_BYTES, &bar[1]);
@@ -224,8 +249,8 @@ bool gold_rows_tma_ok(const RowArgs<FpG>& a) {
         return !(e && e[0] == '0');
     }();
     using namespace grows;
-    return on && !a.perm && a.vec_in && a.vec_out && a.in_seg_log == 0 && a.out_seg_log == 0 && a.in_len == L &&
-           a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0;
+    return on && !a.perm && a.vec_in && a.vec_out && (a.in_seg_log == 0 || a.in_seg_log >= 8) && a.out_seg_log == 0 &&
+           a.in_len == L && a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0;
 }
 
 bool gold_pmul_rows_tma_ok(const PmulArgs<FpG>& a) {
@@ -234,8 +259,8 @@ bool gold_pmul_rows_tma_ok(const PmulArgs<FpG>& a) {
         return !(e && e[0] == '0');
     }();
     using namespace grows;
-    return on && a.nmod <= 1 && a.fs == 1 && a.fs_full != nullptr && a.vec_in && a.vec_out && a.in_seg_log == 0 &&
-           a.out_seg_log == 0 && a.la == L && a.lb == L && a.lc == L && a.a_rs % 2 == 0 && a.b_rs % 2 == 0 &&
+    return on && a.nmod <= 1 && a.fs == 1 && a.fs_full != nullptr && a.vec_in && a.vec_out &&
+           (a.in_seg_log == 0 || a.in_seg_log >= 8) && a.la == L && a.lb == L && a.lc == L && a.a_rs % 2 == 0 && a.b_rs % 2 == 0 &&
            a.rows_per == 0 && ((uintptr_t)a.fs_full & 15) == 0;
 }
 
@@ -259,8 +284,8 @@ bool gold_rows_inv_tma_ok(const RowArgs<FpG>& a) {
     }();
     using namespace grows;
     return on && !a.perm && a.fs == 1 && a.fs_full != nullptr && a.vec_in && a.vec_out && a.in_seg_log == 0 &&
-           a.out_seg_log == 0 && a.in_len == L && a.out_len == L && a.in_rs % 2 == 0 && a.rows_per == 0 &&
-           ((uintptr_t)a.fs_full & 15) == 0;
+           a.in_len == L && a.out_len == L && a.in_rs % 2 == 0 &&
+           a.rows_per == 0 && ((uintptr_t)a.fs_full & 15) == 0;
 }
 
 mm_status launch_gold_rows_inv_tma(const FpG& f, const RowArgs<FpG>& a, cudaStream_t st) {
