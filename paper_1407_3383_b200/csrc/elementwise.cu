@@ -59,16 +59,27 @@ template <int OP> struct OpUses { enum { X = OP != OP_SHOUP_PRE, Y = OP <= OP_MU
 constexpr int EW_THREADS = 256;
 constexpr int EW_UNROLL = 4;
 
+// A thread loads, computes and stores in turn, so HBM stays busy only while
+// enough other warps are in their load phase: registers are held to five
+// CTAs per SM (48; the Shoup precompute 0.82 -> 0.91 of HBM, the others
+// unchanged within noise), except for the full-range Shoup product, whose three operand
+// streams keep HBM busy at three CTAs per SM and which spills at 48 (0.65 ->
+// 0.80 ms).  Two vectors per round at six CTAs per SM made the full-range
+// Barrett and Shoup products slower (0.55 -> 0.60 ms, 0.65 -> 0.68 ms).
+template <int OP> struct EwMinBlocks { enum { v = OP == OP_MUL_SHOUP ? 1 : 5 }; };
+template <int OP> struct EwUnroll { enum { v = EW_UNROLL }; };
+
 template <int OP, bool FULL>
-__global__ void __launch_bounds__(EW_THREADS) k_elementwise_v4(ModDev m, const uint4* __restrict__ x,
+__global__ void __launch_bounds__(EW_THREADS, EwMinBlocks<OP>::v) k_elementwise_v4(ModDev m, const uint4* __restrict__ x,
                                                                const uint4* __restrict__ y,
                                                                const uint4* __restrict__ ys,
                                                                uint4* __restrict__ z, size_t nv) {
-    size_t stride = (size_t)gridDim.x * EW_THREADS * EW_UNROLL;
-    for (size_t base = (size_t)blockIdx.x * EW_THREADS * EW_UNROLL + threadIdx.x; base < nv; base += stride) {
-        uint4 vx[EW_UNROLL], vy[EW_UNROLL], vs[EW_UNROLL];
+    constexpr int U = EwUnroll<OP>::v;
+    size_t stride = (size_t)gridDim.x * EW_THREADS * U;
+    for (size_t base = (size_t)blockIdx.x * EW_THREADS * U + threadIdx.x; base < nv; base += stride) {
+        uint4 vx[U], vy[U], vs[U];
 #pragma unroll
-        for (int u = 0; u < EW_UNROLL; u++) {
+        for (int u = 0; u < U; u++) {
             size_t i = base + (size_t)u * EW_THREADS;
             if (i < nv) {
                 if (OpUses<OP>::X) vx[u] = __ldcs(x + i);
@@ -77,7 +88,7 @@ __global__ void __launch_bounds__(EW_THREADS) k_elementwise_v4(ModDev m, const u
             }
         }
 #pragma unroll
-        for (int u = 0; u < EW_UNROLL; u++) {
+        for (int u = 0; u < U; u++) {
             size_t i = base + (size_t)u * EW_THREADS;
             if (i < nv) {
                 uint4 r;
@@ -132,7 +143,7 @@ static mm_status launch(const mm_mod32* c, const uint32_t* x, const uint32_t* y,
     bool aligned = ((uintptr_t)x | (uintptr_t)y | (uintptr_t)ys | (uintptr_t)z) % 16 == 0;
     size_t nv = aligned ? n / 4 : 0;
     if (nv) {
-        size_t want = (nv + EW_THREADS * EW_UNROLL - 1) / (EW_THREADS * EW_UNROLL);
+        size_t want = (nv + EW_THREADS * EwUnroll<OP>::v - 1) / (EW_THREADS * EwUnroll<OP>::v);
         size_t cap = (size_t)num_sms() * 8;
         int grid = (int)(want < cap ? want : cap);
         LaunchScope ls(op_name(OP), st);
