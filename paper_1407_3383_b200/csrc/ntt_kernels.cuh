@@ -16,6 +16,7 @@
 #include "common.h"
 #include "ntt_core.cuh"
 #include "gold.cuh"
+#include "tma.cuh"
 
 namespace mm {
 
@@ -788,6 +789,182 @@ __global__ void __launch_bounds__(NTc<F, LOGL>::v, 1024 / NTc<F, LOGL>::v) k_col
     if (a.npeers) __threadfence_system();
 }
 
+// ---------------------------------------------------------------- column pass, TMA-staged (32-bit / FP64)
+// The generic column pass for tiles of C columns stored as one padded row
+// per column (RowLayoutOdd: 2^10-point 32-bit columns, 2^10 / 2^11-point
+// FP64 columns -- the 32-bit n >= 2^20 and FP64 n >= 2^20 plans) with its
+// input staged by TMA instead of per-thread loads: L / 256 box copies {C
+// columns, 256 rows} land the tile ([row][C], 32 / 64-byte row segments,
+// rows beyond the valid prefix zero-filled) a tile ahead, the landing buffer
+// is copied into the padded tile (lanes: columns fastest; raw 32-bit words
+// reduced on the way for the three-prime product) and the next tile streams
+// in under the transform.  Same tiles, layouts, twiddles and epilogues as
+// k_cols (a per-tile modulus for Remark 6 batches).
+template <class F, int LOGL> struct ColsTmaK {
+    typedef typename ColsTile<F, LOGL>::Lay Lay;
+    typedef typename F::T T;
+    static constexpr int L = 1 << LOGL, C = Lay::C, BOXR = 256, NB = L / BOXR;
+    static constexpr unsigned LAND_BYTES = (unsigned)L * C * sizeof(T);
+    enum { OK = !Lay::COL && !GoldT<F, LOGL>::v && LOGL >= 8 && (C * sizeof(T)) % 16 == 0 };
+    enum { TWS = ColsK<F, LOGL>::TWS };
+    static constexpr size_t smem() {
+        return LAND_BYTES + (size_t)Lay::ELEMS * sizeof(T) + (TWS ? (size_t)L * sizeof(typename F::W) : 0) + 16;
+    }
+};
+
+template <class F, int LOGL, bool INV, int EPIV>
+__global__ void __launch_bounds__(NT, 3) k_cols_tma(const __grid_constant__ CUtensorMap tm, F f, ColArgs<F> a) {
+    typedef ColsTmaK<F, LOGL> K;
+    typedef typename K::Lay Lay;
+    typedef typename F::T T;
+    typedef typename F::W W;
+    typedef typename Vec<T>::type TV;
+    typedef Epi<F, EPIV> E;
+    constexpr int L = K::L, C = K::C, V = Vec<T>::N, CV = C / V, TOT = L * CV;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T* land = (T*)smem_raw;
+    T* s = land + L * C;
+    W* tws = (W*)(s + Lay::ELEMS);
+    uint64_t* bar = (uint64_t*)(tws + (K::TWS ? L : 0));
+    const long long cgroups = a.ncols / C, ntiles = cgroups * a.nbatch;
+    const bool bmajor = a.nmod > 1;
+    const bool bsel = a.in_bs != 0;            // 0: every batch row reads the same input (three-prime raw limbs)
+    auto coords = [&](long long tile, long long& b, long long& cl0) {
+        b = bmajor ? tile / cgroups : tile % a.nbatch;
+        cl0 = (bmajor ? tile % cgroups : tile / a.nbatch) * C;
+    };
+    auto issue = [&](long long tile) {
+        long long b, cl0;
+        coords(tile, b, cl0);
+        mbar_arrive_tx(&bar[0], K::LAND_BYTES);
+        for (int i = 0; i < K::NB; i++)
+            tma_load_box3(land + i * K::BOXR * C, &tm, (int)cl0, i * K::BOXR, bsel ? (int)b : 0, &bar[0]);
+    };
+    F ff = f;
+    const W* lvl = a.lvl;
+    const W* fsf = a.fs_full;
+    const W* fslo = a.fs_lo;
+    const W* fshi = a.fs_hi;
+    W sc = a.sc;
+    int curq = -1;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_fence_init();
+        if ((long long)blockIdx.x < ntiles) issue(blockIdx.x);
+    }
+    if (K::TWS && !bmajor) stage_twiddles(tws, lvl, L);
+    __syncthreads();
+    const W* tw = K::TWS ? (const W*)tws : lvl;
+    const unsigned ors = (unsigned)a.out_rs;
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        long long b, cl0;
+        coords(tile, b, cl0);
+        const long long lin0 = a.col0 + cl0;
+        if (bmajor) {   // the modulus of this tile (Remark 6)
+            const int q = (int)(b / a.mod_span);
+            if (q != curq) {
+                curq = q;
+                ff = a.fm[q];
+                lvl = a.lvlm[q];
+                fsf = a.fsfullm[q];
+                fslo = a.fslom[q];
+                fshi = a.fshim[q];
+                sc = a.scm[q];
+                if (K::TWS) {
+                    __syncthreads();
+                    stage_twiddles(tws, lvl, L);
+                    __syncthreads();
+                } else {
+                    tw = lvl;
+                }
+            }
+        }
+        mbar_wait(&bar[0], it & 1);
+        for (int e = threadIdx.x; e < L * C; e += NT) {
+            T v = land[e];
+            if constexpr (std::is_same<F, Fp32>::value)
+                if (a.reduce_in) v = ff.reduce_raw(v);
+            s[Lay::addr(e % C, e / C)] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+        run_tile<F, Lay, LOGL, INV, NT>(ff, s, tw, lvl);
+        int tfull, tzero;
+        col_rows_valid(a.out_len, lin0, a.n1, C, L, &tfull, &tzero);
+        T* ob = (T*)a.out + b * a.out_bs + cl0;
+        for (int e = threadIdx.x; e < TOT; e += NT) {
+            const int t = e / CV, c = (e % CV) * V;
+            if (t >= tzero) continue;
+            T v[V];
+            W w[V];
+#pragma unroll
+            for (int i = 0; i < V; i++) v[i] = s[Lay::addr(c + i, t)];
+            if (E::FS == 1) ld_wvec<W, V>(fsf + (unsigned)t * (unsigned)a.n1 + (unsigned)lin0 + c, w);
+            const unsigned bt = (unsigned)brev(t, LOGL);
+#pragma unroll
+            for (int i = 0; i < V; i++) v[i] = E::apply(ff, v[i], w[i], fslo, fshi, a.fs_h, ((unsigned)lin0 + c + i) * bt, sc);
+            if (t < tfull) {
+                *(TV*)(ob + (unsigned)t * ors + c) = vmake<T>(v);
+            } else {
+#pragma unroll
+                for (int i = 0; i < V; i++)
+                    if ((long long)t * a.n1 + lin0 + c + i < a.out_len) ob[(unsigned)t * ors + c + i] = v[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// TMA view of the column input: {ncols (block), valid rows, batch rows}; the
+// valid prefix must end on a row boundary (rows past it are zero-filled)
+static inline bool cols_tma_on() {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_TMA_COLS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <class F, int LOGL> static bool cols_tma_ok(const ColArgs<F>& a) {
+    typedef typename F::T T;
+    return cols_tma_on() && tma_encoder() != nullptr && a.npeers == 0 && a.vec_in && a.vec_out && a.n1 > 0 &&
+           a.in_len % a.n1 == 0 && a.in_len > 0 && (a.in_rs * (long long)sizeof(T)) % 16 == 0 &&
+           ((a.in_bs * (long long)sizeof(T)) % 16 == 0) && a.in_rs >= a.ncols && a.nbatch < (1ll << 31) &&
+           a.ncols < (1ll << 31) && (a.in_bs == 0 || a.in_bs >= (a.in_len / a.n1) * a.in_rs);
+}
+template <class F, int LOGL, bool INV, int EPIV>
+static mm_status launch_cols_tma(const F& f, const ColArgs<F>& a, cudaStream_t st) {
+    typedef ColsTmaK<F, LOGL> K;
+    typedef typename F::T T;
+    auto enc = tma_encoder();
+    const long long rows = a.in_len / a.n1 < K::L ? a.in_len / a.n1 : K::L;
+    const long long nb = a.in_bs ? a.nbatch : 1;
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    cuuint64_t dims[3] = {(cuuint64_t)a.ncols, (cuuint64_t)rows, (cuuint64_t)nb};
+    cuuint64_t strides[2] = {(cuuint64_t)a.in_rs * sizeof(T), (cuuint64_t)(a.in_bs ? a.in_bs : a.in_rs * rows) * sizeof(T)};
+    cuuint32_t box[3] = {(cuuint32_t)K::C, (cuuint32_t)K::BOXR, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tm, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64, 3,
+                     const_cast<void*>(a.in), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(MM_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    auto kern = k_cols_tma<F, LOGL, INV, EPIV>;
+    const size_t smem = K::smem();
+    MM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long tiles = a.ncols / K::C * a.nbatch;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long cap = (long long)num_sms() * per_sm;
+    {
+        LaunchScope ls(INV ? "ntt_cols_inv" : "ntt_cols_fwd", st);
+        kern<<<(int)(tiles < cap ? tiles : cap), NT, smem, st>>>(tm, f, a);
+    }
+    MM_LAUNCH_CHECK();
+    return MM_OK;
+}
+
 // ---------------------------------------------------------------- fused product rows
 template <class F, int LOGL> struct PmulK {
     typedef typename PmulTile<F, LOGL>::Lay Lay;
@@ -989,6 +1166,9 @@ static mm_status launch_cols_e(const F& f, ColArgs<F> a, cudaStream_t st) {
     if constexpr (std::is_same<F, FpG>::value && (LOGL == 11 || LOGL == 12) && INV &&
                   (EPIV == EPI_CANON || EPIV == (EPI_SCALE | EPI_CANON)) && sizeof(TIn) == 8 && sizeof(TOut) == 8)
         if (gold_cols_inv_tma_ok(a, LOGL)) return launch_gold_cols_inv_tma(f, a, LOGL, EPIV, st);
+    if constexpr ((std::is_same<F, Fp32>::value || std::is_same<F, FpD>::value) && ColsTmaK<F, LOGL>::OK &&
+                  sizeof(TIn) == sizeof(T) && sizeof(TOut) == sizeof(T))
+        if (cols_tma_ok<F, LOGL>(a)) return launch_cols_tma<F, LOGL, INV, EPIV>(f, a, st);
     auto kern = k_cols<F, LOGL, INV, TIn, TOut, EPIV>;
     mm_status s = set_smem(kern, smem);
     if (s != MM_OK) return s;

@@ -49,6 +49,14 @@ __device__ __forceinline__ void tma_load_box2(void* dst, const CUtensorMap* tm, 
         : "memory");
 }
 
+// one 3-D box copy completing on a barrier armed by mbar_arrive_tx
+__device__ __forceinline__ void tma_load_box3(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"((const void*)tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
 static inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
