@@ -118,3 +118,18 @@ def test_modnum_constants_host_side(mm):
             L.mm_modnum_destroy(h)
     assert L.mm_modnum_create(64, 4, ctypes.byref(h)) == 1         # even
     assert L.mm_modnum_create(16, 7, ctypes.byref(h)) == 10        # bad fbits
+
+
+def test_run_jobs_validation_on_host(mm):
+    # mm_run_jobs validates the whole table on the host before anything launches
+    L = mm.lib()
+    assert L.mm_run_jobs(None, 0, None) == 0                       # nothing to do
+    assert L.mm_run_jobs(None, 1, None) == 10                      # MM_E_ARG: null table
+    bad = (mm._Job * 1)(mm._Job(7, 0, None, 0, 0, None, None, None, None, 0, 0))
+    assert L.mm_run_jobs(bad, 1, None) == 10                       # unknown kind
+    nullplan = (mm._Job * 1)(mm._Job(mm.Jobs.FORWARD, 0, None, 0, 0, None, None, None, None, 0, 0))
+    assert L.mm_run_jobs(nullplan, 1, None) == 10                  # transform job without a plan
+    big = (mm._Job * 1)(mm._Job(mm.Jobs.POLY_MUL, 0, None, 998244353, 3, 8, 8, 8, None, 4096, 4096))
+    assert L.mm_run_jobs(big, 1, None) == 3                        # MM_E_UNSUPPORTED_SIZE: 8191 > 2^12
+    nontt = (mm._Job * 1)(mm._Job(mm.Jobs.POLY_MUL, 0, None, 1000003, 2, 8, 8, 8, None, 100, 100))
+    assert L.mm_run_jobs(nontt, 1, None) != 0                      # 2^8 does not divide p - 1
