@@ -1,6 +1,9 @@
-// gold_cols.cu -- the Goldilocks forward column pass of 2^11-point columns
-// (C4: 2^24 = 2^11 columns x 2^13 rows, Algorithm 1 steps 1-2)
-// with its tiles staged by TMA.
+// gold_cols.cu -- Goldilocks column passes (Algorithm 1 steps 1-2 and their
+// inverse) with their tiles staged by TMA:
+//   k_gcols_fwd    2^11-point forward columns with step-2 twiddles (C4)
+//   k_gcols_inv    2^11 / 2^12-point inverse columns (C4 inverse, C5)
+//   k_gcols16_fwd  2^12-point forward columns of zero-padded 16-bit limbs (C5)
+// The forward C4 kernel, in detail:
 //
 // k_cols (ntt_kernels.cuh) loads a tile of four columns with per-thread
 // 16-byte loads and the step-2 twiddles at its store with per-thread table
@@ -17,8 +20,8 @@
 //   stores -> barrier -> TMA twiddles(i+1)
 //
 // so the next tile streams in under stages B-D and the twiddles under the
-// whole transform.  Shared memory per CTA: two landing tiles + the padded compute tile
-// (64 + 64 + 65 KiB, one CTA per SM).
+// whole transform.  Shared memory per CTA: two landing tiles + the padded
+// compute tile (64 + 64 + 65 KiB, one CTA per SM).
 #include <string.h>
 #include <stdlib.h>
 #include "ntt_kernels.cuh"
