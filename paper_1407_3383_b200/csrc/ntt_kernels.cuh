@@ -8,6 +8,10 @@
 //   k_rows_pmul : rows of two operands -> DIF, DIF, pointwise product, DIT
 //                 ("two direct TFT and one inverse TFT ... entry-wise
 //                 vector product"), fused in one pass.
+//   k_cols_tma  : k_cols for 32-bit / FP64 one-row-per-column tiles with the
+//                 input staged by TMA box copies.
+// The Goldilocks C4 / C5 passes with TMA / bulk-copy staging live in
+// gold_cols.cu and gold_rows.cu; the launchers below route to them.
 //
 // All sizes are template parameters (LOGL); launchers dispatch on the
 // runtime log2 length.  Explicit instantiations live in ntt_inst*.cu.
