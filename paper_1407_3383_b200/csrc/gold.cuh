@@ -482,6 +482,72 @@ __device__ __forceinline__ void dit_ln(uint64_t* s, const uint64_t* __restrict__
     __syncthreads();
 }
 
+// dit_ln for one 4096-point sub-transform per column (H = 1), split so that a
+// tile's first half can be transformed while its second half is still in
+// flight: stages D', C', B' touch only the rows of one 2048-row half
+// (D', C': rows 64 A + [0, 64) with A in [32 hh, 32 hh + 32); B': rows
+// 512 P + [0, 512) with P in [4 hh, 4 hh + 4)), stage A' needs both
+template <class Lay, int NT, int S>
+__device__ __forceinline__ void dit4096_half(uint64_t* s, const uint64_t* __restrict__ full, int hh) {
+    constexpr int C = Lay::C;
+    for (int q = threadIdx.x; q < C * 32 * 8; q += NT) {       // D': 8-point over bl
+        const int A = 32 * hh + (q & 31), P = (q >> 5) & 7, c = q >> 8;
+        uint64_t* p0 = s + Lay::addr(c, 64 * A + 8 * P);
+        uint64_t v[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(t)];
+        dit8<S>(v);
+#pragma unroll
+        for (int t = 0; t < 8; t++) p0[Lay::off(t)] = v[t];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < C * 32 * 8; q += NT) {       // C': w_64^-(bl r), 8-point over bh
+        const int A = 32 * hh + (q & 31), bl = (q >> 5) & 7, c = q >> 8;   // bl warp-uniform
+        uint64_t* p0 = s + Lay::addr(c, 64 * A + bl);
+        uint64_t v[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(8 * t)];
+        rot<S, 1, 8>(v, bl);
+        dit8<S>(v);
+#pragma unroll
+        for (int t = 0; t < 8; t++) p0[Lay::off(8 * t)] = v[t];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < C * 4 * 64; q += NT) {       // B': w_4096^-(b k_a), 8-point over al
+        const int b = q & 63, P = 4 * hh + ((q >> 6) & 3), c = q >> 8;
+        uint64_t* p0 = s + Lay::addr(c, 512 * P + b);
+        uint64_t v[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(64 * t)];
+        const int r = brev3(P);
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            const int ka = r + 8 * brev3(t);
+            v[t] = FpG::mul(v[t], __ldg(full + b * ka));
+        }
+        dit8<S>(v);
+#pragma unroll
+        for (int t = 0; t < 8; t++) p0[Lay::off(64 * t)] = v[t];
+    }
+    __syncthreads();
+}
+template <class Lay, int NT, int S>
+__device__ __forceinline__ void dit4096_a(uint64_t* s) {
+    constexpr int C = Lay::C;
+    for (int q = threadIdx.x; q < C * 512; q += NT) {           // A': w_64^-(al r), 8-point over ah
+        const int b = q & 63, al = (q >> 6) & 7, c = q >> 9;
+        uint64_t* p0 = s + Lay::addr(c, 64 * al + b);
+        uint64_t v[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) v[t] = p0[Lay::off(512 * t)];
+        rot<S, 1, 8>(v, al);
+        dit8<S>(v);
+#pragma unroll
+        for (int t = 0; t < 8; t++) p0[Lay::off(512 * t)] = v[t];
+    }
+    __syncthreads();
+}
+
 // Whole-tile transforms, L = 2^LOGL in {2^11, 2^12, 2^13}; full = w_L^e, e < L.
 template <class Lay, int LOGL, int NT>
 __device__ __forceinline__ void tile_dif(uint64_t* s, const uint64_t* __restrict__ full) {

@@ -189,7 +189,8 @@ template <int C> static mm_status launch(const FpG& f, const ColArgs<FpG>& a, cu
 // by box copies into a 64 KiB landing buffer -- the whole 2^11-point tile, or
 // a 2^12-point tile in two halves -- and is copied into the padded compute
 // tile (lanes: c fastest, conflict-free with the 4 mod 16 pitch); the next
-// tile's (first half) streams in under the whole DIT.
+// tile's (first half) streams in under the whole DIT.  A 2^12-point tile's
+// first half runs its half-local DIT stages while the second is in flight.
 template <int LOGL> struct Inv {
     static constexpr int L = 1 << LOGL, C = 4, HALVES = LOGL == 12 ? 2 : 1, LR = L / HALVES;
     static constexpr unsigned LAND_BYTES = LR * C * 8;       // 64 KiB
@@ -217,6 +218,8 @@ __global__ void __launch_bounds__(1024, 1) k_gcols_inv(const __grid_constant__ C
     uint64_t* land = (uint64_t*)smem_raw;
     uint64_t* s = land + LR * C;
     uint64_t* bar = s + Lay::ELEMS;
+    const uint64_t* full = (const uint64_t*)a.lvl + L;     // inverse powers w_L^-e, e < L
+    const bool fast = __ldg(full + (L >> 6)) == gold::Pow2Val<gold::S_INV>::v;
     const long long ntiles = a.ncols / C * a.nbatch;
     const unsigned ors = (unsigned)a.out_rs;
     auto coords = [&](long long tile, long long& b, long long& cl0) {
@@ -248,8 +251,13 @@ __global__ void __launch_bounds__(1024, 1) k_gcols_inv(const __grid_constant__ C
                 if (h + 1 < HALVES) issue(tile, h + 1);
                 else if (nxt < ntiles) issue(nxt, 0);
             }
+            // 2^12 points: the stages that stay inside one half run while the
+            // other half is in flight
+            if constexpr (HALVES == 2)
+                if (fast) gold::dit4096_half<Lay, NTH, gold::S_INV>(s, full, h);
         }
-        run_tile<FpG, Lay, LOGL, true, NTH>(f, s, a.lvl, a.lvl);
+        if (HALVES == 2 && fast) gold::dit4096_a<Lay, NTH, gold::S_INV>(s);
+        else run_tile<FpG, Lay, LOGL, true, NTH>(f, s, a.lvl, a.lvl);
         // canonical (and n^-1 for a standalone inverse), truncated to out_len
         const long long lin0 = a.col0 + cl0;
         uint64_t* ob = (uint64_t*)a.out + b * a.out_bs + cl0;
