@@ -471,7 +471,9 @@ __global__ void __launch_bounds__(CARRY_T) k_carry16_fused(const uint64_t* __res
         const long long j = jb + 16 * threadIdx.x + e;
         acc = gp_comb(acc, j < nout ? (g[e] | ((w[e] == 0xFFFFu ? 1u : 0u) << 1)) : 2u);
     }
-    {   // block aggregate
+    uint32_t C;
+    {   // block aggregate; every thread's exclusive prefix within the block is
+        // formed while warp 0 looks back (two barriers instead of four)
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         uint32_t x = acc;
         for (int o = 1; o < 32; o <<= 1) {
@@ -480,6 +482,11 @@ __global__ void __launch_bounds__(CARRY_T) k_carry16_fused(const uint64_t* __res
         }
         if (lane == 31) sh[wid] = x;
         __syncthreads();
+        uint32_t wpre = 2u;                                  // identity: G = 0, P = 1
+        for (int q = 0; q < wid; q++) wpre = gp_comb(wpre, sh[q]);
+        uint32_t excl_l = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) excl_l = 2u;
+        const uint32_t pre = gp_comb(wpre, excl_l);
         if (wid == 0) {
             // warp 0: publish the aggregate, then look back 32 predecessors at a
             // time (lane l reads block k - l) until an inclusive prefix appears
@@ -516,8 +523,8 @@ __global__ void __launch_bounds__(CARRY_T) k_carry16_fused(const uint64_t* __res
             }
         }
         __syncthreads();
+        C = (pre & 1) | ((pre >> 1) & s_cin);             // carry into this thread's first limb
     }
-    uint32_t C = block_carry_in(acc, s_cin, sh);
     const long long j0 = jb + 16 * threadIdx.x;
     uint32_t o[8];
 #pragma unroll
