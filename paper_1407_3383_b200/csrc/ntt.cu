@@ -2585,6 +2585,28 @@ static mm_status carry_run(const D& d, long long nout, uint32_t* agg, typename D
     const long long nblk = (nout + CARRY_B - 1) / CARRY_B;
     if constexpr (std::is_same<D, Dig16>::value) {   // shared-memory staged 16-bit limb path, one pass
         // agg holds 2 nblk + 2 words here: the look-back status words and the ticket
+        // reduce -> scan -> apply (the coefficients read twice) measured faster
+        // than the single-pass look-back once the staging loads were batched
+        // (C5 2.408 -> 2.389 ms: the look-back's chain of inclusive prefixes,
+        // not the second read, set the single pass's time); MMNTT_CARRY_FUSED=1
+        // selects the single pass
+        static const bool fused = getenv("MMNTT_CARRY_FUSED") != nullptr;
+        if (!fused) {
+            {
+                LaunchScope ls("carry_reduce", st);
+                k_carry16_reduce<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg);
+            }
+            {
+                LaunchScope ls("carry_scan", st);
+                k_carry_scan<<<1, 1024, 0, st>>>(agg, nblk);
+            }
+            {
+                LaunchScope ls("carry_apply", st);
+                k_carry16_apply<<<(int)nblk, CARRY_T, 0, st>>>(d.c, d.nc, nout, agg, out);
+            }
+            MM_LAUNCH_CHECK();
+            return MM_OK;
+        }
         unsigned long long* status = (unsigned long long*)agg;
         unsigned* ticket = (unsigned*)(status + nblk);
         MM_CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)nblk * 8 + 8, st));

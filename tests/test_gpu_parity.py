@@ -1278,10 +1278,12 @@ for t in (y, z, c):
 print(h.hexdigest(), bool(torch.equal(z, x)))
 """ % root
     outs = []
-    for v in ("1", "0"):
+    for v, fused in (("1", None), ("0", None), ("1", "1")):   # the last: the single-pass look-back carry
         env = dict(os.environ, MMNTT_GOLD_TMA=v)
+        if fused:
+            env["MMNTT_CARRY_FUSED"] = fused
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.split()[-2:])
-    assert outs[0][1] == "True" and outs[1][1] == "True"
-    assert outs[0][0] == outs[1][0]
+    assert all(o[1] == "True" for o in outs)
+    assert outs[0][0] == outs[1][0] == outs[2][0]
