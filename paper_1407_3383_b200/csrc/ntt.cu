@@ -269,10 +269,30 @@ __global__ void __launch_bounds__(CARRY_T) k_carry_reduce(D d, long long nout, u
     }
 }
 
-// sequential-in-chunks scan of block aggregates -> carry-in per block
+// scan of block aggregates -> carry-in per block.  Up to 16 aggregates per
+// thread: each thread combines its run of E consecutive ones, one block scan
+// gives the carry into every run, and the run is walked again (one pass of
+// barriers instead of one per 1024 aggregates); longer inputs go in chunks.
 __global__ void k_carry_scan(uint32_t* agg, long long nblk) {
     __shared__ uint32_t sh[64];
     __shared__ uint32_t carry;
+    if (nblk <= 16ll * blockDim.x) {
+        const int E = (int)((nblk + blockDim.x - 1) / blockDim.x);
+        const long long i0 = (long long)threadIdx.x * E;
+        uint32_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; e++) v[e] = (e < E && i0 + e < nblk) ? agg[i0 + e] : 2u;   // all loads in flight
+        uint32_t loc = 2u;                                   // identity: G = 0, P = 1
+#pragma unroll
+        for (int e = 0; e < 16; e++) loc = gp_comb(loc, v[e]);
+        uint32_t c = block_carry_in(loc, 0u, sh);            // carry into this run
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+            if (e < E && i0 + e < nblk) agg[i0 + e] = c;
+            c = (v[e] & 1) | ((v[e] >> 1) & c);
+        }
+        return;
+    }
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (long long base = 0; base < nblk; base += blockDim.x) {
