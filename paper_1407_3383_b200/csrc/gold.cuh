@@ -209,6 +209,12 @@ template <int S, int STEP, int R> __device__ __forceinline__ void rot(uint64_t v
 // bound of every intermediate; every subk<K> has its subtrahend < K p
 // (p > 2^63, so K p > 2^(63 + log2 K)).
 
+// DIF levels of span 2 and 1 of the 8-point kernel below (shared by dif8 and
+// dif8_zh): inputs s_i < 2^65, d0 < 2^66, d1..d3 < 2^64
+template <int S>
+__device__ __forceinline__ void dif8_l23(uint64_t v[8], const U3& s0, const U3& s1, const U3& s2, const U3& s3,
+                                         const U3& d0, uint64_t d1, uint64_t d2, uint64_t d3);
+
 // DIF, natural in, bit-reversed out (positions of the radix-2 network)
 template <int S> __device__ __forceinline__ void dif8(uint64_t v[8]) {
     typedef Pow2<8 * S> W1;
@@ -220,6 +226,26 @@ template <int S> __device__ __forceinline__ void dif8(uint64_t v[8]) {
     const uint64_t d1 = mul2k<W1::KR>(fold(W1::NEG ? subk<2>(v[5], v[1]) : subk<2>(v[1], v[5])));
     const uint64_t d2 = mul2k<W2::KR>(fold(W2::NEG ? subk<2>(v[6], v[2]) : subk<2>(v[2], v[6])));
     const uint64_t d3 = mul2k<W3::KR>(fold(W3::NEG ? subk<2>(v[7], v[3]) : subk<2>(v[3], v[7])));
+    dif8_l23<S>(v, s0, s1, s2, s3, d0, d1, d2, d3);
+}
+
+// the same with v[4..7] = 0 (the upper half of a zero-padded column): the
+// span-4 level is v_i, v_i w_8^i -- no sums, differences or folds (the
+// generic kernel cannot see through its inline-PTX carry chains)
+template <int S> __device__ __forceinline__ void dif8_zh(uint64_t v[8]) {
+    typedef Pow2<8 * S> W1;
+    typedef Pow2<16 * S> W2;
+    typedef Pow2<24 * S> W3;
+    const uint64_t d1 = mul2k<W1::KR>(W1::NEG ? neg(v[1]) : v[1]);
+    const uint64_t d2 = mul2k<W2::KR>(W2::NEG ? neg(v[2]) : v[2]);
+    const uint64_t d3 = mul2k<W3::KR>(W3::NEG ? neg(v[3]) : v[3]);
+    dif8_l23<S>(v, mk(v[0]), mk(v[1]), mk(v[2]), mk(v[3]), mk(v[0]), d1, d2, d3);
+}
+
+template <int S>
+__device__ __forceinline__ void dif8_l23(uint64_t v[8], const U3& s0, const U3& s1, const U3& s2, const U3& s3,
+                                         const U3& d0, uint64_t d1, uint64_t d2, uint64_t d3) {
+    typedef Pow2<16 * S> W2;
     // level span 2 (twiddles 1, w_4)
     const U3 a0 = add(s0, s2);                                                        // < 2^66
     const U3 a2 = subk<4>(s0, s2);                                                    // < 2^67

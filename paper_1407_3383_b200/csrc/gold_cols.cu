@@ -368,13 +368,15 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols16_fwd(const __grid_constant__ 
                 for (int q = threadIdx.x; q < C * 512; q += NTH) {
                     const int c = q % C, b6 = (q / C) & 63, al = q / (64 * C);
                     const int j0 = 64 * al + b6;
+                    static_assert(RMAX / 512 == 4, "rows >= 2048 (t >= 4) are zero padding");
                     uint64_t v[8];
 #pragma unroll
                     for (int t = 0; t < 8; t++) {
                         const int row = j0 + 512 * t;
-                        v[t] = (t < RMAX / 512 && row < nrows) ? land[row * SUPER + sub * C + c] : 0ull;
+                        v[t] = (t < 4 && row < nrows) ? land[row * SUPER + sub * C + c] : 0ull;
                     }
-                    gold::dif_a<8, gold::S_FWD>(v, al);
+                    gold::dif8_zh<gold::S_FWD>(v);      // the zero upper half skips the span-4 level
+                    gold::rot<gold::S_FWD, 1, 8>(v, al);
 #pragma unroll
                     for (int t = 0; t < 8; t++) s[Lay::addr(c, j0 + 512 * t)] = v[t];
                 }
