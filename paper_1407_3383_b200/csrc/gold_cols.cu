@@ -411,6 +411,14 @@ __global__ void __launch_bounds__(NTH, 1) k_gcols16_fwd(const __grid_constant__ 
 }  // namespace g16
 }  // namespace gcols
 
+bool gold_tma_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MMNTT_GOLD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on && tma_encoder() != nullptr;
+}
+
 bool gold_cols_tma_ok(const ColArgs<FpG>& a) {
     static const bool on = [] {
         const char* e = getenv("MMNTT_GOLD_TMA");

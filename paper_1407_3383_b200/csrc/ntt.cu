@@ -1529,7 +1529,10 @@ static mm_status fwd_impl(mm_ntt_plan* P, const void* in, void* out, mm_order or
     // 64-bit four-step batches run as sub-batches on the fork streams (the
     // latency-bound column pass of one overlaps the row pass of the other:
     // C4 3.25 -> 3.04 ms on B200, tools/exp_streams2.py)
-    if (sizeof(T) == 8) return forked((const T*)in, (T*)out, (long long)P->batch, n, st, four_step);
+    // (not when both passes are the whole-SM TMA / bulk-copy Goldilocks kernels,
+    // which cannot share an SM: C4 forward 2.76 forked vs 2.73 ms one stream)
+    const bool whole_sm = std::is_same<F, FpG>::value && P->k1 == 13 && P->k2 == 11 && gold_tma_enabled();
+    if (sizeof(T) == 8 && !whole_sm) return forked((const T*)in, (T*)out, (long long)P->batch, n, st, four_step);
     return four_step(in, out, (long long)P->batch, st);
 }
 

@@ -162,6 +162,7 @@ template <class F> struct ColArgs {
 // Goldilocks forward column pass of 2^11-point columns with TMA-staged tiles
 // and step-2 twiddles (gold_cols.cu); taken by launch_cols_e when
 // gold_cols_tma_ok (full-length input, one modulus; peer scatter included)
+bool gold_tma_enabled();   // MMNTT_GOLD_TMA not 0 and the tensor-map encoder available
 bool gold_cols_tma_ok(const ColArgs<FpG>& a);
 mm_status launch_gold_cols_tma(const FpG& f, const ColArgs<FpG>& a, cudaStream_t st);
 // the same for 2^12-point columns of zero-padded 16-bit limbs (C5, gold_cols.cu)
