@@ -706,9 +706,10 @@ def test_int_matmul_u32(mm, O, m, kk, n, na, nb):
     assert all(_to_int32(C[i, j]) == ref for i in range(m) for j in range(n))
 
 
-@pytest.mark.parametrize("N", [1, 2, 4097, 1 << 16])
+@pytest.mark.parametrize("N", [1, 2, 4097, 1 << 16, 1 << 20])
 def test_int_mul_u32_all_ones(mm, O, N):
-    # (2^(32N) - 1)^2: every coefficient at its maximum N (2^32 - 1)^2 (closed form)
+    # (2^(32N) - 1)^2: every coefficient at its maximum N (2^32 - 1)^2 (closed form);
+    # N = 2^20: Table 16's size, raw limbs reduced in the TMA column loader
     a = np.full(N, 0xFFFFFFFF, dtype=np.uint32)
     c = host(mm.int_mul_u32(dev(a), dev(a)))
     ref = np.zeros(2 * N, dtype=np.uint32)
