@@ -378,6 +378,16 @@ def extras_run(mm, torch, dev, peaks):
     out = {}
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
 
+    def with_clocks(fn):
+        # the SM clock (median of NVML samples) and throttle reasons while fn runs
+        cs = ClockSampler(dev.index or 0).__enter__()
+        cs.mark(True)
+        r = fn()
+        cs.mark(False)
+        cs.__exit__(None, None, None)
+        sm = cs.summary()
+        return r, {"sm_mhz": sm.get("sm_mhz"), "reasons": sm.get("reasons"), "samples": sm.get("samples")}
+
     def tloop(fn, reps, warm=3):
         for _ in range(warm):
             fn()
@@ -591,7 +601,7 @@ def extras_run(mm, torch, dev, peaks):
     x4 = gen.residues_torch(gen.config_seed(4), 1, 8 << 24, PG, dev).view(torch.uint64)
     y4 = torch.empty_like(x4)
     f4 = lambda: plan4.forward(x4, out=y4, order=mm.BITREV)
-    ms = tloop(f4, 10)
+    ms, ck4 = with_clocks(lambda: tloop(f4, 10))
     bfly = 8 * (1 << 23) * 24
     gbs2 = 8 * (1 << 24) * 32 / (ms * 1e-3) / 1e9
     inf4 = plan4.info()
@@ -600,7 +610,8 @@ def extras_run(mm, torch, dev, peaks):
                                        "split": f"{inf4['n2']} cols x {inf4['n1']} rows", "kernels_ms": kern_ms(f4),
                                        "alu_frac_vs_gold8_probe": round(bfly / (ms * 1e-3) / bg8, 3),
                                        "alu_note": "achieved butterflies / register-resident gold.cuh 8-point rate "
-                                                   "(the passes also carry the w_L and step-2 table products)"}
+                                                   "(the passes also carry the w_L and step-2 table products)",
+                                       "clocks": ck4}
     del x4, y4, plan4
 
     # C5: 2^28-bit x 2^28-bit integer product (2^24 16-bit limbs each)
@@ -609,10 +620,10 @@ def extras_run(mm, torch, dev, peaks):
     ib = gen.limbs16_torch(gen.config_seed(5), 2, na, dev).view(torch.uint16)
     ic = torch.empty(2 * na, dtype=torch.uint16, device=dev)
     f5 = lambda: mm.int_mul_u16(ia, ib, out=ic)
-    ms = tloop(f5, 10)
+    ms, ck5 = with_clocks(lambda: tloop(f5, 10))
     out["C5_int_mul_2^28bit"] = {"ms": round(ms, 3), "Mbit_per_s": round(2 * (1 << 28) / (ms * 1e-3) / 1e6, 1),
                                  "Gbutterfly_per_s": round(3 * (1 << 24) * 25 / (ms * 1e-3) / 1e9, 1),
-                                 "kernels_ms": kern_ms(f5)}
+                                 "kernels_ms": kern_ms(f5), "clocks": ck5}
     # polynomial matrix product (Table 15: n x n, d < 2^15 over 469762049)
     pm = {}
     for N in (8, 32):
