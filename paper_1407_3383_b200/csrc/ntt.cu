@@ -2723,7 +2723,6 @@ extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t
     uint32_t* R = (uint32_t*)ws;          // R[i * rs + j]: a_j mod p_i (j < na), b at offset na
     uint32_t* Cp = R + 3 * rs;            // Cp[i * lc + k]: c_k mod p_i
     uint32_t* Wd = Cp + 3 * lc;           // 96-bit coefficients
-    uint32_t* agg = Wd + 3 * lc;
     mm_ntt_plan* PL[3];
     for (int i = 0; i < 3; i++) {
         uint64_t omega = hpowmod(GEN[i], (PR[i] - 1) >> k, PR[i]);
@@ -2733,7 +2732,6 @@ extern "C" mm_status mm_int_mul_u32(const uint32_t* a, size_t na, const uint32_t
     if ((s = product3_impl(PL, a, b, K, R, (long long)rs, (long long)na, (long long)nb, Cp, (long long)lc, st)) != MM_OK)
         return s;
     // Garner CRT and carries in one pass (crt_carry32); Wd is its look-back scratch
-    (void)agg;
     return crt_carry32(Cp, (long long)lc, (long long)lc, (long long)nout, (long long)nout,
                        (unsigned long long*)(((uintptr_t)Wd + 7) & ~(uintptr_t)7), c, st);
 }
@@ -3000,7 +2998,6 @@ extern "C" mm_status mm_int_matmul_u32(const uint32_t* A, const uint32_t* B, uin
     uint32_t* RB = RA + 3 * sa;             // [3][sb]
     uint32_t* RC = RB + 3 * sb;             // [3][sc]
     uint32_t* Wd = RC + 3 * sc;             // [sc][3]
-    uint32_t* agg = Wd + 3 * sc;
     const int grid = num_sms() * 8;
     {
         LaunchScope ls("crt_residues", st);
@@ -3011,7 +3008,6 @@ extern "C" mm_status mm_int_matmul_u32(const uint32_t* A, const uint32_t* B, uin
     for (int i = 0; i < 3; i++)
         if ((s = mm_poly_matmul(PR[i], GEN[i], RA + i * sa, RB + i * sb, RC + i * sc, m, kk, n, na, nb, stream)) != MM_OK)
             return s;
-    (void)agg;
     return crt_carry32(RC, (long long)sc, (long long)lc, (long long)nout, (long long)nall,
                        (unsigned long long*)(((uintptr_t)Wd + 7) & ~(uintptr_t)7), C, st);
 }

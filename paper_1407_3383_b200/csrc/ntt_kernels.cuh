@@ -826,8 +826,8 @@ __global__ void __launch_bounds__(NT, 3) k_cols_tma(const __grid_constant__ CUte
     typedef typename Vec<T>::type TV;
     typedef Epi<F, EPIV> E;
     constexpr int L = K::L, C = K::C, V = Vec<T>::N, CV = C / V, TOT = L * CV;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    T* land = (T*)smem_raw;
+    extern __shared__ __align__(1024) unsigned char smem_tma[];   // own name: the 16-byte smem_raw of the other kernels would override the alignment
+    T* land = (T*)smem_tma;
     T* s = land + L * C;
     W* tws = (W*)(s + Lay::ELEMS);
     uint64_t* bar = (uint64_t*)(tws + (K::TWS ? L : 0));

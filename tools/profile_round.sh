@@ -21,7 +21,7 @@ ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_grows
     -o gpurun_out/${R}_full_c4 python tools/prof_run.py c4 > gpurun_out/${R}_ncu_full_c4.log 2>&1
 echo full_c4_rc=$?
 python tools/prof_run.py c5 > gpurun_out/${R}_plain_c5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_gpmul|k_cols|k_rows|k_carry" -s 5 -c 5 \
+ncu --set full --clock-control none --import-source on -k "regex:k_gcols|k_gpmul|k_cols|k_rows|k_carry" -s 7 -c 7 \
     -o gpurun_out/${R}_full_c5 python tools/prof_run.py c5 > gpurun_out/${R}_ncu_full_c5.log 2>&1
 echo full_c5_rc=$?
 python tools/ncu_summary.py launches gpurun_out/${R}_launches.csv gpurun_out/${R}_launches_summary.txt > /dev/null
