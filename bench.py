@@ -974,6 +974,312 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- other BASELINE configs (--config)
+# `--config c1|c2|c4|c5` prints the contract line of that BASELINE config
+# instead of C3's: the same timing rules (W >= 3 untimed steps, K steps on the
+# device, max over ranks, clocks sampled during the timed region), an e2e leg
+# through the public API with the step's inputs uploaded from pinned host
+# memory and its result read back inside the timed region, the dominant
+# kernel's roofline from a serialised per-launch pass, and the oracle on the
+# host cores.  Weak scaling at N > 1: every rank runs its own copy of the
+# config's work on its own generator range (the partitioned C4 / C5 forms are
+# the N > 1 extras of the default run).
+def timed_flush(fn, steps, warmup, world, flush, on_start=None, on_stop=None):
+    """timed() for configs whose inputs fit in L2 (C1, C5): a write larger than
+    L2 before every timed step, outside that step's event pair; the K
+    per-step durations are summed."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    evs = []
+    if on_start:
+        on_start()
+    for _ in range(steps):
+        flush.add_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        fn()
+        e1.record(st)
+        evs.append((e0, e1))
+    if on_stop:
+        on_stop()
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(world, sum(a.elapsed_time(b) for a, b in evs))
+
+
+def oracle_c1(nthreads: int, budget_s: float = 3.0) -> dict:
+    """C1 on the oracle: 16 forward + inverse NTTs of 2^10 and one product of two
+    degree-511 polynomials per unit; units spread over the threads."""
+    import gen
+    import oracle as O
+    O.build()
+    w = O.root_of_unity(G30, 10, P30)
+    x = gen.residues(gen.config_seed(1), 1, 16 << 10, P30).reshape(16, 1 << 10)
+    a = gen.residues(gen.config_seed(1), 2, 512, P30)
+    b = gen.residues(gen.config_seed(1), 3, 512, P30)
+
+    def unit(t, i):
+        O.intt_rows(O.ntt_rows(x, w, P30), w, P30)
+        O.poly_mul_ntt(a, b, P30, G30)
+    t0 = time.perf_counter()
+    unit(0, 0)
+    quota = max(1, int(budget_s / max(time.perf_counter() - t0, 1e-4)))
+    wall = _parallel(unit, nthreads, quota)
+    units = nthreads * quota
+    return {"value": round(units * C1_BFLY / wall / 1e9, 6), "unit": "Gbutterfly/s", "cores": nthreads,
+            "units": units, "wall_s": round(wall, 2)}
+
+
+C1_BFLY = 16 * 2 * (1 << 9) * 10 + 3 * (1 << 9) * 10   # 16 round trips of 2^10 + one 1024-point product
+
+
+def config_spec(which, mm, torch, dev, rank):
+    """Device inputs, the step, its host-side (e2e) form and the per-launch
+    algorithmic work of each kernel family for one BASELINE config."""
+    import gen
+    s = {}
+    if which == "c1":
+        w10 = root_of_unity(P30, G30, 10)
+        plan = mm.NttPlan(32, P30, 10, w10, 16)
+        x = gen.residues_torch(gen.config_seed(1), 1, 16 << 10, P30, dev, start=rank << 14).view(torch.uint32)
+        x = x.reshape(16, 1 << 10)
+        a = gen.residues_torch(gen.config_seed(1), 2, 512, P30, dev, start=rank << 9).view(torch.uint32)
+        b = gen.residues_torch(gen.config_seed(1), 3, 512, P30, dev, start=rank << 9).view(torch.uint32)
+        y, z = torch.empty_like(x), torch.empty_like(x)
+        c = torch.empty(1023, dtype=torch.uint32, device=dev)
+        jobs = mm.Jobs()
+        for r in range(16):
+            jobs.roundtrip(plan, x[r], z[r], out=y[r], order=mm.NATURAL)
+        jobs.poly_mul(a, b, P30, G30, c)
+        s.update(step=jobs.run, inputs=[x, a, b], outputs=[y, z, c], units=C1_BFLY, unit="Gbutterfly/s",
+                 metric="NTT Gbutterfly/s", scale=1e9, dtype="u32", flush=True, keep=(plan, jobs),
+                 workload="C1: 16 independent forward + inverse NTTs of 2^10 (NATURAL order) and one product of two "
+                          "degree-511 polynomials, p = 998244353, ONE launch (mm_run_jobs)",
+                 fam={"jobs": (4 * (3 * 16 * 1024 + 2 * 512 + 1023), C1_BFLY)}, peak="alu32")
+    elif which == "c2":
+        n = 1 << 28
+        x = gen.residues_torch(gen.config_seed(2), 1, n, P32, dev, start=rank * n).view(torch.uint32)
+        y = gen.residues_torch(gen.config_seed(2), 2, n, P32, dev, start=rank * n).view(torch.uint32)
+        z = torch.empty_like(x)
+        M = mm.Mod32(P32)
+        s.update(step=lambda: M.mul(x, y, mm.MUL_MONTGOMERY, out=z), inputs=[x, y], outputs=[z], units=n,
+                 unit="Gelem/s", metric="modmul Gelem/s", scale=1e9, dtype="u32", flush=False, keep=(M,),
+                 workload="C2: Montgomery modmul over 2^28 uint32 pairs, p = 3221225473 (Shoup, Barrett, add, sub "
+                          "in config.variants)",
+                 fam={"modmul_montgomery": (12 * n, 0)}, peak="hbm")
+        ys = M.shoup_precompute(y)
+        s["variants"] = [("modadd", lambda: M.add(x, y, out=z), 12), ("modsub", lambda: M.sub(x, y, out=z), 12),
+                         ("modmul_barrett", lambda: M.mul(x, y, mm.MUL_BARRETT, out=z), 12),
+                         ("modmul_shoup", lambda: M.mul(x, y, mm.MUL_SHOUP, y_shoup=ys, out=z), 16),
+                         ("shoup_precompute", lambda: M.shoup_precompute(y, out=z), 8)]
+        s["keep"] = (M, ys)
+    elif which == "c4":
+        plan = mm.NttPlan(64, PG, 24, root_of_unity(PG, 7, 24), 8)
+        x = gen.residues_torch(gen.config_seed(4), 1, 8 << 24, PG, dev, start=rank << 27).view(torch.uint64)
+        y = torch.empty_like(x)
+        bf = 8 * (1 << 23) * 24
+        inf = plan.info()
+        kc, kr = 11, 13          # 2^11-point column tiles, 2^13-point rows (DESIGN.md §6)
+        s.update(step=lambda: plan.forward(x, out=y, order=mm.BITREV), inputs=[x], outputs=[y], units=bf,
+                 unit="Gbutterfly/s", metric="NTT Gbutterfly/s", scale=1e9, dtype="u64", flush=False, keep=(plan,),
+                 workload=f"C4: 8 forward NTTs of 2^24 over p = 2^64 - 2^32 + 1 (generator 7), four-step "
+                          f"({inf['n2']} cols x {inf['n1']} rows), BITREV output",
+                 fam={"ntt_cols_fwd": (2 * 8 * 8 << 24, 8 * (1 << 23) * kc),
+                      "ntt_rows_fwd": (2 * 8 * 8 << 24, 8 * (1 << 23) * kr)}, peak="gold8")
+    elif which == "c5":
+        n = 1 << 24
+        a = gen.limbs16_torch(gen.config_seed(5), 1, n, dev, start=rank * n).view(torch.uint16)
+        b = gen.limbs16_torch(gen.config_seed(5), 2, n, dev, start=rank * n).view(torch.uint16)
+        c = torch.empty(2 * n, dtype=torch.uint16, device=dev)
+        N = 1 << 25
+        s.update(step=lambda: mm.int_mul_u16(a, b, out=c), inputs=[a, b], outputs=[c], units=2 * 16 * n,
+                 unit="Mbit/s", metric="int_mul Mbit/s", scale=1e6, dtype="u64", flush=True, keep=(),
+                 workload="C5: product of two 2^28-bit integers (2^24 16-bit limbs each), length-2^25 convolution "
+                          "over p = 2^64 - 2^32 + 1 (four-step 2^13 x 2^12), carries to 16-bit limbs",
+                 fam={"ntt_cols_fwd": (2 * (2 * n + 8 * N), 2 * (1 << 24) * 12),
+                      "pmul_rows_fourstep": (3 * 8 * N, 3 * (1 << 24) * 13),
+                      "ntt_cols_inv": (2 * 8 * N, (1 << 24) * 12)}, peak="gold8")
+    else:
+        raise SystemExit(f"unknown --config {which}")
+    return s
+
+
+def run_config(args, world, rank, local):
+    import torch
+    import paper_1407_3383_b200 as mm
+
+    which = args.config
+    mm.lib()
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json)" if hbm_peak else "fallback (B200_PROFILING.md)"
+    hbm_peak = hbm_peak or HBM_FALLBACK_GBS
+    sm_mhz_max = peaks.get("sm_max_mhz", 1965.0)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    S = config_spec(which, mm, torch, dev, rank)
+    step = S["step"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if S["flush"] else None
+    step()
+    torch.cuda.synchronize()
+    cnt = {}
+    clk = ClockSampler(local).__enter__()
+    time.sleep(0.05)
+    on_start = lambda: (cnt.__setitem__("n0", mm.launch_count()), clk.mark(True))
+    on_stop = lambda: cnt.__setitem__("n1", mm.launch_count())
+    if flush is not None:
+        ms_total = timed_flush(step, args.steps, args.warmup, world, flush, on_start, on_stop)
+    else:
+        ms_total = timed(step, args.steps, args.warmup, world, on_start=on_start, on_stop=on_stop)
+    clk.mark(False)
+    ms_step = ms_total / args.steps
+    value = world * S["units"] / (ms_step * 1e-3) / S["scale"]
+
+    # serialised per-launch pass (one stream; events on the launching stream)
+    mm.set_product_streams(1)
+    mm.prof_collect()
+    mm.prof_enable(True)
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.add_(1)
+        step()
+    torch.cuda.synchronize()
+    mm.prof_enable(False)
+    prof = mm.prof_collect()
+    mm.set_product_streams(2)
+    ms_serial = sum(v[1] for v in prof.values()) / args.steps
+    alu32 = nsm * 16 * sm_mhz_max * 1e6
+    gold8 = None
+    if S["peak"] == "gold8":   # first call loads the probe module: warm up, keep the best of three
+        mm.probe_butterfly(65, 200)
+        gold8 = max(mm.probe_butterfly(65, 1000) for _ in range(3))
+    kernels, roof = {}, None
+    for k_, (n_, tot) in prof.items():
+        per = tot / n_
+        e = {"launches": n_, "avg_ms": round(per, 4), "share": round(tot / max(ms_serial * args.steps, 1e-9), 3)}
+        if k_ in S["fam"]:
+            by, bf = S["fam"][k_]
+            lps = n_ / args.steps                     # launches per step
+            by, bf = by / lps, bf / lps
+            e["GB_per_s"] = round(by / (per * 1e-3) / 1e9, 1)
+            e["hbm_frac"] = round(by / (per * 1e-3) / 1e9 / hbm_peak, 3)
+            if bf:
+                e["Gbutterfly_per_s"] = round(bf / (per * 1e-3) / 1e9, 1)
+        kernels[k_] = e
+    fam = max((k for k in prof if k in S["fam"]), key=lambda k: prof[k][1], default=None)
+    if fam is not None:
+        e = kernels[fam]
+        if S["peak"] == "hbm":
+            roof = {"bound": "hbm", "kernel": fam, "achieved": e["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
+                    "frac": e["hbm_frac"], "traffic": None, "peak_source": peak_src}
+        else:
+            pk = alu32 if S["peak"] == "alu32" else gold8
+            src = (f"derived: {nsm} SMs x 16 butterflies/clk/SM (fmaheavy: IMAD.HI 4 + 2 x IMAD 2 cycles per warp) "
+                   f"x {sm_mhz_max:.0f} MHz" if S["peak"] == "alu32" else
+                   "measured on this GPU: register-resident gold.cuh 8-point Goldilocks DIF rate (mm_probe_butterfly "
+                   "65; no loads, shift twiddles only: an upper bound the passes' table products cannot reach)")
+            ach = e["Gbutterfly_per_s"] * 1e9
+            roof = {"bound": "alu", "kernel": fam, "achieved": e["Gbutterfly_per_s"], "peak": round(pk / 1e9, 1),
+                    "unit": "Gbutterfly/s", "frac": round(ach / pk, 3), "traffic": None, "hbm_frac": e["hbm_frac"],
+                    "peak_source": src}
+
+    # e2e: upload the step's inputs from pinned host memory, run, read the result back
+    hin = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in S["inputs"]]
+    hout = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in S["outputs"]]
+
+    def e2e_step():
+        for h, d in zip(hin, S["inputs"]):
+            d.copy_(h, non_blocking=True)
+        step()
+        for h, d in zip(hout, S["outputs"]):
+            h.copy_(d, non_blocking=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    ms_e2e = timed(e2e_step, e2e_steps, 1, world) / e2e_steps
+    h2d = sum(t.numel() * t.element_size() for t in S["inputs"])
+    d2h = sum(t.numel() * t.element_size() for t in S["outputs"])
+    variants = {}
+    for nm, fn, bpe in S.get("variants", []):
+        msv = timed(fn, args.steps, args.warmup, world) / args.steps
+        gbs = S["units"] * bpe / (msv * 1e-3) / 1e9
+        variants[nm] = {"Gelem_per_s": round(S["units"] / (msv * 1e-3) / 1e9, 1), "ms": round(msv, 4),
+                        "hbm_frac": round(gbs / hbm_peak, 3)}
+    time.sleep(0.02)
+    clk.__exit__(None, None, None)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_config(which, args.cpu_seconds)
+    if rank != 0:
+        return
+    cfg = {"workload": S["workload"], "config": which.upper(),
+           "l2": "L2 flushed (256 MiB write) before every timed step, outside its events" if S["flush"]
+           else "inputs > 126 MB L2 (no flush needed)",
+           "parallelism": f"dp{world} (each rank its own copy of the config's work, no collective)"}
+    if variants:
+        cfg["variants"] = variants
+    line = {
+        "metric": S["metric"], "value": round(value, 2), "unit": S["unit"], "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": S["dtype"],
+        "data": "synthetic (seeded counter-based SplitMix64, uniform, generated in HBM)", "config": cfg,
+        "e2e": {"value": round(world * S["units"] / (ms_e2e * 1e-3) / S["scale"], 2), "unit": S["unit"],
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": int(cnt["n1"] - cnt["n0"]), "roofline": roof, "kernels": kernels,
+        "clocks": clk.summary(), "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_config(which: str, budget_s: float) -> dict:
+    ci = cpu_info()
+    allc = ci["cores"]
+    fn = {"c1": lambda t: oracle_c1(t, budget_s / 2), "c2": oracle_c2,
+          "c4": lambda t: oracle_c4(min(t, 8)), "c5": oracle_c5}[which]
+    one, many = fn(1), fn(allc)
+    return {"value": many["value"], "unit": many["unit"], "cores": many["cores"], "kind": "oracle",
+            "cpu_model": ci["model"], "sample": {k: v for k, v in many.items() if k not in ("value", "unit")},
+            "single_thread": one, "all_cores": many}
+
+
+def run_reference_config(args, rank):
+    """--impl reference --config cX: the oracle on the host cores, one bounded
+    sample of the config's work per step."""
+    if rank != 0:
+        return
+    ci = cpu_info()
+    nth = ci["cores"]
+    fn = {"c1": lambda: oracle_c1(nth, 2.0), "c2": lambda: oracle_c2(nth),
+          "c4": lambda: oracle_c4(min(nth, 8), k=22), "c5": lambda: oracle_c5(nth, limbs=1 << 18)}[args.config]
+    for _ in range(args.warmup):
+        fn()
+    vals, walls, samp = [], [], None
+    for _ in range(args.steps):
+        r = fn()
+        vals.append(r["value"])
+        walls.append(r["wall_s"])
+        samp = {k: v for k, v in r.items() if k not in ("value", "unit")}
+    val = statistics.mean(vals)
+    unit = r["unit"]
+    line = {
+        "impl": "reference", "metric": {"c1": "NTT Gbutterfly/s", "c2": "modmul Gelem/s", "c4": "NTT Gbutterfly/s",
+                                        "c5": "int_mul Mbit/s"}[args.config],
+        "value": round(val, 6), "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.mean(walls), 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64" if args.config in ("c4", "c5") else "u32",
+        "data": "synthetic (seeded SplitMix64)",
+        "config": {"workload": f"{args.config.upper()} oracle sample per step: {samp}", "config": args.config.upper(),
+                   "parallelism": f"{nth} CPU threads"},
+        "cpu_baseline": {"value": round(val, 6), "unit": unit, "cores": samp.get("cores", nth), "kind": "oracle",
+                         "cpu_model": ci["model"], "sample": samp},
+        "e2e": {"value": round(val, 6), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -984,13 +1290,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=6.0)
     ap.add_argument("--cpu-legs", default="c2,c4,c5", help="other configs timed on the oracle beside C3")
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE config of the printed line (default: the C3 headline with the others in extra)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
-        run_reference(args, world, rank)
+        if args.config != "c3":
+            run_reference_config(args, rank)
+        else:
+            run_reference(args, world, rank)
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched without torchrun: start N ranks ourselves (one per GPU)
@@ -1013,7 +1324,10 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE = {world}")
     try:
-        run_ours(args, world, rank, local)
+        if args.config != "c3":
+            run_config(args, world, rank, local)
+        else:
+            run_ours(args, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist

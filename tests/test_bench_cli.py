@@ -31,3 +31,22 @@ def test_gpus_n_without_devices_fails_loudly():
                          capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode != 0
     assert "CUDA devices visible" in (out.stderr + out.stdout)
+
+
+def test_reference_arm_per_config():
+    # --config selects the BASELINE config of the line; the reference arm times
+    # the oracle on a bounded sample of that config's work
+    for cfg, metric in (("c1", "NTT Gbutterfly/s"), ("c2", "modmul Gelem/s")):
+        out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", cfg, "--steps", "1",
+                              "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+        assert line["impl"] == "reference" and line["metric"] == metric and line["value"] > 0
+        assert line["config"]["config"] == cfg.upper()
+        assert line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_unknown_config_rejected():
+    out = subprocess.run([sys.executable, "bench.py", "--config", "c9"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode != 0 and "invalid choice" in out.stderr
