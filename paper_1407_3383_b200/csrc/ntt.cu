@@ -2443,11 +2443,15 @@ extern "C" mm_status mm_poly_mul(int word_bits, uint64_t p, uint64_t g, const vo
 // Three device slots; H2D and D2H on their own streams, the products on the
 // caller's stream, events between them, so chunk i+1 uploads and chunk i-1
 // downloads while chunk i computes.  Device output rows use a 128-byte
-// leading dimension; the D2H copy packs them (cudaMemcpy2DAsync).
+// leading dimension; the D2H copy packs them (cudaMemcpy2DAsync).  Measured
+// (tools/time_e2e.py, r12): 25.4-29.2 ms per C3 step for chunk sizes 48-128
+// MiB, packed or aligned rows, with run-to-run spread larger than any
+// setting's effect, against a 21.6 ms concurrent copy floor (pcie_probe).
 struct HostPipe {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t in[3], done[3], freed[3];
     bool used[3] = {false, false, false};
+    int next = 0;            // slot of the next chunk: the rotation continues across calls
     void* buf = nullptr;
     size_t bytes = 0;
     std::mutex mu;
@@ -2482,9 +2486,14 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     if (la == 0 || lb == 0 || batch == 0) return set_err(MM_E_ARG, "empty operands");
     if (word_bits != 32 && word_bits != 64 && word_bits != 52) return set_err(MM_E_ARG, "word_bits must be 32, 64 or 52");
     const size_t es = esize(word_bits), lc = la + lb - 1;
-    const size_t q = 128 / es, ldc = (lc + q - 1) / q * q;
+    // MMNTT_HOST_PACKED=1: device output rows packed at lc (one 1-D download per
+    // chunk) instead of 128-byte aligned rows (2-D download); MMNTT_HOST_CHUNK_MIB:
+    // device traffic per chunk (default 96)
+    static const bool packed = getenv("MMNTT_HOST_PACKED") && atoi(getenv("MMNTT_HOST_PACKED")) != 0;
+    static const size_t chunk_mib = getenv("MMNTT_HOST_CHUNK_MIB") ? (size_t)atoi(getenv("MMNTT_HOST_CHUNK_MIB")) : 96;
+    const size_t q = 128 / es, ldc = packed ? lc : (lc + q - 1) / q * q;
     const size_t per = (la + lb + ldc) * es;
-    size_t ch = ((size_t)96 << 20) / per;               // ~96 MiB of device traffic per chunk
+    size_t ch = ((chunk_mib ? chunk_mib : 96) << 20) / per;   // device traffic per chunk
     if (ch < 1) ch = 1;
     if (ch > batch) ch = batch;
     HostPipe* H = nullptr;
@@ -2501,11 +2510,14 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
         MM_CUDA_TRY(cudaMalloc(&H->buf, 3 * slot_bytes));
         H->bytes = 3 * slot_bytes;
         for (int i = 0; i < 3; i++) H->used[i] = false;
+        H->next = 0;
     }
     const size_t nch = (batch + ch - 1) / ch;
     int last = 0;
     for (size_t i = 0; i < nch; i++) {
-        const int k = (int)(i % 3);
+        // slots rotate across calls too, so the next call's first upload waits
+        // for the download of this call's third-to-last chunk, not its last
+        const int k = (int)((H->next + i) % 3);
         const size_t r0 = i * ch, rows = batch - r0 < ch ? batch - r0 : ch;
         char* base = (char*)H->buf + k * slot_bytes;
         char* da = base;
@@ -2519,12 +2531,16 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
         if ((s = mm_poly_mul_ld(word_bits, p, g, da, la, la, db, lb, lb, dc, ldc, rows, stream)) != MM_OK) return s;
         MM_CUDA_TRY(cudaEventRecord(H->done[k], st));
         MM_CUDA_TRY(cudaStreamWaitEvent(H->d2h, H->done[k], 0));
-        MM_CUDA_TRY(cudaMemcpy2DAsync((char*)c + r0 * lc * es, lc * es, dc, ldc * es, lc * es, rows,
-                                      cudaMemcpyDeviceToHost, H->d2h));
+        if (ldc == lc)
+            MM_CUDA_TRY(cudaMemcpyAsync((char*)c + r0 * lc * es, dc, rows * lc * es, cudaMemcpyDeviceToHost, H->d2h));
+        else
+            MM_CUDA_TRY(cudaMemcpy2DAsync((char*)c + r0 * lc * es, lc * es, dc, ldc * es, lc * es, rows,
+                                          cudaMemcpyDeviceToHost, H->d2h));
         MM_CUDA_TRY(cudaEventRecord(H->freed[k], H->d2h));
         H->used[k] = true;
         last = k;
     }
+    H->next = (int)((H->next + nch) % 3);
     // the caller's stream is ordered after the last download
     MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
     return MM_OK;

@@ -570,6 +570,26 @@ def test_poly_mul_host_pipeline(mm, O):
         assert np.array_equal(u64(c[r].numpy()), O.poly_mul_schoolbook(a[r], b[r], PG)), r
 
 
+def test_poly_mul_host_back_to_back(mm, O):
+    # consecutive calls of 2, 1, 4 and 3 chunks: the slot rotation continues
+    # across calls (a call's first upload takes the slot after the previous
+    # call's last one); every result checked
+    p, g, d = P30, 3, 1 << 15
+    outs = []
+    for i, B in enumerate((300, 100, 700, 450)):
+        a = torch.from_numpy(residues(40 + i, 1, B * d, p).reshape(B, d)).pin_memory()
+        b = torch.from_numpy(residues(40 + i, 2, B * d, p).reshape(B, d)).pin_memory()
+        c = torch.empty((B, 2 * d - 1), dtype=torch.uint32).pin_memory()
+        mm.poly_mul_host(a, b, p, g, out=c)
+        outs.append((a, b, c))
+    torch.cuda.synchronize()
+    for a, b, c in outs:
+        assert torch.equal(c, mm.poly_mul(a.to(DEV), b.to(DEV), p, g).cpu())
+    a, b, c = outs[2]
+    for r in (0, 191, 192, 699):
+        assert np.array_equal(u64(c[r].numpy()), O.poly_mul_ntt(a[r].numpy(), b[r].numpy(), p, g)), r
+
+
 @pytest.mark.parametrize("p,g", [(P30, 3), (469762049, 3)])
 def test_poly_mul_tft(mm, O, p, g):
     # Algorithm 1 with l < n (truncated rows) + inverse column TFT: products of

@@ -17,9 +17,10 @@ if len(sys.argv) > 1:
     e0.record()
     for _ in range(5): mm.poly_mul_host(ah, bh, P, G, out=ch)
     e1.record(); torch.cuda.synchronize()
-    print(json.dumps({"chunk_mib": os.environ.get("MMNTT_HOST_CHUNK_MIB"), "ms": round(e0.elapsed_time(e1) / 5, 3)}))
+    print(json.dumps({"chunk_mib": os.environ.get("MMNTT_HOST_CHUNK_MIB"), "packed": os.environ.get("MMNTT_HOST_PACKED"),
+                      "ms": round(e0.elapsed_time(e1) / 5, 3)}))
 else:
-    for mib in (96, 128, 192):
-        env = dict(os.environ, MMNTT_HOST_CHUNK_MIB=str(mib))
+    for mib, pk in ((96, 0), (96, 1), (64, 0), (64, 1), (48, 1), (128, 1), (96, 0), (96, 1), (64, 1)):
+        env = dict(os.environ, MMNTT_HOST_CHUNK_MIB=str(mib), MMNTT_HOST_PACKED=str(pk))
         print(subprocess.run([sys.executable, __file__, "x"], env=env, capture_output=True, text=True).stdout.strip(),
               flush=True)
