@@ -1090,7 +1090,8 @@ def config_spec(which, mm, torch, dev, rank):
                  workload=f"C4: 8 forward NTTs of 2^24 over p = 2^64 - 2^32 + 1 (generator 7), four-step "
                           f"({inf['n2']} cols x {inf['n1']} rows), BITREV output",
                  fam={"ntt_cols_fwd": (2 * 8 * 8 << 24, 8 * (1 << 23) * kc),
-                      "ntt_rows_fwd": (2 * 8 * 8 << 24, 8 * (1 << 23) * kr)}, peak="gold8")
+                      "ntt_rows_fwd": (2 * 8 * 8 << 24, 8 * (1 << 23) * kr)}, peak="gold8",
+                 traffic=("r11_traffic_c4.json", {"ntt_cols_fwd": "k_gcols_fwd", "ntt_rows_fwd": "k_grows_fwd"}))
     elif which == "c5":
         n = 1 << 24
         a = gen.limbs16_torch(gen.config_seed(5), 1, n, dev, start=rank * n).view(torch.uint16)
@@ -1103,7 +1104,9 @@ def config_spec(which, mm, torch, dev, rank):
                           "over p = 2^64 - 2^32 + 1 (four-step 2^13 x 2^12), carries to 16-bit limbs",
                  fam={"ntt_cols_fwd": (2 * (2 * n + 8 * N), 2 * (1 << 24) * 12),
                       "pmul_rows_fourstep": (3 * 8 * N, 3 * (1 << 24) * 13),
-                      "ntt_cols_inv": (2 * 8 * N, (1 << 24) * 12)}, peak="gold8")
+                      "ntt_cols_inv": (2 * 8 * N, (1 << 24) * 12)}, peak="gold8",
+                 traffic=("r12_traffic_c5.json", {"ntt_cols_fwd": "k_gcols16_fwd", "pmul_rows_fourstep": "k_gpmul_rows",
+                                                  "ntt_cols_inv": "k_gcols_inv"}))
     else:
         raise SystemExit(f"unknown --config {which}")
     return s
@@ -1172,11 +1175,18 @@ def run_config(args, world, rank, local):
                 e["Gbutterfly_per_s"] = round(bf / (per * 1e-3) / 1e9, 1)
         kernels[k_] = e
     fam = max((k for k in prof if k in S["fam"]), key=lambda k: prof[k][1], default=None)
+    traffic = None     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    if fam is not None and S.get("traffic"):
+        try:
+            with open(os.path.join(ROOT, "profiles", S["traffic"][0])) as fh:
+                traffic = json.load(fh).get(S["traffic"][1].get(fam))
+        except OSError:
+            traffic = None
     if fam is not None:
         e = kernels[fam]
         if S["peak"] == "hbm":
             roof = {"bound": "hbm", "kernel": fam, "achieved": e["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
-                    "frac": e["hbm_frac"], "traffic": None, "peak_source": peak_src}
+                    "frac": e["hbm_frac"], "traffic": traffic, "peak_source": peak_src}
         else:
             pk = alu32 if S["peak"] == "alu32" else gold8
             src = (f"derived: {nsm} SMs x 16 butterflies/clk/SM (fmaheavy: IMAD.HI 4 + 2 x IMAD 2 cycles per warp) "
@@ -1185,7 +1195,8 @@ def run_config(args, world, rank, local):
                    "65; no loads, shift twiddles only: an upper bound the passes' table products cannot reach)")
             ach = e["Gbutterfly_per_s"] * 1e9
             roof = {"bound": "alu", "kernel": fam, "achieved": e["Gbutterfly_per_s"], "peak": round(pk / 1e9, 1),
-                    "unit": "Gbutterfly/s", "frac": round(ach / pk, 3), "traffic": None, "hbm_frac": e["hbm_frac"],
+                    "unit": "Gbutterfly/s", "frac": round(ach / pk, 3), "traffic": traffic, "hbm_frac": e["hbm_frac"],
+                    "algorithmic_bytes": int(S["fam"][fam][0] * args.steps / prof[fam][0]),
                     "peak_source": src}
 
     # e2e: upload the step's inputs from pinned host memory, run, read the result back
