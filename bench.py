@@ -1071,7 +1071,8 @@ def config_spec(which, mm, torch, dev, rank):
                  unit="Gelem/s", metric="modmul Gelem/s", scale=1e9, dtype="u32", flush=False, keep=(M,),
                  workload="C2: Montgomery modmul over 2^28 uint32 pairs, p = 3221225473 (Shoup, Barrett, add, sub "
                           "in config.variants)",
-                 fam={"modmul_montgomery": (12 * n, 0)}, peak="hbm")
+                 fam={"modmul_montgomery": (12 * n, 0)}, peak="hbm",
+                 traffic=("r12_traffic_c2.json", {"modmul_montgomery": "modmul_montgomery"}))
         ys = M.shoup_precompute(y)
         s["variants"] = [("modadd", lambda: M.add(x, y, out=z), 12), ("modsub", lambda: M.sub(x, y, out=z), 12),
                          ("modmul_barrett", lambda: M.mul(x, y, mm.MUL_BARRETT, out=z), 12),
@@ -1186,7 +1187,8 @@ def run_config(args, world, rank, local):
         e = kernels[fam]
         if S["peak"] == "hbm":
             roof = {"bound": "hbm", "kernel": fam, "achieved": e["GB_per_s"], "peak": hbm_peak, "unit": "GB/s",
-                    "frac": e["hbm_frac"], "traffic": traffic, "peak_source": peak_src}
+                    "frac": e["hbm_frac"], "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic_bytes": int(S["fam"][fam][0] * args.steps / prof[fam][0])}
         else:
             pk = alu32 if S["peak"] == "alu32" else gold8
             src = (f"derived: {nsm} SMs x 16 butterflies/clk/SM (fmaheavy: IMAD.HI 4 + 2 x IMAD 2 cycles per warp) "

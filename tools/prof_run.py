@@ -1,5 +1,5 @@
 """Small driver for ncu captures: one warm-up + one measured call of the
-C3 poly_mul, C4 forward and C5 int_mul paths (select with argv[1])."""
+C2 modmul, C3 poly_mul, C4 forward and C5 int_mul paths (select with argv[1])."""
 import os
 import sys
 
@@ -26,6 +26,17 @@ elif which == "c4":
     y = torch.empty_like(x)
     for _ in range(2):
         plan.forward(x, out=y, order=mm.BITREV)
+elif which == "c2":
+    n = 1 << 28
+    x = gen.residues_torch(gen.config_seed(2), 1, n, 3221225473, dev).view(torch.uint32)
+    y = gen.residues_torch(gen.config_seed(2), 2, n, 3221225473, dev).view(torch.uint32)
+    z = torch.empty_like(x)
+    M = mm.Mod32(3221225473)
+    ys = M.shoup_precompute(y)
+    for _ in range(2):
+        M.mul(x, y, mm.MUL_MONTGOMERY, out=z)
+        M.mul(x, y, mm.MUL_SHOUP, y_shoup=ys, out=z)
+        M.mul(x, y, mm.MUL_BARRETT, out=z)
 elif which == "c5":
     n = 1 << 24
     a = gen.limbs16_torch(gen.config_seed(5), 1, n, dev).view(torch.uint16)
