@@ -1308,3 +1308,20 @@ print(h.hexdigest(), bool(torch.equal(z, x)))
         outs.append(r.stdout.split()[-2:])
     assert all(o[1] == "True" for o in outs)
     assert outs[0][0] == outs[1][0] == outs[2][0]
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_bench_config_line(cfg):
+    # bench.py --config: one contract line for that BASELINE config, with the
+    # library's kernels counted inside the timed region
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--config", cfg, "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["config"]["config"] == cfg.upper() and line["value"] > 0 and line["gpu_launches"] >= 3
+    assert line["roofline"]["frac"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["clocks"]["sm_mhz"] is None or line["clocks"]["sm_mhz"] > 0
