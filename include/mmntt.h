@@ -184,6 +184,19 @@ mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, const void *a,
 mm_status mm_poly_mul_ld(int word_bits, uint64_t p, uint64_t g, const void *a, size_t la, size_t lda,
                          const void *b, size_t lb, size_t ldb, void *c, size_t ldc, size_t batch, void *stream);
 
+/* FFT_w of P:887-893 (mm_ntt_forward / mm_ntt_inverse above) with HOST input
+ * and output: in, out: [plan batch][2^log2n] elements, packed, page-locked
+ * memory for overlap; in == out is allowed.  The batch rows are cut into
+ * chunks that upload (own stream), transform (the caller's `stream`) and
+ * download (own stream) through the three library-owned device slots of
+ * mm_poly_mul_host, so both PCIe directions overlap the kernels; a plan of
+ * batch 1 is one chunk (no overlap).  Same value and order semantics as the
+ * device calls; asynchronous with respect to the host: `stream` is ordered
+ * after the last download.  Errors: MM_E_ARG (null pointer, bad order),
+ * MM_E_CUDA. */
+mm_status mm_ntt_forward_host(const mm_ntt_plan *plan, const void *in, void *out, mm_order order, void *stream);
+mm_status mm_ntt_inverse_host(const mm_ntt_plan *plan, const void *in, void *out, mm_order order, void *stream);
+
 /* ------------------------------------------------------------------------
  * Modular vectors over IEEE doubles (paper §3; SURVEY §8(f)
  * item 3): residues of an odd p < 2^50 held as integral doubles in [0, p).

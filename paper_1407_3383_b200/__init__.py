@@ -53,6 +53,8 @@ EXPORTS = {
     "mm_ntt_plan_info": (_ST, [_P, ctypes.POINTER(_u64)]),
     "mm_ntt_forward": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_ntt_inverse": (_ST, [_P, _P, _P, _i32, _P]),
+    "mm_ntt_forward_host": (_ST, [_P, _P, _P, _i32, _P]),
+    "mm_ntt_inverse_host": (_ST, [_P, _P, _P, _i32, _P]),
     "mm_poly_mul": (_ST, [_i32, _u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_mul_tft": (_ST, [_u64, _u64, _P, _sz, _P, _sz, _P, _sz, _P]),
     "mm_poly_matmul": (_ST, [_u64, _u64, _P, _P, _P, _sz, _sz, _sz, _sz, _sz, _P]),
@@ -485,6 +487,30 @@ class NttPlan:
         _need(out, x.numel(), x.element_size(), "out", x)
         _check(lib().mm_ntt_inverse(self._h, _ptr(x), _ptr(out), order, _stream(x)))
         return out
+
+    def _host(self, fn, x, out, order):
+        """HOST tensors (pinned for overlap) through the library's chunked upload /
+        transform / download pipeline; returns after the result is in `out`."""
+        if x.is_cuda:
+            raise ValueError("forward_host / inverse_host take host tensors")
+        self._chk(x)
+        if not x.is_contiguous():
+            raise ValueError("x must be contiguous")
+        if out is None:
+            out = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        if out.is_cuda or not out.is_contiguous() or out.numel() != x.numel() or out.element_size() != x.element_size():
+            raise ValueError("out must be a contiguous host tensor of x's size and element width")
+        st = torch.cuda.current_stream()
+        _check(fn(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), order,
+                  ctypes.c_void_p(st.cuda_stream)))
+        st.synchronize()
+        return out
+
+    def forward_host(self, x, out=None, order=BITREV):
+        return self._host(lib().mm_ntt_forward_host, x, out, order)
+
+    def inverse_host(self, x, out=None, order=BITREV):
+        return self._host(lib().mm_ntt_inverse_host, x, out, order)
 
     # four-step building blocks (distributed transform)
     def fwd_cols(self, x, out, col0, ncols):

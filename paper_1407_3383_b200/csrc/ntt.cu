@@ -2454,6 +2454,7 @@ struct HostPipe {
     int next = 0;            // slot of the next chunk: the rotation continues across calls
     void* buf = nullptr;
     size_t bytes = 0;
+    size_t layout = 0;       // slot size of the last call (slot k = buf + k layout)
     std::mutex mu;
 };
 static std::mutex g_pipe_mu;
@@ -2480,6 +2481,27 @@ static mm_status host_pipe(HostPipe** out) {
     return MM_OK;
 }
 
+// Three slots of slot_bytes each.  When the slot size differs from the last
+// call's, the new slots overlap other old ones, so the upload stream first
+// waits for every pending download (otherwise only for its own slot's).
+static mm_status pipe_reserve(HostPipe* H, size_t slot_bytes) {
+    if (H->bytes < 3 * slot_bytes) {
+        MM_CUDA_TRY(cudaDeviceSynchronize());
+        if (H->buf) cudaFree(H->buf);
+        H->buf = nullptr;
+        H->bytes = 0;
+        MM_CUDA_TRY(cudaMalloc(&H->buf, 3 * slot_bytes));
+        H->bytes = 3 * slot_bytes;
+        for (int i = 0; i < 3; i++) H->used[i] = false;
+        H->next = 0;
+    } else if (H->layout != slot_bytes) {
+        for (int i = 0; i < 3; i++)
+            if (H->used[i]) MM_CUDA_TRY(cudaStreamWaitEvent(H->h2d, H->freed[i], 0));
+    }
+    H->layout = slot_bytes;
+    return MM_OK;
+}
+
 extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, const void* a, size_t la, const void* b,
                                       size_t lb, void* c, size_t batch, void* stream) {
     if (!a || !b || !c) return set_err(MM_E_ARG, "null argument");
@@ -2502,16 +2524,7 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     std::lock_guard<std::mutex> lk(H->mu);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t slot_bytes = ch * per;
-    if (H->bytes < 3 * slot_bytes) {
-        MM_CUDA_TRY(cudaDeviceSynchronize());
-        if (H->buf) cudaFree(H->buf);
-        H->buf = nullptr;
-        H->bytes = 0;
-        MM_CUDA_TRY(cudaMalloc(&H->buf, 3 * slot_bytes));
-        H->bytes = 3 * slot_bytes;
-        for (int i = 0; i < 3; i++) H->used[i] = false;
-        H->next = 0;
-    }
+    if ((s = pipe_reserve(H, slot_bytes)) != MM_OK) return s;
     const size_t nch = (batch + ch - 1) / ch;
     int last = 0;
     for (size_t i = 0; i < nch; i++) {
@@ -2546,6 +2559,57 @@ extern "C" mm_status mm_poly_mul_host(int word_bits, uint64_t p, uint64_t g, con
     return MM_OK;
 }
 
+// ---- host-buffer transforms: the same three-slot pipeline over batch rows ---------
+static mm_status ntt_host(const mm_ntt_plan* plan, const void* in, void* out, mm_order order, void* stream, bool inverse) {
+    if (!plan || !in || !out) return set_err(MM_E_ARG, "null argument");
+    if (order != MM_ORDER_NATURAL && order != MM_ORDER_BITREV) return set_err(MM_E_ARG, "bad order");
+    static const size_t chunk_mib = getenv("MMNTT_HOST_CHUNK_MIB") ? (size_t)atoi(getenv("MMNTT_HOST_CHUNK_MIB")) : 96;
+    const size_t es = esize(plan->word_bits), row = (es << plan->k), batch = plan->batch;
+    size_t ch = ((chunk_mib ? chunk_mib : 96) << 20) / (2 * row);   // device traffic per chunk
+    if (ch < 1) ch = 1;
+    if (ch > batch) ch = batch;
+    HostPipe* H = nullptr;
+    mm_status s = host_pipe(&H);
+    if (s != MM_OK) return s;
+    std::lock_guard<std::mutex> lk(H->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t slot_bytes = 2 * ch * row;
+    if ((s = pipe_reserve(H, slot_bytes)) != MM_OK) return s;
+    const size_t nch = (batch + ch - 1) / ch;
+    mm_ntt_plan Q = *plan;   // the tables do not depend on the batch: a chunk runs on a copy with its row count
+    int last = 0;
+    for (size_t i = 0; i < nch; i++) {
+        const int k = (int)((H->next + i) % 3);
+        const size_t r0 = i * ch, rows = batch - r0 < ch ? batch - r0 : ch;
+        char* din = (char*)H->buf + k * slot_bytes;
+        char* dout = din + ch * row;
+        if (H->used[k]) MM_CUDA_TRY(cudaStreamWaitEvent(H->h2d, H->freed[k], 0));
+        MM_CUDA_TRY(cudaMemcpyAsync(din, (const char*)in + r0 * row, rows * row, cudaMemcpyHostToDevice, H->h2d));
+        MM_CUDA_TRY(cudaEventRecord(H->in[k], H->h2d));
+        MM_CUDA_TRY(cudaStreamWaitEvent(st, H->in[k], 0));
+        Q.batch = rows;
+        s = inverse ? mm_ntt_inverse(&Q, din, dout, order, stream) : mm_ntt_forward(&Q, din, dout, order, stream);
+        if (s != MM_OK) return s;
+        MM_CUDA_TRY(cudaEventRecord(H->done[k], st));
+        MM_CUDA_TRY(cudaStreamWaitEvent(H->d2h, H->done[k], 0));
+        MM_CUDA_TRY(cudaMemcpyAsync((char*)out + r0 * row, dout, rows * row, cudaMemcpyDeviceToHost, H->d2h));
+        MM_CUDA_TRY(cudaEventRecord(H->freed[k], H->d2h));
+        H->used[k] = true;
+        last = k;
+    }
+    H->next = (int)((H->next + nch) % 3);
+    MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
+    return MM_OK;
+}
+
+extern "C" mm_status mm_ntt_forward_host(const mm_ntt_plan* plan, const void* in, void* out, mm_order order, void* stream) {
+    return ntt_host(plan, in, out, order, stream, false);
+}
+
+extern "C" mm_status mm_ntt_inverse_host(const mm_ntt_plan* plan, const void* in, void* out, mm_order order, void* stream) {
+    return ntt_host(plan, in, out, order, stream, true);
+}
+
 extern "C" mm_status mm_set_product_streams(int n) {
     if (n < 1 || n > MAX_FORK) return set_err(MM_E_ARG, "product streams must be in [1, %d]", MAX_FORK);
     g_product_streams = n;
@@ -2578,6 +2642,7 @@ extern "C" mm_status mm_release_cached(void) {
             if (h->buf) cudaFree(h->buf);
             h->buf = nullptr;
             h->bytes = 0;
+            h->layout = 0;
             for (int i = 0; i < 3; i++) h->used[i] = false;
         }
     }

@@ -590,6 +590,70 @@ def test_poly_mul_host_back_to_back(mm, O):
         assert np.array_equal(u64(c[r].numpy()), O.poly_mul_ntt(a[r].numpy(), b[r].numpy(), p, g)), r
 
 
+def test_ntt_host_pipeline(mm, O):
+    # mm_ntt_forward_host / mm_ntt_inverse_host: host rows through the three-slot
+    # upload / transform / download pipeline.  500 rows of 2^16 (192 rows per
+    # chunk: two full chunks and a ragged one), both orders, in place on the host
+    p, k, B = P30, 16, 500
+    w = O.root_of_unity(3, k, p)
+    x = torch.from_numpy(residues(61, 1, B << k, p).reshape(B, 1 << k)).pin_memory()
+    plan = mm.NttPlan(32, p, k, w, B)
+    for order in (mm.BITREV, mm.NATURAL):
+        y = plan.forward_host(x, order=order)
+        assert torch.equal(y, plan.forward(x.to(DEV), out=torch.empty_like(x, device=DEV), order=order).cpu())
+        for r in (0, 191, 192, 383, 384, 499):
+            nat = O.ntt(u64(x[r].numpy()), w, p)
+            assert np.array_equal(u64(y[r].numpy()), nat if order == mm.NATURAL else O.to_bitrev(nat)), (order, r)
+        z = y.clone().pin_memory()
+        plan.inverse_host(z, out=z, order=order)
+        assert torch.equal(z, x), order
+    # Goldilocks, 9 rows of 2^20 (6 rows per chunk), every row against the oracle
+    k, B = 20, 9
+    w = O.root_of_unity(7, k, PG)
+    xh = residues(62, 1, B << k, PG).reshape(B, 1 << k)
+    plan64 = mm.NttPlan(64, PG, k, w, B)
+    y = plan64.forward_host(torch.from_numpy(xh).pin_memory(), order=mm.BITREV).numpy()
+    for r in range(B):
+        assert np.array_equal(u64(y[r]), O.to_bitrev(O.ntt(xh[r], w, PG))), r
+    # a single transform is one chunk
+    plan1 = mm.NttPlan(64, PG, k, w, 1)
+    y1 = plan1.forward_host(torch.from_numpy(xh[4:5].copy()), order=mm.BITREV).numpy()
+    assert np.array_equal(y1[0], y[4])
+    with pytest.raises(ValueError):
+        plan1.forward_host(dev(xh[:1]))
+
+
+def test_host_pipeline_mixed_calls(mm, O):
+    # a host product and a host transform queued back to back through the C ABI
+    # without a synchronise in between: the two calls cut the library's slots
+    # differently (the second call's uploads must wait for every pending
+    # download of the first)
+    import ctypes
+    p, g, d, B = P30, 3, 1 << 15, 450
+    a = torch.from_numpy(residues(63, 1, B * d, p).reshape(B, d)).pin_memory()
+    b = torch.from_numpy(residues(63, 2, B * d, p).reshape(B, d)).pin_memory()
+    c = torch.empty((B, 2 * d - 1), dtype=torch.uint32).pin_memory()
+    k, Bn = 12, 5000
+    w = O.root_of_unity(3, k, p)
+    x = torch.from_numpy(residues(64, 1, Bn << k, p).reshape(Bn, 1 << k)).pin_memory()
+    y = torch.empty_like(x).pin_memory()
+    plan = mm.NttPlan(32, p, k, w, Bn)
+    c.fill_(0)
+    y.fill_(0)
+    torch.cuda.synchronize()
+    L, vp = mm.lib(), ctypes.c_void_p
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        assert L.mm_poly_mul_host(32, p, g, vp(a.data_ptr()), d, vp(b.data_ptr()), d, vp(c.data_ptr()), B,
+                                  vp(st.cuda_stream)) == 0
+        assert L.mm_ntt_forward_host(plan._h, vp(x.data_ptr()), vp(y.data_ptr()), mm.BITREV, vp(st.cuda_stream)) == 0
+    st.synchronize()
+    assert torch.equal(c, mm.poly_mul(a.to(DEV), b.to(DEV), p, g).cpu())
+    assert torch.equal(y, plan.forward(x.to(DEV), out=torch.empty_like(x, device=DEV), order=mm.BITREV).cpu())
+    for r in (0, 4999):
+        assert np.array_equal(u64(y[r].numpy()), O.to_bitrev(O.ntt(u64(x[r].numpy()), w, p))), r
+
+
 @pytest.mark.parametrize("p,g", [(P30, 3), (469762049, 3)])
 def test_poly_mul_tft(mm, O, p, g):
     # Algorithm 1 with l < n (truncated rows) + inverse column TFT: products of
