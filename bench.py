@@ -1072,7 +1072,9 @@ def config_spec(which, mm, torch, dev, rank):
                  workload="C2: Montgomery modmul over 2^28 uint32 pairs, p = 3221225473 (Shoup, Barrett, add, sub "
                           "in config.variants)",
                  fam={"modmul_montgomery": (12 * n, 0)}, peak="hbm",
-                 traffic=("r12_traffic_c2.json", {"modmul_montgomery": "modmul_montgomery"}))
+                 traffic=("r12_traffic_c2.json", {"modmul_montgomery": "modmul_montgomery"}),
+                 e2e_host=(lambda hin, hout: M.op_host("mul_montgomery", hin[0], hin[1], out=hout[0]),
+                           "mm_modop_u32_host (chunked upload, REDC product, download pipelined)"))
         ys = M.shoup_precompute(y)
         s["variants"] = [("modadd", lambda: M.add(x, y, out=z), 12), ("modsub", lambda: M.sub(x, y, out=z), 12),
                          ("modmul_barrett", lambda: M.mul(x, y, mm.MUL_BARRETT, out=z), 12),

@@ -100,6 +100,20 @@ mm_status mm_shoup_precompute_u32(const mm_mod32 *ctx, const uint32_t *y, uint32
                                   void *stream);
 mm_status mm_to_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, size_t n, void *stream);
 mm_status mm_from_mont_u32(const mm_mod32 *ctx, const uint32_t *x, uint32_t *z, size_t n, void *stream);
+/* The binary operations above on HOST vectors (x, y, y_shoup, z: n packed
+ * uint32 residues in page-locked memory for overlap; z may alias x or y):
+ * the vectors are cut into chunks that upload (own stream), run the device
+ * operation (the caller's `stream`) and download (own stream) through three
+ * library-owned device slots, so both PCIe directions overlap.  Same values
+ * as mm_modadd_u32 / mm_modsub_u32 / mm_modmul_u32 of the variant; y_shoup
+ * is read for MM_OP_MUL_SHOUP only (MM_E_ARG when null).  n = 0 is a no-op.
+ * Asynchronous with respect to the host: `stream` is ordered after the last
+ * download. */
+typedef enum {
+    MM_OP_ADD = 0, MM_OP_SUB = 1, MM_OP_MUL_BARRETT = 2, MM_OP_MUL_SHOUP = 3, MM_OP_MUL_MONTGOMERY = 4
+} mm_host_op;
+mm_status mm_modop_u32_host(const mm_mod32 *ctx, mm_host_op op, const uint32_t *x, const uint32_t *y,
+                            const uint32_t *y_shoup, uint32_t *z, size_t n, void *stream);
 
 /* ------------------------------------------------------------------------
  * 64-bit modulus context (SURVEY §8(b) mm_mod64_create; BASELINE C4 / C5's

@@ -46,6 +46,7 @@ EXPORTS = {
     "mm_modsub_u32": (_ST, [_P, _P, _P, _P, _sz, _P]),
     "mm_modmul_u32": (_ST, [_P, _i32, _P, _P, _P, _P, _sz, _P]),
     "mm_shoup_precompute_u32": (_ST, [_P, _P, _P, _sz, _P]),
+    "mm_modop_u32_host": (_ST, [_P, _i32, _P, _P, _P, _P, _sz, _P]),
     "mm_to_mont_u32": (_ST, [_P, _P, _P, _sz, _P]),
     "mm_from_mont_u32": (_ST, [_P, _P, _P, _sz, _P]),
     "mm_ntt_plan_create": (_ST, [_i32, _u64, _i32, _u64, _sz, ctypes.POINTER(_P)]),
@@ -428,6 +429,25 @@ class Mod32:
         _check(lib().mm_modmul_u32(self._h, variant, _ptr(x), _ptr(y), _ptr(y_shoup), _ptr(z), x.numel(),
                                    _stream(x)))
         return z
+
+    def op_host(self, op: str, x, y, y_shoup=None, out=None):
+        """add / sub / mul_barrett / mul_shoup / mul_montgomery on HOST uint32
+        vectors (pinned for overlap) through mm_modop_u32_host's chunked upload /
+        compute / download pipeline; returns after the result is in `out`."""
+        code = {"add": 0, "sub": 1, "mul_barrett": 2, "mul_shoup": 3, "mul_montgomery": 4}[op]
+        ts = [("x", x), ("y", y)] + ([("y_shoup", y_shoup)] if code == 3 else [])
+        if out is None:
+            out = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        for nm, t in ts + [("out", out)]:
+            if t is None or t.is_cuda or not t.is_contiguous() or t.numel() != x.numel() or t.element_size() != 4:
+                raise ValueError(f"{nm} must be a contiguous host tensor of {x.numel()} 32-bit elements")
+        st = torch.cuda.current_stream()
+        vp = ctypes.c_void_p
+        _check(lib().mm_modop_u32_host(self._h, code, vp(x.data_ptr()), vp(y.data_ptr()),
+                                       vp(y_shoup.data_ptr()) if code == 3 else None, vp(out.data_ptr()), x.numel(),
+                                       vp(st.cuda_stream)))
+        st.synchronize()
+        return out
 
     def shoup_precompute(self, y, out=None):
         z = self._out(y, out)

@@ -2610,6 +2610,59 @@ extern "C" mm_status mm_ntt_inverse_host(const mm_ntt_plan* plan, const void* in
     return ntt_host(plan, in, out, order, stream, true);
 }
 
+// ---- host-buffer elementwise operations: chunks of the vectors through the same slots
+extern "C" mm_status mm_modop_u32_host(const mm_mod32* ctx, mm_host_op op, const uint32_t* x, const uint32_t* y,
+                                       const uint32_t* y_shoup, uint32_t* z, size_t n, void* stream) {
+    if (!ctx) return set_err(MM_E_ARG, "null context");
+    if (op < MM_OP_ADD || op > MM_OP_MUL_MONTGOMERY) return set_err(MM_E_ARG, "bad operation");
+    if (n == 0) return MM_OK;
+    if (!x || !y || !z) return set_err(MM_E_ARG, "null argument");
+    const bool shoup = op == MM_OP_MUL_SHOUP;
+    if (shoup && !y_shoup) return set_err(MM_E_ARG, "SHOUP needs y_shoup");
+    static const size_t chunk_mib = getenv("MMNTT_HOST_CHUNK_MIB") ? (size_t)atoi(getenv("MMNTT_HOST_CHUNK_MIB")) : 96;
+    const size_t arrays = shoup ? 4 : 3;
+    size_t ch = ((chunk_mib ? chunk_mib : 96) << 20) / (arrays * 4) & ~(size_t)3;   // elements per chunk, 16-byte multiples
+    if (ch < 4) ch = 4;
+    if (ch > n) ch = (n + 3) & ~(size_t)3;
+    HostPipe* H = nullptr;
+    mm_status s = host_pipe(&H);
+    if (s != MM_OK) return s;
+    std::lock_guard<std::mutex> lk(H->mu);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t slot_bytes = arrays * ch * 4;
+    if ((s = pipe_reserve(H, slot_bytes)) != MM_OK) return s;
+    const size_t nch = (n + ch - 1) / ch;
+    int last = 0;
+    for (size_t i = 0; i < nch; i++) {
+        const int k = (int)((H->next + i) % 3);
+        const size_t e0 = i * ch, cnt = n - e0 < ch ? n - e0 : ch;
+        uint32_t* dx = (uint32_t*)((char*)H->buf + k * slot_bytes);
+        uint32_t* dy = dx + ch;
+        uint32_t* dz = dy + ch;
+        uint32_t* dys = dz + ch;
+        if (H->used[k]) MM_CUDA_TRY(cudaStreamWaitEvent(H->h2d, H->freed[k], 0));
+        MM_CUDA_TRY(cudaMemcpyAsync(dx, x + e0, cnt * 4, cudaMemcpyHostToDevice, H->h2d));
+        MM_CUDA_TRY(cudaMemcpyAsync(dy, y + e0, cnt * 4, cudaMemcpyHostToDevice, H->h2d));
+        if (shoup) MM_CUDA_TRY(cudaMemcpyAsync(dys, y_shoup + e0, cnt * 4, cudaMemcpyHostToDevice, H->h2d));
+        MM_CUDA_TRY(cudaEventRecord(H->in[k], H->h2d));
+        MM_CUDA_TRY(cudaStreamWaitEvent(st, H->in[k], 0));
+        if (op == MM_OP_ADD) s = mm_modadd_u32(ctx, dx, dy, dz, cnt, stream);
+        else if (op == MM_OP_SUB) s = mm_modsub_u32(ctx, dx, dy, dz, cnt, stream);
+        else s = mm_modmul_u32(ctx, op == MM_OP_MUL_BARRETT ? MM_MUL_BARRETT : shoup ? MM_MUL_SHOUP : MM_MUL_MONTGOMERY,
+                               dx, dy, shoup ? dys : nullptr, dz, cnt, stream);
+        if (s != MM_OK) return s;
+        MM_CUDA_TRY(cudaEventRecord(H->done[k], st));
+        MM_CUDA_TRY(cudaStreamWaitEvent(H->d2h, H->done[k], 0));
+        MM_CUDA_TRY(cudaMemcpyAsync(z + e0, dz, cnt * 4, cudaMemcpyDeviceToHost, H->d2h));
+        MM_CUDA_TRY(cudaEventRecord(H->freed[k], H->d2h));
+        H->used[k] = true;
+        last = k;
+    }
+    H->next = (int)((H->next + nch) % 3);
+    MM_CUDA_TRY(cudaStreamWaitEvent(st, H->freed[last], 0));
+    return MM_OK;
+}
+
 extern "C" mm_status mm_set_product_streams(int n) {
     if (n < 1 || n > MAX_FORK) return set_err(MM_E_ARG, "product streams must be in [1, %d]", MAX_FORK);
     g_product_streams = n;

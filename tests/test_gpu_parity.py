@@ -590,6 +590,37 @@ def test_poly_mul_host_back_to_back(mm, O):
         assert np.array_equal(u64(c[r].numpy()), O.poly_mul_ntt(a[r].numpy(), b[r].numpy(), p, g)), r
 
 
+def test_modop_host_pipeline(mm, O):
+    # mm_modop_u32_host: 2^24 + 5 elements (three chunks of 2^23 for the
+    # three-array operations, a ragged tail), every operation against the device
+    # call and sampled against the oracle; in place on the host; empty vectors
+    p, n = 3221225473, (1 << 24) + 5
+    x = torch.from_numpy(residues(71, 1, n, p)).pin_memory()
+    y = torch.from_numpy(residues(71, 2, n, p)).pin_memory()
+    M = mm.Mod32(p)
+    xd, yd = x.to(DEV), y.to(DEV)
+    ys = M.shoup_precompute(yd).cpu().pin_memory()
+    idx = np.concatenate([np.arange(0, 64), np.arange((1 << 23) - 32, (1 << 23) + 32), np.arange(n - 64, n)])
+    xs, ysm = u64(x.numpy()[idx]), u64(y.numpy()[idx])
+    want = {"add": (M.add(xd, yd), O.vec_addmod(xs, ysm, p)), "sub": (M.sub(xd, yd), O.vec_submod(xs, ysm, p)),
+            "mul_barrett": (M.mul(xd, yd, mm.MUL_BARRETT), O.vec_mulmod(xs, ysm, p)),
+            "mul_shoup": (M.mul(xd, yd, mm.MUL_SHOUP, y_shoup=ys.to(DEV)), O.vec_mulmod(xs, ysm, p)),
+            "mul_montgomery": (M.mul(xd, yd, mm.MUL_MONTGOMERY), O.vec_montmul(xs, ysm, p, 32))}
+    for op, (zd, zo) in want.items():
+        z = M.op_host(op, x, y, y_shoup=ys)
+        assert torch.equal(z, zd.cpu()), op
+        assert np.array_equal(u64(z.numpy()[idx]), zo), op
+    z = x.clone().pin_memory()
+    M.op_host("mul_barrett", z, y, out=z)
+    assert torch.equal(z, want["mul_barrett"][0].cpu())
+    e = torch.empty(0, dtype=torch.uint32)
+    assert M.op_host("add", e, e).numel() == 0
+    with pytest.raises(ValueError):
+        M.op_host("mul_shoup", x, y)
+    with pytest.raises(ValueError):
+        M.op_host("add", xd, y)
+
+
 def test_ntt_host_pipeline(mm, O):
     # mm_ntt_forward_host / mm_ntt_inverse_host: host rows through the three-slot
     # upload / transform / download pipeline.  500 rows of 2^16 (192 rows per
