@@ -38,6 +38,35 @@ __global__ void k_bitrev_perm(const T* __restrict__ in, T* __restrict__ out, int
     }
 }
 
+// Tiled form for k >= 10.  Write j = (a : 5 bits | m : k - 10 bits | b : 5 bits);
+// its mirror is ([b] | [m] | [a]).  A tile is the 32 x 32 pairs (a, b) of one m:
+// it is read as 32 runs of 32 consecutive elements (run a at (a | m | 0)) and
+// written as 32 runs of 32 consecutive elements (run [b] at ([b] | [m] | 0)),
+// transposed through shared memory, so both sides move whole 128- / 256-byte
+// lines (the element-wise form reads one element per sector).
+template <class T>
+__global__ void __launch_bounds__(256) k_bitrev_tiled(const T* __restrict__ in, T* __restrict__ out, int k, long long batch) {
+    __shared__ T tile[32][33];
+    const int km = k - 10;
+    const long long ntiles = batch << km;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int rtx = (int)(__brev((unsigned)tx) >> 27);
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const long long b = t >> km;
+        const unsigned m = (unsigned)(t & ((1ll << km) - 1));
+        const unsigned rm = km ? __brev(m) >> (32 - km) : 0u;
+        const T* src = in + (b << k) + ((long long)m << 5) + tx;
+        T* dst = out + (b << k) + ((long long)rm << 5) + tx;
+#pragma unroll
+        for (int a = ty; a < 32; a += 8) tile[a][tx] = src[(long long)a << (k - 5)];
+        __syncthreads();
+        // out[(rb | rm | ra)] = in[([ra] | m | [rb])] = tile[[ra]][[rb]], ra = tx
+#pragma unroll
+        for (int rb = ty; rb < 32; rb += 8) dst[(long long)rb << (k - 5)] = tile[rtx][__brev((unsigned)rb) >> 27];
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- twiddle tables (device)
 __device__ __forceinline__ uint32_t dmulmod32(uint32_t a, uint32_t b, uint32_t p) {
     return (uint32_t)(((uint64_t)a * b) % p);
@@ -1357,7 +1386,10 @@ template <class T>
 static mm_status bitrev_rows(const void* in, void* out, int k, long long batch, cudaStream_t st) {
     {
         LaunchScope ls("bitrev_permute", st);
-        k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)out, k, batch);
+        // MMNTT_BITREV_TILED=0 selects the element-wise form (comparison runs)
+        static const bool tiled = !(getenv("MMNTT_BITREV_TILED") && atoi(getenv("MMNTT_BITREV_TILED")) == 0);
+        if (k >= 10 && tiled) k_bitrev_tiled<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)out, k, batch);
+        else k_bitrev_perm<T><<<num_sms() * 8, 256, 0, st>>>((const T*)in, (T*)out, k, batch);
     }
     MM_LAUNCH_CHECK();
     return MM_OK;

@@ -21,3 +21,17 @@ print(json.dumps({"fwd_bitrev": t(lambda: pl.forward(x, out=y, order=mm.BITREV))
                   "fwd_natural": t(lambda: pl.forward(x, out=y, order=mm.NATURAL)),
                   "inv_bitrev": t(lambda: pl.inverse(y, out=x, order=mm.BITREV)),
                   "inv_natural": t(lambda: pl.inverse(y, out=x, order=mm.NATURAL))}))
+# other four-step sizes (permutation pass through a pool temporary): C4 and 64 x 2^20 32-bit
+del x, y, pl
+PG = (1 << 64) - (1 << 32) + 1
+out = {}
+for name, bits, p, g, k, B in (("C4_8x2^24_u64", 64, PG, 7, 24, 8), ("64x2^20_u32", 32, P, 3, 20, 64),
+                               ("256x2^18_u64", 64, PG, 7, 18, 256)):
+    pl = mm.NttPlan(bits, p, k, pow(g, (p - 1) >> k, p), B)
+    x = gen.residues_torch(gen.config_seed(4), 1, B << k, p, dev).view(torch.uint64 if bits == 64 else torch.uint32)
+    y = torch.empty_like(x)
+    out[name] = {"fwd_bitrev": t(lambda: pl.forward(x, out=y, order=mm.BITREV), 5),
+                 "fwd_natural": t(lambda: pl.forward(x, out=y, order=mm.NATURAL), 5),
+                 "inv_natural": t(lambda: pl.inverse(y, out=x, order=mm.NATURAL), 5)}
+    del pl, x, y
+print(json.dumps(out))
