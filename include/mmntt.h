@@ -143,7 +143,7 @@ mm_status mm_modmul_u64(const mm_mod64 *ctx, const uint64_t *x, const uint64_t *
  * (32-bit) or 26 (64-bit).
  * `batch` independent transforms, rows contiguous with row stride n elements
  * (uint32 for 32-bit, uint64 for 64-bit).
- * Transforms of length <= 2^12 (2^13 for 64-bit) run as one shared-memory pass per row;
+ * Transforms of length <= 2^13 (2^12 for FP64 residues) run as one shared-memory pass per row;
  * longer ones use Algorithm 1 with l = n as a two-pass four-step
  * n = n2 x n1 (column pass + twiddle, row pass).
  * Creating a plan builds the twiddle tables on the device (one sync). */
@@ -285,7 +285,7 @@ mm_status mm_reduce_num(const mm_modnum *ctx, mm_num_variant v, const void *a, v
  * operand and for the inverse, and an inverse column TFT (van der Hoeven)
  * that rebuilds each column's lambda coefficients.  For lc just above a
  * power of two this skips about half of the padded transform's row work.
- * Products that fit one pass (lc <= 2^12), and those whose four-step split has
+ * Products that fit one pass (lc <= 2^13), and those whose four-step split has
  * columns longer than 2^10 (n = 2^24), go to mm_poly_mul: the same c. */
 mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t *a, size_t la, const uint32_t *b, size_t lb,
                           uint32_t *c, size_t batch, void *stream);
@@ -349,7 +349,7 @@ mm_status mm_int_matmul_u32(const uint32_t *A, const uint32_t *B, uint32_t *C, s
  *   in place allowed; output position i2 n1 + i1 = ahat_{[i2 n1 + i1]_k}.
  * mm_ntt_inv_rows / mm_ntt_inv_cols: the inverse steps in reverse order
  *   (inverse row TFFT, multiply by w^(-j1 [i2]); inverse column TFFT and
- *   n^-1), with the same layouts.  Plans must be four-step plans (log2n > 12)
+ *   n^-1), with the same layouts.  Plans must be four-step plans (log2n > 13)
  *   with batch = 1. */
 mm_status mm_ntt_fwd_cols(const mm_ntt_plan *plan, const void *in, void *out, size_t col0, size_t ncols,
                           void *stream);
@@ -526,7 +526,7 @@ mm_status mm_carry_chunks_apply(const uint64_t *coef, const uint64_t *halo_in, s
  *       fits `bytes`.
  *   mm_dist_p2p_status: 0, or 1 + the flag slot of a device-side wait that
  *       timed out (~20 s: a peer stopped); synchronises the device.
- * Plans: four-step (log2n > 12, 32-bit; > 13, 64-bit), batch 1, with n1 and
+ * Plans: four-step (log2n > 13), batch 1, with n1 and
  * n2 divisible by world.  Rank g of G, c1 = n1 / G, r2 = n2 / G:
  *   mm_ntt_forward_dist : local_in = [n2][c1] column block (natural input
  *       element j2 n1 + j1, j1 in [g c1, (g+1) c1)); local_out = [r2][n1] row

@@ -1329,6 +1329,15 @@ static mm_status check_modulus(int word_bits, uint64_t p, int log2n) {
     return MM_OK;
 }
 
+// longest one-pass transform: 2^13 points for 64-bit and 32-bit words (a 32 KiB
+// row tile; against the 2^6 x 2^7 split: forward 1.59 -> 1.09 ms per 2^28
+// elements, products of 4096 x 4096 coefficients 4.31 -> 2.98 ms per 2^27;
+// MMNTT_ONEPASS32_13=0 restores the split), 2^12 for FP64 residues
+static int onepass_log(int word_bits) {
+    static const bool w32 = !(getenv("MMNTT_ONEPASS32_13") && atoi(getenv("MMNTT_ONEPASS32_13")) == 0);
+    return word_bits == 64 || (word_bits == 32 && w32) ? MAX_BLOCK_LOG + 1 : MAX_BLOCK_LOG;
+}
+
 static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omega, size_t batch, mm_ntt_plan** out) {
     mm_status s = check_modulus(word_bits, p, log2n);
     if (s != MM_OK) return s;
@@ -1344,7 +1353,7 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
     P->k = log2n;
     P->batch = batch;
     // Goldilocks rows of 2^13 points run in one pass (512-thread CTAs, gold.cuh)
-    if (log2n <= (word_bits == 64 ? MAX_BLOCK_LOG + 1 : MAX_BLOCK_LOG)) {
+    if (log2n <= onepass_log(word_bits)) {
         P->k1 = log2n;
         P->k2 = 0;
     } else {
@@ -2348,7 +2357,7 @@ extern "C" mm_status mm_ntt_inverse(const mm_ntt_plan* plan, const void* in, voi
 static mm_status dist_check(const mm_ntt_plan* P, const void* in, void* out, size_t off, size_t cnt, bool cols) {
     if (!P || !in || !out) return set_err(MM_E_ARG, "null argument");
     if (P->k2 == 0) return set_err(MM_E_UNSUPPORTED_SIZE, "four-step blocks need a two-pass plan (log2n > %d)",
-                                   P->word_bits == 64 ? MAX_BLOCK_LOG + 1 : MAX_BLOCK_LOG);
+                                   onepass_log(P->word_bits));
     if (P->word_bits == 52) return set_err(MM_E_ARG, "four-step blocks are built for 32- and 64-bit plans");
     size_t lim = cols ? (1ull << P->k1) : (1ull << P->k2);
     if (cnt == 0 || off + cnt > lim) return set_err(MM_E_ARG, "block [%zu, %zu) out of range %zu", off, off + cnt, lim);
@@ -3289,7 +3298,7 @@ extern "C" mm_status mm_poly_mul_tft(uint64_t p, uint64_t g, const uint32_t* a, 
     const size_t lc = la + lb - 1;
     int k = 0;
     while ((1ull << k) < lc) k++;
-    if (k <= MAX_BLOCK_LOG) return mm_poly_mul(32, p, g, a, la, b, lb, c, batch, stream);   // one pass: nothing to truncate
+    if (k <= onepass_log(32)) return mm_poly_mul(32, p, g, a, la, b, lb, c, batch, stream);   // one pass: nothing to truncate
     mm_status s = check_modulus(32, p, k);
     if (s != MM_OK) return s;
     uint64_t omega = hpowmod(g % p, (p - 1) >> k, p);
@@ -3400,7 +3409,7 @@ extern "C" mm_status mm_run_jobs(const mm_job* jobs, int njobs, void* stream) {
         } else if (J.kind == MM_JOB_FORWARD || J.kind == MM_JOB_INVERSE || J.kind == MM_JOB_ROUNDTRIP) {
             P = J.plan;
             if (!P) return set_err(MM_E_ARG, "job %d: null plan", i);
-            if (P->word_bits != 32 || P->k2 != 0)
+            if (P->word_bits != 32 || P->k2 != 0 || P->k > MAX_BLOCK_LOG)
                 return set_err(MM_E_UNSUPPORTED_SIZE, "job %d: jobs take 32-bit single-pass plans (log2n <= %d)", i,
                                MAX_BLOCK_LOG);
             if (!J.in || (J.kind != MM_JOB_ROUNDTRIP && !J.out) || (J.kind == MM_JOB_ROUNDTRIP && !J.out2))

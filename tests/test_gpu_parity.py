@@ -590,6 +590,35 @@ def test_poly_mul_host_back_to_back(mm, O):
         assert np.array_equal(u64(c[r].numpy()), O.poly_mul_ntt(a[r].numpy(), b[r].numpy(), p, g)), r
 
 
+def test_onepass_2e13_32bit(mm, O):
+    # 32-bit transforms and products of 2^13 points run in one pass (a 32 KiB
+    # row tile): a batch spanning several tiles with a ragged tail, both orders,
+    # round trips, and ragged products whose length lands in (2^12, 2^13]
+    p, g, k, B = P30, 3, 13, 37
+    w = O.root_of_unity(g, k, p)
+    plan = mm.NttPlan(32, p, k, w, B)
+    assert plan.info()["passes"] == 1
+    x = residues(81, 1, B << k, p).reshape(B, 1 << k)
+    xt = dev(x)
+    nat = O.ntt_rows(x, w, p)
+    yb = plan.forward(xt, out=torch.empty_like(xt), order=mm.BITREV)
+    assert np.array_equal(u64(host(yb)), np.stack([O.to_bitrev(r) for r in nat]))
+    yn = plan.forward(xt, out=torch.empty_like(xt), order=mm.NATURAL)
+    assert np.array_equal(u64(host(yn)), nat)
+    assert np.array_equal(host(plan.inverse(yb, order=mm.BITREV)), x)
+    assert np.array_equal(host(plan.inverse(yn, order=mm.NATURAL)), x)
+    for la, lb, batch in ((4096, 4097, 5), (8000, 193, 3), (2049, 2049, 19), (1, 8192, 2), (4096, 1, 2)):
+        a = residues(82 + la, 1, batch * la, p).reshape(batch, la)
+        b = residues(82 + la, 2, batch * lb, p).reshape(batch, lb)
+        c = u64(host(mm.poly_mul(dev(a), dev(b), p, g)))
+        for r in range(batch):
+            assert np.array_equal(c[r], O.poly_mul_ntt(a[r], b[r], p, g)), (la, lb, r)
+    # all p - 1: every lazy range at its maximum
+    a = np.full((2, 4096), p - 1, dtype=np.uint32)
+    c = u64(host(mm.poly_mul(dev(a), dev(a), p, g)))
+    assert np.array_equal(c[0], O.poly_mul_ntt(a[0], a[0], p, g)) and np.array_equal(c[1], c[0])
+
+
 def test_modop_host_pipeline(mm, O):
     # mm_modop_u32_host: 2^24 + 5 elements (three chunks of 2^23 for the
     # three-array operations, a ragged tail), every operation against the device
