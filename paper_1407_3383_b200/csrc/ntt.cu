@@ -1367,6 +1367,14 @@ static mm_status plan_create(int word_bits, uint64_t p, int log2n, uint64_t omeg
         // on the interleaved generic tiles (2^19..2^21: 10-11 % faster than the
         // balanced split; 2^18, 2^22, 2^23 measured slower)
         if (word_bits == 64 && log2n >= 19 && log2n <= 21) k2 = log2n - 13;   // measured: tools/time_split.py
+        // 32-bit: 2^8-point columns up to 2^21 (tools/exp_split32.py, per 2^28
+        // elements: 2^18 forward 2.21 -> 1.55 ms, 2^20 2.31 -> 1.55 ms against the
+        // 2^9 / 2^10-point columns of the balanced split; 2^22 would need 2^14-point
+        // rows and keeps 2^10 x 2^12; MMNTT_SPLIT32_BALANCED=1 restores the old rule)
+        static const bool bal32 = getenv("MMNTT_SPLIT32_BALANCED") && atoi(getenv("MMNTT_SPLIT32_BALANCED")) != 0;
+        if (word_bits == 32 && log2n >= 17 && log2n <= 21 && !bal32) k2 = 8;
+        if (const char* e = getenv("MMNTT_K2_32"))   // 32-bit split experiments (tools/exp_split32.py)
+            if (word_bits == 32 && atoi(e) >= log2n - 13 && atoi(e) >= 1 && atoi(e) <= 10 && atoi(e) < log2n) k2 = atoi(e);
         if (const char* e = getenv("MMNTT_K2_64"))   // split experiments (tools/time_g.py)
             if (word_bits == 64 && atoi(e) >= log2n - 13 && atoi(e) <= 12 && atoi(e) < log2n) k2 = atoi(e);
         P->k2 = k2;
